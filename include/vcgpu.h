@@ -1,0 +1,144 @@
+/* C-ABI of the B200 component-aware branch-and-reduce vertex-cover solver.
+ *
+ * Plain pointers and sizes only.  Every entry point returns 0 on success and
+ * a nonzero code on failure, with vcg_last_error() describing it.  The
+ * library never falls back to a CPU path: without a CUDA device every
+ * compute entry point fails with VCG_ENODEV.
+ *
+ * Reference interfaces replaced (arxiv/paper_2512_18334 = python package
+ * `vcsolver`, /root/reference/pkg/src/vcsolver):
+ *   vcg_graph_create / vcg_graph_destroy  <- graph.py:69 build_csr / StaticGraph
+ *                                            (the CSR is uploaded once to HBM)
+ *   vcg_induced_subgraph                   <- graph.py:112 induced_subgraph
+ *   vcg_greedy_bound                       <- preprocess.py:348 greedy_bound,
+ *                                            oracle.py:632 greedy_cover
+ *   vcg_root_reduce                        <- preprocess.py:397 root_reduce
+ *                                            (reductions.py:110 reduce_to_fixpoint
+ *                                            + reductions.py:263 crown_reduce
+ *                                            + graph.py:112 induced_subgraph)
+ *   vcg_search                             <- engine.py:160 _Engine.run (the
+ *                                            threaded search behind solve(),
+ *                                            engine.py:561)
+ *   vcg_node_op                            <- kernels/__init__.py:38-49, the
+ *                                            per-node kernel API (pure.py /
+ *                                            _native.pyx), one node per call
+ */
+#ifndef VCGPU_H
+#define VCGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VCG_OK 0
+#define VCG_EINVAL 1
+#define VCG_ENODEV 2
+#define VCG_ECUDA 3
+#define VCG_ERESOURCE 4
+#define VCG_EPROTOCOL 5
+
+typedef struct vcg_graph vcg_graph;
+
+/* Upload a canonical CSR (offsets int64[n+1], neighbors int32[offsets[n]],
+ * sorted slices, symmetric) to the current device. */
+int vcg_graph_create(int64_t n, const int64_t* offsets, const int32_t* neighbors,
+                     vcg_graph** out);
+int vcg_graph_destroy(vcg_graph* g);
+int64_t vcg_graph_num_vertices(const vcg_graph* g);
+int64_t vcg_graph_num_edges(const vcg_graph* g);
+/* Copy the device CSR back (offsets int64[n+1], neighbors int32[2m]). */
+int vcg_graph_download(const vcg_graph* g, int64_t* offsets, int32_t* neighbors);
+
+/* Subgraph induced on keep[0..nkeep) (strictly increasing ids), built on the
+ * device by flag / scan / gather.  vertex_map == keep. */
+int vcg_induced_subgraph(const vcg_graph* g, const int64_t* keep, int64_t nkeep,
+                         vcg_graph** out);
+
+/* Max-degree greedy cover (lowest index on ties).  members may be NULL,
+ * else receives the picks in order (capacity n). */
+int vcg_greedy_bound(const vcg_graph* g, int32_t* members, int64_t* size);
+
+typedef struct {
+  int64_t n_reduced;
+  int64_t m_reduced;
+  int64_t forced_count;
+  int64_t greedy_original;
+  int64_t greedy_reduced;
+  int64_t max_degree_reduced;
+  int64_t rule_counts[4]; /* degree_one, degree_two_triangle, high_degree, crown */
+  double seconds[3];      /* device reduction, crown, compaction */
+} vcg_preprocessed;
+
+/* Root reduction (lightweight rules on the device to a joint fixpoint with
+ * the crown rule) and device compaction of the survivors.
+ * forced_out: capacity n, original ids in forcing order.
+ * vertex_map_out: capacity n, reduced id -> original id.
+ * reduced_out: new graph handle (the input handle itself is never aliased). */
+int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int has_bound, int64_t bound,
+                    vcg_preprocessed* info, int32_t* forced_out, int64_t* vertex_map_out,
+                    vcg_graph** reduced_out);
+
+typedef struct {
+  int width;                  /* 8, 16 or 32: degree-array entry width */
+  int pvc;                    /* 0: MVC, 1: PVC with budget k_red */
+  int64_t k_red;
+  int64_t best_init;          /* root ChildEntry best */
+  int best_init_achieved;
+  int use_components;
+  int use_bounds;
+  int disable_pruning;
+  int deterministic;          /* one worker, private stack only */
+  int load_balance;           /* offload through the shared worklist */
+  int workers;                /* persistent blocks; 0 = every resident slot */
+  int threads;                /* block size; 0 = chosen from n */
+  int64_t worklist_threshold; /* 0 = 2 * workers (engine.py:182) */
+  double timeout;             /* seconds; 0 = none */
+  int check_registry;         /* verify quiescence + conservation afterwards */
+} vcg_search_config;
+
+typedef struct {
+  int64_t best;               /* root scope best (reduced graph) */
+  int best_achieved;
+  int found;                  /* PVC: root best <= k_red was reached */
+  int timed_out;
+  int error;                  /* device-side error code (0 = none) */
+  int64_t tree_nodes_visited;
+  int64_t component_branches;
+  int64_t worklist_pushes;
+  int64_t worklist_pops;
+  int64_t max_stack_depth;
+  int64_t rule_counts[6];     /* degree_one, d2t, high_degree, crown, clique, cycle */
+  int64_t registry_entries;
+  int64_t registry_violations;
+  double kernel_ms;           /* device time of the search kernel (CUDA events) */
+  int workers;
+  int threads;
+} vcg_search_result;
+
+/* Run the persistent search kernel.  hist_out (nullable, capacity n+2)
+ * receives the components-per-branch histogram indexed by component count. */
+int vcg_search(const vcg_graph* g, const vcg_search_config* cfg, vcg_search_result* res,
+               int64_t* hist_out);
+
+/* One per-node kernel on the device (parity surface of vcsolver.kernels).
+ * op: 0 degree_one_pass, 1 degree_two_triangle_pass, 2 high_degree_pass,
+ *     3 reduce_fixpoint, 4 recompute_bounds, 5 select_max_degree,
+ *     6 count_live, 7 remove_vertex, 8 remove_neighbors,
+ *     9 component of vertex `v` (bfs_component result set)
+ * deg: host uint32[n] in/out.  out: host int32 (capacity 4n+4) in/out.
+ * ret: host int64[8], op-specific (same tuples as the reference). */
+int vcg_node_op(int op, int width, int64_t n, const int64_t* offsets, const int32_t* neighbors,
+                uint32_t* deg, int64_t lo, int64_t hi, int64_t budget, int64_t v, int32_t* out,
+                int64_t pos, int64_t* ret);
+
+const char* vcg_last_error(void);
+int vcg_device_count(void);
+/* Device time in ms of the last vcg_root_reduce phases etc. is in the structs. */
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VCGPU_H */

@@ -1,0 +1,30 @@
+"""B200-native component-aware branch-and-reduce vertex cover (MVC / PVC).
+
+Drop-in for the solve path of the reference package ``vcsolver``
+(arxiv/paper_2512_18334): same entry points and result format, with the
+root reduction, compaction and the whole search running as hand-written
+sm_100a CUDA kernels behind the C-ABI in ``include/vcgpu.h``.
+"""
+
+from .engine import SolveResult, SolverConfig, Stats, solve
+from .graph import StaticGraph, build_csr, induced_subgraph
+from .preprocess import Preprocessed, greedy_bound, root_reduce, select_width
+
+BACKEND = "cuda-sm_100a"
+__version__ = "0.1.0"
+
+__all__ = [
+    "BACKEND",
+    "Preprocessed",
+    "SolveResult",
+    "SolverConfig",
+    "StaticGraph",
+    "Stats",
+    "build_csr",
+    "greedy_bound",
+    "induced_subgraph",
+    "root_reduce",
+    "select_width",
+    "solve",
+    "__version__",
+]

@@ -1,0 +1,104 @@
+"""ctypes binding of the in-tree CUDA library (``_build/libvcgpu.so``).
+
+The C-ABI is declared in ``include/vcgpu.h``.  There is no fallback: if the
+library is missing the import fails loudly, and every compute call fails
+with ``VCG_ENODEV`` when no CUDA device is present.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_build", "libvcgpu.so")
+CSRC = os.path.join(_HERE, "csrc")
+
+I64 = C.c_int64
+P = C.c_void_p
+
+
+class GpuError(RuntimeError):
+    """A C-ABI call failed (bad input, no device, CUDA error, resource)."""
+
+
+class Preprocessed_t(C.Structure):
+    _fields_ = [
+        ("n_reduced", I64), ("m_reduced", I64), ("forced_count", I64),
+        ("greedy_original", I64), ("greedy_reduced", I64), ("max_degree_reduced", I64),
+        ("rule_counts", I64 * 4), ("seconds", C.c_double * 3),
+    ]
+
+
+class SearchConfig_t(C.Structure):
+    _fields_ = [
+        ("width", C.c_int), ("pvc", C.c_int), ("k_red", I64), ("best_init", I64),
+        ("best_init_achieved", C.c_int), ("use_components", C.c_int), ("use_bounds", C.c_int),
+        ("disable_pruning", C.c_int), ("deterministic", C.c_int), ("load_balance", C.c_int),
+        ("workers", C.c_int), ("threads", C.c_int), ("worklist_threshold", I64),
+        ("timeout", C.c_double), ("check_registry", C.c_int),
+    ]
+
+
+class SearchResult_t(C.Structure):
+    _fields_ = [
+        ("best", I64), ("best_achieved", C.c_int), ("found", C.c_int), ("timed_out", C.c_int),
+        ("error", C.c_int), ("tree_nodes_visited", I64), ("component_branches", I64),
+        ("worklist_pushes", I64), ("worklist_pops", I64), ("max_stack_depth", I64),
+        ("rule_counts", I64 * 6), ("registry_entries", I64), ("registry_violations", I64),
+        ("kernel_ms", C.c_double), ("workers", C.c_int), ("threads", C.c_int),
+    ]
+
+
+EXPORTS = (
+    "vcg_graph_create", "vcg_graph_destroy", "vcg_graph_num_vertices", "vcg_graph_num_edges",
+    "vcg_graph_download", "vcg_induced_subgraph", "vcg_greedy_bound", "vcg_root_reduce",
+    "vcg_search", "vcg_node_op", "vcg_last_error", "vcg_device_count",
+)
+
+
+def build(force: bool = False) -> str:
+    """Compile the library for sm_100a with nvcc (make in csrc/)."""
+    srcs = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    srcs.append(os.path.join(os.path.dirname(_HERE), "include", "vcgpu.h"))
+    stale = force or not os.path.exists(LIB_PATH) or any(
+        os.path.getmtime(s) > os.path.getmtime(LIB_PATH) for s in srcs)
+    if stale:
+        subprocess.check_call(["make", "-s", "-C", CSRC])
+    return LIB_PATH
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"CUDA library not built: {LIB_PATH} (run __graft_entry__.build() or make -C {CSRC})")
+    lib = C.CDLL(LIB_PATH)
+    lib.vcg_last_error.restype = C.c_char_p
+    lib.vcg_graph_num_vertices.restype = I64
+    lib.vcg_graph_num_edges.restype = I64
+    lib.vcg_graph_create.argtypes = [I64, P, P, C.POINTER(P)]
+    lib.vcg_graph_destroy.argtypes = [P]
+    lib.vcg_graph_num_vertices.argtypes = [P]
+    lib.vcg_graph_num_edges.argtypes = [P]
+    lib.vcg_graph_download.argtypes = [P, P, P]
+    lib.vcg_induced_subgraph.argtypes = [P, P, I64, C.POINTER(P)]
+    lib.vcg_greedy_bound.argtypes = [P, P, C.POINTER(I64)]
+    lib.vcg_root_reduce.argtypes = [P, C.c_int, C.c_int, C.c_int, I64,
+                                    C.POINTER(Preprocessed_t), P, P, C.POINTER(P)]
+    lib.vcg_search.argtypes = [P, C.POINTER(SearchConfig_t), C.POINTER(SearchResult_t), P]
+    lib.vcg_node_op.argtypes = [C.c_int, C.c_int, I64, P, P, P, I64, I64, I64, I64, P, I64, P]
+    return lib
+
+
+lib = _load()
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = lib.vcg_last_error().decode(errors="replace")
+        raise GpuError(f"vcgpu error {rc}: {msg}")
+
+
+def device_count() -> int:
+    return int(lib.vcg_device_count())

@@ -1,0 +1,807 @@
+// C-ABI implementation (include/vcgpu.h): device-resident graphs, the root
+// reduction + compaction pipeline, the search launcher and the per-node
+// kernel surface.  No CPU fallback: every compute entry point needs a device.
+#include <cub/device/device_scan.cuh>
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/vcgpu.h"
+#include "host_algos.h"
+#include "search.cuh"
+
+using namespace vcg;
+
+namespace vcg {
+template <typename T>
+__global__ void search_kernel(SearchParams P);
+__global__ void drain_kernel(SearchParams P);
+__global__ void queue_init_kernel(unsigned long long* seq, long long cap);
+}  // namespace vcg
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(VCG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+extern "C" const char* vcg_last_error(void) { return g_err.c_str(); }
+
+extern "C" int vcg_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+  return c;
+}
+
+static int need_device() {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess || c == 0) return fail(VCG_ENODEV, "no CUDA device available");
+  return 0;
+}
+
+// ------------------------------------------------------------------ graph --
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  int ensure(size_t b) {
+    if (b <= bytes && p) return 0;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    if (cudaMalloc(&p, b ? b : 16) != cudaSuccess) return fail(VCG_ERESOURCE, "cudaMalloc failed");
+    bytes = b;
+    return 0;
+  }
+  template <typename U>
+  U* as() const {
+    return (U*)p;
+  }
+};
+
+struct SearchCtx {
+  DevBuf stacks, qseq, qdata, qctl, reg, ctl, hist, gws;
+};
+
+struct vcg_graph {
+  int64_t n = 0;
+  int64_t m2 = 0;  // 2 * edges
+  std::vector<int64_t> h_off;
+  std::vector<int32_t> h_nbr;
+  DevBuf d_off;  // int32[n+1]
+  DevBuf d_nbr;  // int32[2m]
+};
+
+// search buffers are reused across graphs and solves (grown on demand)
+static SearchCtx& search_ctx() {
+  static SearchCtx* ctx = new SearchCtx();
+  return *ctx;
+}
+
+extern "C" int vcg_graph_create(int64_t n, const int64_t* offsets, const int32_t* neighbors,
+                                vcg_graph** out) {
+  if (int r = need_device()) return r;
+  if (n < 0 || !offsets || !out) return fail(VCG_EINVAL, "bad arguments");
+  int64_t m2 = offsets[n];
+  if (m2 >= (int64_t)1 << 31) return fail(VCG_EINVAL, "graph too large for int32 CSR offsets");
+  auto* g = new vcg_graph();
+  g->n = n;
+  g->m2 = m2;
+  g->h_off.assign(offsets, offsets + n + 1);
+  g->h_nbr.assign(neighbors, neighbors + m2);
+  std::vector<int32_t> off32(n + 1);
+  for (int64_t i = 0; i <= n; ++i) off32[i] = (int32_t)offsets[i];
+  if (g->d_off.ensure((n + 1) * 4) || g->d_nbr.ensure(m2 * 4 + 4)) {
+    delete g;
+    return VCG_ERESOURCE;
+  }
+  cudaMemcpy(g->d_off.p, off32.data(), (n + 1) * 4, cudaMemcpyHostToDevice);
+  if (m2) cudaMemcpy(g->d_nbr.p, neighbors, m2 * 4, cudaMemcpyHostToDevice);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    delete g;
+    return fail(VCG_ECUDA, cudaGetErrorString(e));
+  }
+  *out = g;
+  return 0;
+}
+
+extern "C" int vcg_graph_destroy(vcg_graph* g) {
+  delete g;
+  return 0;
+}
+extern "C" int64_t vcg_graph_num_vertices(const vcg_graph* g) { return g ? g->n : -1; }
+extern "C" int64_t vcg_graph_num_edges(const vcg_graph* g) { return g ? g->m2 / 2 : -1; }
+
+extern "C" int vcg_graph_download(const vcg_graph* g, int64_t* offsets, int32_t* neighbors) {
+  if (!g) return fail(VCG_EINVAL, "null graph");
+  std::vector<int32_t> off32(g->n + 1);
+  CK(cudaMemcpy(off32.data(), g->d_off.p, (g->n + 1) * 4, cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i <= g->n; ++i) offsets[i] = off32[i];
+  if (g->m2) CK(cudaMemcpy(neighbors, g->d_nbr.p, g->m2 * 4, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+// ------------------------------------------------------------ compaction --
+// graph.py:112 induced_subgraph, on the device: flag -> scan (new ids) ->
+// per-vertex surviving-neighbour counts -> scan (offsets) -> gather.
+
+__global__ void k_keep_flags(const int32_t* deg_or_null, const int64_t* keep_list, int64_t nkeep,
+                             int n, int32_t* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = deg_or_null ? (deg_or_null[i] > 0) : 0;
+  (void)keep_list;
+  (void)nkeep;
+}
+
+__global__ void k_flag_from_list(const int64_t* keep, int64_t nkeep, int32_t* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nkeep;
+       i += (int64_t)gridDim.x * blockDim.x)
+    flag[keep[i]] = 1;
+}
+
+// one warp per kept vertex: count surviving neighbours
+__global__ void k_count_kept(int n, const int32_t* off, const int32_t* nbr, const int32_t* flag,
+                             const int32_t* newid, int32_t* vmap, int32_t* cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < n; v += nwarps) {
+    if (!flag[v]) continue;
+    int c = 0;
+    for (int j = off[v] + lane; j < off[v + 1]; j += 32) c += flag[nbr[j]];
+    c = vcg::warp_sum(c);
+    if (lane == 0) {
+      cnt[newid[v]] = c;
+      vmap[newid[v]] = (int32_t)v;
+    }
+  }
+}
+
+// one warp per kept vertex: ballot-compact surviving neighbours, relabelled
+__global__ void k_gather_kept(int n, const int32_t* off, const int32_t* nbr, const int32_t* flag,
+                              const int32_t* newid, const int32_t* noff, int32_t* nnbr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < n; v += nwarps) {
+    if (!flag[v]) continue;
+    int at = noff[newid[v]];
+    for (int base = off[v]; base < off[v + 1]; base += 32) {
+      int j = base + lane;
+      int x = -1;
+      bool keep = false;
+      if (j < off[v + 1]) {
+        x = nbr[j];
+        keep = flag[x] != 0;
+      }
+      unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (keep) nnbr[at + __popc(m & ((1u << lane) - 1))] = newid[x];
+      at += __popc(m);
+    }
+  }
+}
+
+static int exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t count, DevBuf& tmp) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int)count);
+  if (tmp.ensure(bytes)) return VCG_ERESOURCE;
+  CK(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, (int)count));
+  return 0;
+}
+
+// Builds the induced subgraph of the vertices with flag[v] != 0 (device).
+static int compact_flagged(const vcg_graph* g, DevBuf& flag, vcg_graph** out,
+                           std::vector<int64_t>* vmap_host) {
+  const int n = (int)g->n;
+  DevBuf newid, cnt, noff, vmap, tmp;
+  if (newid.ensure((size_t)(n + 1) * 4) || cnt.ensure((size_t)(n + 1) * 4) ||
+      vmap.ensure((size_t)(n + 1) * 4))
+    return VCG_ERESOURCE;
+  if (int r = exclusive_scan_i32(flag.as<int32_t>(), newid.as<int32_t>(), n + 1, tmp)) return r;
+  int32_t nk = 0;
+  CK(cudaMemcpy(&nk, newid.as<int32_t>() + n, 4, cudaMemcpyDeviceToHost));
+  const int threads = 256;
+  const int blocks = (int)std::min<int64_t>(((int64_t)n * 32 + threads - 1) / threads, 148 * 16);
+  CK(cudaMemset(cnt.p, 0, (size_t)(nk + 1) * 4));
+  if (n) {
+    k_count_kept<<<blocks > 0 ? blocks : 1, threads>>>(n, g->d_off.as<int32_t>(),
+                                                       g->d_nbr.as<int32_t>(), flag.as<int32_t>(),
+                                                       newid.as<int32_t>(), vmap.as<int32_t>(),
+                                                       cnt.as<int32_t>());
+    CK(cudaGetLastError());
+  }
+  auto* r = new vcg_graph();
+  r->n = nk;
+  if (r->d_off.ensure((size_t)(nk + 1) * 4)) {
+    delete r;
+    return VCG_ERESOURCE;
+  }
+  if (int e = exclusive_scan_i32(cnt.as<int32_t>(), r->d_off.as<int32_t>(), nk + 1, tmp)) {
+    delete r;
+    return e;
+  }
+  int32_t m2 = 0;
+  CK(cudaMemcpy(&m2, r->d_off.as<int32_t>() + nk, 4, cudaMemcpyDeviceToHost));
+  r->m2 = m2;
+  if (r->d_nbr.ensure((size_t)m2 * 4 + 4)) {
+    delete r;
+    return VCG_ERESOURCE;
+  }
+  if (n && nk) {
+    k_gather_kept<<<blocks > 0 ? blocks : 1, threads>>>(
+        n, g->d_off.as<int32_t>(), g->d_nbr.as<int32_t>(), flag.as<int32_t>(),
+        newid.as<int32_t>(), r->d_off.as<int32_t>(), r->d_nbr.as<int32_t>());
+    CK(cudaGetLastError());
+  }
+  // host mirror of the compacted CSR (the reference's StaticGraph is host data)
+  std::vector<int32_t> off32(nk + 1), vm(nk);
+  CK(cudaMemcpy(off32.data(), r->d_off.p, (size_t)(nk + 1) * 4, cudaMemcpyDeviceToHost));
+  r->h_off.resize(nk + 1);
+  for (int i = 0; i <= nk; ++i) r->h_off[i] = off32[i];
+  r->h_nbr.resize(m2);
+  if (m2) CK(cudaMemcpy(r->h_nbr.data(), r->d_nbr.p, (size_t)m2 * 4, cudaMemcpyDeviceToHost));
+  if (nk) CK(cudaMemcpy(vm.data(), vmap.p, (size_t)nk * 4, cudaMemcpyDeviceToHost));
+  if (vmap_host) vmap_host->assign(vm.begin(), vm.end());
+  *out = r;
+  return 0;
+}
+
+extern "C" int vcg_induced_subgraph(const vcg_graph* g, const int64_t* keep, int64_t nkeep,
+                                    vcg_graph** out) {
+  if (!g || (nkeep && !keep)) return fail(VCG_EINVAL, "bad arguments");
+  for (int64_t i = 0; i < nkeep; ++i)
+    if (keep[i] < 0 || keep[i] >= g->n || (i && keep[i] <= keep[i - 1]))
+      return fail(VCG_EINVAL, "keep must be strictly increasing vertex ids in range");
+  DevBuf flag, dkeep;
+  if (flag.ensure((size_t)(g->n + 1) * 4) || dkeep.ensure((size_t)nkeep * 8 + 8))
+    return VCG_ERESOURCE;
+  CK(cudaMemset(flag.p, 0, (size_t)(g->n + 1) * 4));
+  if (nkeep) {
+    CK(cudaMemcpy(dkeep.p, keep, nkeep * 8, cudaMemcpyHostToDevice));
+    k_flag_from_list<<<(int)std::min<int64_t>((nkeep + 255) / 256, 4096), 256>>>(
+        dkeep.as<int64_t>(), nkeep, flag.as<int32_t>());
+    CK(cudaGetLastError());
+  }
+  return compact_flagged(g, flag, out, nullptr);
+}
+
+extern "C" int vcg_greedy_bound(const vcg_graph* g, int32_t* members, int64_t* size) {
+  if (!g || !size) return fail(VCG_EINVAL, "bad arguments");
+  *size = greedy_cover_host(g->n, g->h_off.data(), g->h_nbr.data(), members);
+  return 0;
+}
+
+// ------------------------------------------------------- node workspaces --
+
+template <typename T>
+static long long ws_total(int n) {
+  return ws_bytes<T>(n);
+}
+
+// single-block kernel running one per-node operation on a global workspace
+template <typename T>
+__global__ void k_node_op(int op, int n, const int32_t* off, const int32_t* nbr, T* deg_io,
+                          char* wsmem, int lo, int hi, int budget, int v, int32_t* out, int pos,
+                          long long* ret) {
+  __shared__ BlockScratch bs;
+  NodeWs<T> w = carve_ws<T>(wsmem, n, &bs, off, nbr);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    w.deg[i] = deg_io[i];
+    w.tmin[i] = kInf;
+    w.flag[i] = 0;
+  }
+  __syncthreads();
+  long long r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (op == 0 || op == 1 || op == 2) {
+    PassRet pr = op == 0   ? degree_one_pass(w, lo, hi, out, pos)
+                 : op == 1 ? degree_two_triangle_pass(w, lo, hi, out, pos)
+                           : high_degree_pass(w, lo, hi, budget, out, pos);
+    r[0] = pr.applied;
+    r[1] = pr.forced;
+    r[2] = pr.edges;
+    r[3] = pr.pos;
+  } else if (op == 3) {
+    FixRet f = reduce_fixpoint(w, lo, hi, budget, out, pos);
+    r[0] = f.forced;
+    r[1] = f.d1;
+    r[2] = f.d2t;
+    r[3] = f.hd;
+    r[4] = f.edges;
+    r[5] = f.lo;
+    r[6] = f.hi;
+    r[7] = f.pos;
+  } else if (op == 4) {
+    int l = lo, h = hi;
+    recompute_bounds(w, &l, &h);
+    r[0] = l;
+    r[1] = h;
+  } else if (op == 5) {
+    r[0] = select_max_degree(w, lo, hi);
+  } else if (op == 6) {
+    r[0] = count_live(w, lo, hi);
+  } else if (op == 7) {
+    r[0] = remove_vertex(w, v);
+  } else if (op == 8) {
+    int removed, edges;
+    remove_neighbors(w, v, out, pos, &removed, &edges);
+    r[0] = removed;
+    r[1] = edges;
+    r[2] = pos + removed;
+  } else if (op == 9) {
+    // component of v among live vertices of [lo, hi]
+    int nc = label_components(w, lo, hi);
+    (void)nc;
+    int root = w.ia[v];
+    int size = 0, dsum = 0, mn = kInf, mx = 0, vmn = kInf, vmx = -1;
+    for (int x = lo + threadIdx.x; x <= hi; x += blockDim.x) {
+      int d = w.deg[x];
+      if (d > 0 && w.ia[x] == root) {
+        ++size;
+        dsum += d;
+        mn = min(mn, d);
+        mx = max(mx, d);
+        vmn = min(vmn, x);
+        vmx = max(vmx, x);
+      }
+    }
+    size = block_sum(size, w.bs);
+    dsum = block_sum(dsum, w.bs);
+    mn = block_min(mn, w.bs);
+    mx = block_max(mx, w.bs);
+    vmn = block_min(vmn, w.bs);
+    vmx = block_max(vmx, w.bs);
+    r[0] = size;
+    r[1] = dsum;
+    r[2] = mn;
+    r[3] = mx;
+    r[4] = vmn;
+    r[5] = vmx;
+    // members in index order
+    if (threadIdx.x == 0) {
+      int k = 0;
+      for (int x = lo; x <= hi; ++x)
+        if (w.deg[x] > 0 && w.ia[x] == root) out[k++] = x;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) deg_io[i] = w.deg[i];
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 8; ++i) ret[i] = r[i];
+}
+
+template <typename T>
+static int node_op_t(int op, int64_t n, const int64_t* offsets, const int32_t* neighbors,
+                     uint32_t* deg, int64_t lo, int64_t hi, int64_t budget, int64_t v,
+                     int32_t* out, int64_t pos, int64_t* ret) {
+  const int64_t m2 = offsets[n];
+  std::vector<int32_t> off32(n + 1);
+  for (int64_t i = 0; i <= n; ++i) off32[i] = (int32_t)offsets[i];
+  std::vector<T> degt(n > 0 ? n : 1);
+  for (int64_t i = 0; i < n; ++i) degt[i] = (T)deg[i];
+  const int64_t ocap = 4 * n + 4;
+  DevBuf doff, dnbr, ddeg, dws, dout, dret;
+  if (doff.ensure((n + 1) * 4) || dnbr.ensure(m2 * 4 + 4) || ddeg.ensure(deg_bytes<T>((int)n) + 16) ||
+      dws.ensure(ws_total<T>((int)n)) || dout.ensure(ocap * 4) || dret.ensure(64))
+    return VCG_ERESOURCE;
+  CK(cudaMemcpy(doff.p, off32.data(), (n + 1) * 4, cudaMemcpyHostToDevice));
+  if (m2) CK(cudaMemcpy(dnbr.p, neighbors, m2 * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ddeg.p, degt.data(), n * sizeof(T), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dout.p, out, ocap * 4, cudaMemcpyHostToDevice));
+  k_node_op<T><<<1, 128>>>(op, (int)n, doff.as<int32_t>(), dnbr.as<int32_t>(), ddeg.as<T>(),
+                           dws.as<char>(), (int)lo, (int)hi, (int)budget, (int)v,
+                           dout.as<int32_t>(), (int)pos, dret.as<long long>());
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(degt.data(), ddeg.p, n * sizeof(T), cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < n; ++i) deg[i] = degt[i];
+  CK(cudaMemcpy(out, dout.p, ocap * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(ret, dret.p, 64, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+extern "C" int vcg_node_op(int op, int width, int64_t n, const int64_t* offsets,
+                           const int32_t* neighbors, uint32_t* deg, int64_t lo, int64_t hi,
+                           int64_t budget, int64_t v, int32_t* out, int64_t pos, int64_t* ret) {
+  if (int r = need_device()) return r;
+  if (n <= 0 || op < 0 || op > 9) return fail(VCG_EINVAL, "bad node op arguments");
+  if (width == 8) return node_op_t<uint8_t>(op, n, offsets, neighbors, deg, lo, hi, budget, v, out, pos, ret);
+  if (width == 16) return node_op_t<uint16_t>(op, n, offsets, neighbors, deg, lo, hi, budget, v, out, pos, ret);
+  if (width == 32) return node_op_t<uint32_t>(op, n, offsets, neighbors, deg, lo, hi, budget, v, out, pos, ret);
+  return fail(VCG_EINVAL, "width must be 8, 16 or 32");
+}
+
+// -------------------------------------------------------- root reduction --
+
+// One block reduces the whole graph to the lightweight-rule fixpoint on a
+// global-memory workspace (deg int32).  ret: forced, d1, d2t, hd, edges, lo, hi, pos
+__global__ void k_root_fixpoint(int n, const int32_t* off, const int32_t* nbr, char* wsmem,
+                                int lo, int hi, int budget, int32_t* out, int pos, long long* ret,
+                                int init) {
+  __shared__ BlockScratch bs;
+  NodeWs<uint32_t> w = carve_ws<uint32_t>(wsmem, n, &bs, off, nbr);
+  if (init) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      w.deg[i] = (uint32_t)(off[i + 1] - off[i]);
+      w.tmin[i] = kInf;
+      w.flag[i] = 0;
+    }
+  }
+  __syncthreads();
+  FixRet f = reduce_fixpoint(w, lo, hi, budget, out, pos);
+  if (threadIdx.x == 0) {
+    ret[0] = f.forced;
+    ret[1] = f.d1;
+    ret[2] = f.d2t;
+    ret[3] = f.hd;
+    ret[4] = f.edges;
+    ret[5] = f.lo;
+    ret[6] = f.hi;
+    ret[7] = f.pos;
+  }
+}
+
+__global__ void k_flags_from_deg(const uint32_t* deg, int n, int32_t* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = (i < n) ? (deg[i] > 0) : 0;
+}
+
+extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int has_bound,
+                               int64_t bound, vcg_preprocessed* info, int32_t* forced_out,
+                               int64_t* vertex_map_out, vcg_graph** reduced_out) {
+  if (int r = need_device()) return r;
+  if (!g || !info || !reduced_out) return fail(VCG_EINVAL, "bad arguments");
+  memset(info, 0, sizeof(*info));
+  const int n = (int)g->n;
+  info->greedy_original = greedy_cover_host(g->n, g->h_off.data(), g->h_nbr.data(), nullptr);
+  const int64_t bound0 = has_bound ? bound : info->greedy_original;
+  DevBuf flag;
+  if (flag.ensure((size_t)(n + 1) * 4)) return VCG_ERESOURCE;
+  std::vector<int64_t> vmap;
+  int64_t forced_count = 0;
+  if (!enabled) {
+    std::vector<int32_t> ones(n + 1, 1);
+    ones[n] = 0;
+    CK(cudaMemcpy(flag.p, ones.data(), (size_t)(n + 1) * 4, cudaMemcpyHostToDevice));
+  } else {
+    DevBuf ws, dout, dret;
+    if (ws.ensure(ws_total<uint32_t>(n)) || dout.ensure((size_t)(2 * n + 4) * 4) ||
+        dret.ensure(64))
+      return VCG_ERESOURCE;
+    NodeWs<uint32_t> layout = {};
+    (void)layout;
+    int lo = 0, hi = n - 1;
+    {
+      int l = -1, h = -1;
+      for (int v = 0; v < n; ++v)
+        if (g->h_off[v + 1] > g->h_off[v]) {
+          if (l < 0) l = v;
+          h = v;
+        }
+      if (l < 0 || g->m2 == 0) {
+        lo = n > 1 ? n : 1;
+        hi = 0;
+      } else {
+        lo = l;
+        hi = h;
+      }
+    }
+    std::vector<int32_t> hdeg(n);
+    int first = 1;
+    int pos = 0;
+    std::vector<int32_t> forced;
+    while (true) {
+      int64_t progressed = 0;
+      auto t0 = std::chrono::steady_clock::now();
+      long long ret[8];
+      k_root_fixpoint<<<1, 1024>>>(n, g->d_off.as<int32_t>(), g->d_nbr.as<int32_t>(),
+                                   ws.as<char>(), lo, hi, (int)(bound0 - forced_count),
+                                   dout.as<int32_t>(), 0, dret.as<long long>(), first);
+      CK(cudaGetLastError());
+      CK(cudaMemcpy(ret, dret.p, 64, cudaMemcpyDeviceToHost));
+      first = 0;
+      if (ret[7] > 0) {
+        size_t old = forced.size();
+        forced.resize(old + ret[7]);
+        CK(cudaMemcpy(forced.data() + old, dout.p, (size_t)ret[7] * 4, cudaMemcpyDeviceToHost));
+      }
+      info->rule_counts[0] += ret[1];
+      info->rule_counts[1] += ret[2];
+      info->rule_counts[2] += ret[3];
+      forced_count += ret[0];
+      progressed += ret[0];
+      lo = (int)ret[5];
+      hi = (int)ret[6];
+      info->seconds[0] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (has_bound && forced_count > bound) break;
+      if (crown) {
+        auto t1 = std::chrono::steady_clock::now();
+        CK(cudaMemcpy(hdeg.data(), ws.p, (size_t)n * 4, cudaMemcpyDeviceToHost));
+        std::vector<int32_t> heads;
+        int64_t er = 0;
+        int64_t nh = crown_reduce_host(n, g->h_off.data(), g->h_nbr.data(), hdeg.data(), lo, hi,
+                                       &heads, &er);
+        if (nh > 0) {
+          info->rule_counts[3] += 1;
+          forced.insert(forced.end(), heads.begin(), heads.end());
+          forced_count += nh;
+          progressed += nh;
+          CK(cudaMemcpy(ws.p, hdeg.data(), (size_t)n * 4, cudaMemcpyHostToDevice));
+          int l = -1, h = -1;
+          for (int v = lo; v <= hi; ++v)
+            if (hdeg[v] > 0) {
+              if (l < 0) l = v;
+              h = v;
+            }
+          if (l < 0) {
+            lo = n > 1 ? n : 1;
+            hi = 0;
+          } else {
+            lo = l;
+            hi = h;
+          }
+        }
+        info->seconds[1] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+      }
+      if (progressed == 0) break;
+    }
+    (void)pos;
+    if (forced_out)
+      for (size_t i = 0; i < forced.size(); ++i) forced_out[i] = forced[i];
+    k_flags_from_deg<<<(n + 256) / 256 + 1, 256>>>(ws.as<uint32_t>(), n, flag.as<int32_t>());
+    CK(cudaGetLastError());
+  }
+  auto t2 = std::chrono::steady_clock::now();
+  vcg_graph* red = nullptr;
+  if (int r = compact_flagged(g, flag, &red, &vmap)) return r;
+  info->seconds[2] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t2).count();
+  info->forced_count = forced_count;
+  info->n_reduced = red->n;
+  info->m_reduced = red->m2 / 2;
+  int64_t md = 0;
+  for (int64_t v = 0; v < red->n; ++v) md = std::max<int64_t>(md, red->h_off[v + 1] - red->h_off[v]);
+  info->max_degree_reduced = md;
+  info->greedy_reduced = greedy_cover_host(red->n, red->h_off.data(), red->h_nbr.data(), nullptr);
+  if (vertex_map_out)
+    for (size_t i = 0; i < vmap.size(); ++i) vertex_map_out[i] = vmap[i];
+  *reduced_out = red;
+  return 0;
+}
+
+// ----------------------------------------------------------------- search --
+
+__global__ void k_read_timer(unsigned long long* t) { *t = globaltimer(); }
+
+template <typename T>
+static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_search_result* res,
+                    int64_t* hist_out) {
+  vcg_graph* g = const_cast<vcg_graph*>(gc);
+  SearchCtx& C = search_ctx();
+  const int n = (int)g->n;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev));
+
+  int threads = cfg->threads;
+  if (threads <= 0) threads = n <= 512 ? 64 : n <= 4096 ? 128 : n <= 32768 ? 256 : 512;
+  const long long wsb = ws_total<T>(n);
+  const long long smem_limit = (long long)prop.sharedMemPerBlockOptin - 2048;
+  const int in_smem = wsb <= smem_limit;
+  const size_t dsmem = in_smem ? (size_t)wsb : 0;
+  CK(cudaFuncSetAttribute(search_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)dsmem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, search_kernel<T>, threads, dsmem));
+  if (per_sm < 1) return fail(VCG_ERESOURCE, "search kernel does not fit on an SM");
+  const int resident = per_sm * prop.multiProcessorCount;
+  int blocks = cfg->deterministic ? 1 : (cfg->workers > 0 ? cfg->workers : resident);
+  if (blocks > resident) blocks = resident;
+
+  const long long slot = (long long)sizeof(NodeHdr) + deg_bytes<T>(n);
+  // private stack: depth <= n + 1 (SPEC preprocess: stack bound), capped by memory
+  long long stack_cap = (long long)n + 2;
+  const long long stack_budget = 16LL << 30;
+  if (stack_cap * slot * blocks > stack_budget) stack_cap = std::max(16LL, stack_budget / (slot * blocks));
+  const int share = cfg->load_balance && !cfg->deterministic;
+  long long threshold = cfg->worklist_threshold > 0 ? cfg->worklist_threshold : 2LL * blocks;
+  long long qcap = std::max<long long>(4 * threshold + 1024, 4096);
+  const long long q_budget = 8LL << 30;
+  if (qcap * slot > q_budget) qcap = std::max(threshold + 64, q_budget / slot);
+  const int reg_cap = (int)std::min<long long>(1LL << 23, std::max<long long>(1LL << 16, (long long)n * 1024));
+
+  if (C.stacks.ensure((size_t)(stack_cap * slot * blocks)) || C.qseq.ensure((size_t)qcap * 8) ||
+      C.qdata.ensure((size_t)(qcap * slot)) || C.qctl.ensure(64) ||
+      C.reg.ensure((size_t)reg_cap * 4 * 12 + 64) || C.ctl.ensure(sizeof(Ctl)) ||
+      C.hist.ensure((size_t)(n + 2) * 8) ||
+      (!in_smem && C.gws.ensure((size_t)(wsb * blocks))))
+    return VCG_ERESOURCE;
+
+  SearchParams P;
+  memset(&P, 0, sizeof(P));
+  P.n = n;
+  P.off = g->d_off.as<int32_t>();
+  P.nbr = g->d_nbr.as<int32_t>();
+  P.stacks = C.stacks.as<char>();
+  P.stack_cap = stack_cap;
+  P.slot_bytes = slot;
+  P.q.seq = C.qseq.as<unsigned long long>();
+  P.q.head = C.qctl.as<unsigned long long>();
+  P.q.tail = C.qctl.as<unsigned long long>() + 1;
+  P.q.data = C.qdata.as<char>();
+  P.q.cap = qcap;
+  int* rb = C.reg.as<int>();
+  Registry& R = P.reg;
+  R.key = rb;
+  R.live = rb + reg_cap;
+  R.link = rb + 2 * reg_cap;
+  R.kind = rb + 3 * reg_cap;
+  R.sum = rb + 4 * reg_cap;
+  R.sum_ach = rb + 5 * reg_cap;
+  R.init_sum = rb + 6 * reg_cap;
+  R.folded = rb + 7 * reg_cap;
+  R.first_child = rb + 8 * reg_cap;
+  R.nchild = rb + 9 * reg_cap;
+  R.disc_done = rb + 10 * reg_cap;
+  R.child_folded = rb + 11 * reg_cap;
+  R.count = rb + 12 * reg_cap;
+  R.cap = reg_cap;
+  P.ctl = C.ctl.as<Ctl>();
+  P.hist = C.hist.as<unsigned long long>();
+  P.gws = C.gws.as<char>();
+  P.gws_bytes = wsb;
+  P.ws_in_smem = in_smem;
+  P.share = share;
+  P.threshold = threshold;
+  P.use_components = cfg->use_components;
+  P.use_bounds = cfg->use_bounds;
+  P.disable_pruning = cfg->disable_pruning;
+  P.pvc = cfg->pvc;
+  P.k_red = (int)cfg->k_red;
+  P.root_index = 0;
+  P.root_in_stack = 1;
+
+  // root scope entry + root node record (engine.py:183-188)
+  int root_fields[12] = {0};
+  root_fields[0] = (int)(cfg->best_init * 2 + (cfg->best_init_achieved ? 0 : 1));  // key
+  root_fields[1] = 1;    // live
+  root_fields[2] = -1;   // link
+  for (int f = 0; f < 12; ++f) CK(cudaMemcpy(rb + (size_t)f * reg_cap, &root_fields[f], 4, cudaMemcpyHostToDevice));
+  int one = 1;
+  CK(cudaMemcpy(R.count, &one, 4, cudaMemcpyHostToDevice));
+  std::vector<char> rec(slot, 0);
+  NodeHdr* hh = (NodeHdr*)rec.data();
+  T* rdeg = (T*)(rec.data() + sizeof(NodeHdr));
+  int lo = -1, hi = -1;
+  for (int v = 0; v < n; ++v) {
+    int64_t d = g->h_off[v + 1] - g->h_off[v];
+    rdeg[v] = (T)d;
+    if (d) {
+      if (lo < 0) lo = v;
+      hi = v;
+    }
+  }
+  if (lo < 0 || g->m2 == 0) {
+    lo = n > 1 ? n : 1;
+    hi = 0;
+  }
+  hh->S = 0;
+  hh->E = (int)(g->m2 / 2);
+  hh->lo = lo;
+  hh->hi = hi;
+  hh->scope = 0;
+  hh->depth = 0;
+  CK(cudaMemcpy(C.stacks.p, rec.data(), slot, cudaMemcpyHostToDevice));
+  CK(cudaMemset(C.qctl.p, 0, 64));
+  CK(cudaMemset(C.ctl.p, 0, sizeof(Ctl)));
+  CK(cudaMemset(C.hist.p, 0, (size_t)(n + 2) * 8));
+  queue_init_kernel<<<256, 256>>>(P.q.seq, qcap);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  double limit = cfg->timeout;
+  if (limit <= 0) {
+    // safety watchdog for test/bench runs: a protocol bug must not hang the GPU
+    const char* wd = getenv("VCG_WATCHDOG_S");
+    if (wd) limit = atof(wd);
+  }
+  if (limit > 0) {
+    // %globaltimer is ns since an arbitrary epoch: read it on the device
+    unsigned long long now = 0;
+    DevBuf t;
+    if (t.ensure(8)) return VCG_ERESOURCE;
+    k_read_timer<<<1, 1>>>(t.as<unsigned long long>());
+    CK(cudaMemcpy(&now, t.p, 8, cudaMemcpyDeviceToHost));
+    P.deadline_ns = now + (unsigned long long)(limit * 1e9);
+  }
+
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  search_kernel<T><<<blocks, threads, dsmem>>>(P);
+  cudaEventRecord(e1);
+  cudaError_t le = cudaGetLastError();
+  if (le != cudaSuccess) return fail(VCG_ECUDA, std::string("search launch: ") + cudaGetErrorString(le));
+  drain_kernel<<<1, 32>>>(P);
+  CK(cudaDeviceSynchronize());
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+
+  Ctl ctl;
+  CK(cudaMemcpy(&ctl, C.ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost));
+  int root_key = 0, count = 0;
+  CK(cudaMemcpy(&root_key, R.key, 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&count, R.count, 4, cudaMemcpyDeviceToHost));
+  memset(res, 0, sizeof(*res));
+  res->best = root_key >> 1;
+  res->best_achieved = !(root_key & 1);
+  res->found = ctl.found;
+  res->timed_out = ctl.timed_out;
+  res->error = ctl.error;
+  res->tree_nodes_visited = (int64_t)ctl.nodes;
+  res->component_branches = (int64_t)ctl.comp_branches;
+  res->worklist_pushes = (int64_t)ctl.pushes;
+  res->worklist_pops = (int64_t)ctl.pops;
+  res->max_stack_depth = ctl.max_depth;
+  for (int i = 0; i < 6; ++i) res->rule_counts[i] = (int64_t)ctl.rules[i];
+  res->registry_entries = count;
+  res->kernel_ms = ms;
+  res->workers = blocks;
+  res->threads = threads;
+  if (hist_out) {
+    std::vector<unsigned long long> h(n + 2);
+    CK(cudaMemcpy(h.data(), C.hist.p, (size_t)(n + 2) * 8, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n + 2; ++i) hist_out[i] = (int64_t)h[i];
+  }
+  if (cfg->check_registry && count > 0) {
+    // registry quiescence + conservation (SPEC registry invariants)
+    std::vector<int> f[12];
+    for (int k = 0; k < 12; ++k) {
+      f[k].resize(count);
+      CK(cudaMemcpy(f[k].data(), rb + (size_t)k * reg_cap, (size_t)count * 4, cudaMemcpyDeviceToHost));
+    }
+    int64_t bad = 0;
+    for (int i = 0; i < count; ++i) {
+      if (f[1][i] != 0) ++bad;  // live counters quiesced
+      if (f[3][i] == 1) {
+        long long expect = (long long)f[6][i] + f[7][i];
+        for (int c = f[8][i]; c < f[8][i] + f[9][i]; ++c) expect += f[0][c] >> 1;
+        if (expect != f[4][i]) ++bad;
+      }
+    }
+    res->registry_violations = bad;
+  }
+  return 0;
+}
+
+extern "C" int vcg_search(const vcg_graph* g, const vcg_search_config* cfg, vcg_search_result* res,
+                          int64_t* hist_out) {
+  if (int r = need_device()) return r;
+  if (!g || !cfg || !res) return fail(VCG_EINVAL, "bad arguments");
+  if (g->n == 0 || g->m2 == 0) return fail(VCG_EINVAL, "search needs a graph with edges");
+  if (cfg->width == 8) return search_t<uint8_t>(g, cfg, res, hist_out);
+  if (cfg->width == 16) return search_t<uint16_t>(g, cfg, res, hist_out);
+  if (cfg->width == 32) return search_t<uint32_t>(g, cfg, res, hist_out);
+  return fail(VCG_EINVAL, "width must be 8, 16 or 32");
+}

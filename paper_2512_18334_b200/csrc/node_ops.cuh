@@ -1,0 +1,718 @@
+// Block-level operations on one search-tree node's degree array.
+//
+// One thread block owns one search node at a time (north star (2)); every
+// function here is called by ALL threads of the block with block-uniform
+// arguments and returns block-uniform results.  The degree array lives in
+// shared memory when it fits (generic pointers, so the same code also runs on
+// a global-memory workspace for very large reduced graphs).
+//
+// Semantics are those of the reference's sequential kernels
+// (vcsolver/kernels/pure.py) -- same forced sets, same `out` order, same
+// returned counters -- obtained with parallel formulations that are exact,
+// not approximate:
+//
+// * degree-one sweep (pure.py:82-110): a snapshot candidate v (deg 1, unique
+//   live neighbour u(v)) applies iff it is the lowest-index candidate
+//   targeting u(v) and is not the higher end of an isolated edge whose lower
+//   end is also a candidate.  (v can only lose its degree through u(v), so
+//   this closed form equals the in-order sweep.)
+// * triangle sweep (pure.py:113-155): valid candidates are found in
+//   parallel; the in-order conflict resolution is a lane-0 scan over the
+//   (short) compacted list; removals are applied in parallel.
+// * high-degree sweep (pure.py:158-185): in-order warp scan while the running
+//   budget is >= 0; once it is negative the remaining candidates follow the
+//   closed form "applies iff it still has a live neighbour that is not an
+//   earlier remaining candidate".
+//
+// Sub-word degree decrements use a 32-bit atomicSub on the containing word:
+// a live entry is >= 1, so the subtraction never borrows into the neighbour
+// entry (SPEC graph_core design decision on sub-word atomics, §4.4).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vcg {
+
+constexpr int kInf = 0x7fffffff;
+constexpr int kMaxWarps = 32;
+
+// ---------------------------------------------------------------------------
+// memory helpers
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__device__ __forceinline__ int ldv(const T* p, int i) {
+  return (int)(*(const volatile T*)(p + i));
+}
+
+template <typename T>
+__device__ __forceinline__ void deg_dec(T* deg, int x) {
+  if constexpr (sizeof(T) == 4) {
+    atomicSub((unsigned*)(deg + x), 1u);
+  } else {
+    uintptr_t a = (uintptr_t)(deg + x);
+    unsigned* w = (unsigned*)(a & ~(uintptr_t)3);
+    unsigned sh = (unsigned)(a & 3) * 8u;
+    atomicSub(w, 1u << sh);
+  }
+}
+
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// block collectives (all threads call; result is block-uniform)
+// ---------------------------------------------------------------------------
+
+struct BlockScratch {
+  int v[kMaxWarps + 8];
+  long long w[kMaxWarps + 2];
+  int bc[16];  // broadcast slots
+};
+
+__device__ __forceinline__ int warp_sum(int x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+__device__ __forceinline__ int block_sum(int x, BlockScratch* bs) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  x = warp_sum(x);
+  __syncthreads();
+  if (lane == 0) bs->v[wid] = x;
+  __syncthreads();
+  int t = 0;
+  for (int i = 0; i < nw; ++i) t += bs->v[i];
+  return t;
+}
+
+__device__ __forceinline__ int block_min(int x, BlockScratch* bs) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = min(x, __shfl_xor_sync(0xffffffffu, x, o));
+  __syncthreads();
+  if (lane == 0) bs->v[wid] = x;
+  __syncthreads();
+  int t = kInf;
+  for (int i = 0; i < nw; ++i) t = min(t, bs->v[i]);
+  return t;
+}
+
+__device__ __forceinline__ int block_max(int x, BlockScratch* bs) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
+  __syncthreads();
+  if (lane == 0) bs->v[wid] = x;
+  __syncthreads();
+  int t = -kInf;
+  for (int i = 0; i < nw; ++i) t = max(t, bs->v[i]);
+  return t;
+}
+
+__device__ __forceinline__ long long block_max64(long long x, BlockScratch* bs) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    long long y = __shfl_xor_sync(0xffffffffu, x, o);
+    x = y > x ? y : x;
+  }
+  __syncthreads();
+  if (lane == 0) bs->w[wid] = x;
+  __syncthreads();
+  long long t = bs->w[0];
+  for (int i = 1; i < nw; ++i) t = bs->w[i] > t ? bs->w[i] : t;
+  return t;
+}
+
+// Exclusive prefix of x over threads in threadIdx order; *total = sum.
+__device__ __forceinline__ int block_exscan(int x, BlockScratch* bs, int* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  int inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  __syncthreads();
+  if (lane == 31 || (int)threadIdx.x == (int)blockDim.x - 1) bs->v[wid] = inc;
+  __syncthreads();
+  int before = 0, tot = 0;
+  for (int i = 0; i < nw; ++i) {
+    int s = bs->v[i];
+    if (i < wid) before += s;
+    tot += s;
+  }
+  *total = tot;
+  return before + inc - x;
+}
+
+// contiguous chunk [b, e) of [lo, hi] owned by this thread (index order is
+// preserved across threads, so chunked scans give in-order compaction)
+__device__ __forceinline__ void my_chunk(int lo, int hi, int* b, int* e) {
+  int len = hi - lo + 1;
+  if (len <= 0) {
+    *b = *e = 0;
+    return;
+  }
+  int per = (len + (int)blockDim.x - 1) / (int)blockDim.x;
+  long long s = (long long)lo + (long long)threadIdx.x * per;
+  long long t = s + per;
+  if (s > hi + 1) s = hi + 1;
+  if (t > hi + 1) t = hi + 1;
+  *b = (int)s;
+  *e = (int)t;
+}
+
+// ---------------------------------------------------------------------------
+// per-node workspace
+// ---------------------------------------------------------------------------
+
+template <typename T>
+struct NodeWs {
+  T* deg;           // current node degree array [n] (4-byte aligned)
+  int* tmin;        // [n], kept == kInf between operations
+  int* ia;          // [n] int scratch
+  int* ib;          // [n]
+  int* ic;          // [n]
+  int* lst;         // [n]
+  int* id;          // [n]
+  uint8_t* flag;    // [n], kept == 0 between operations
+  BlockScratch* bs;
+  const int* off;   // static CSR (reduced graph), int32 offsets
+  const int* nbr;
+  int n;
+};
+
+struct PassRet {
+  int applied;
+  int forced;
+  int edges;
+  int pos;
+};
+
+template <typename T>
+__device__ __forceinline__ bool adjacent_static(const NodeWs<T>& w, int u, int x) {
+  int lo = w.off[u], hi = w.off[u + 1] - 1;
+  while (lo <= hi) {
+    int mid = (lo + hi) >> 1;
+    int y = w.nbr[mid];
+    if (y == x) return true;
+    if (y < x) lo = mid + 1;
+    else hi = mid - 1;
+  }
+  return false;
+}
+
+// Removal of a vertex u that is part of a set being removed together
+// (flag[.] == mark for every member): live neighbours outside the set are
+// decremented, an edge inside the set is counted once.  Returns edges.
+// deg[u] itself is zeroed by the caller once every member is processed.
+template <typename T>
+__device__ __forceinline__ int remove_marked_edges(const NodeWs<T>& w, int u, uint8_t mark) {
+  int e = 0;
+  const int b = w.off[u], end = w.off[u + 1];
+  for (int i = b; i < end; ++i) {
+    int x = w.nbr[i];
+    if (w.flag[x] == mark) {
+      if (x > u && ldv(w.deg, x) > 0) ++e;
+    } else if (ldv(w.deg, x) > 0) {
+      deg_dec(w.deg, x);
+      ++e;
+    }
+  }
+  return e;
+}
+
+// Parallel removal of the list out[b0, b0+cnt) (all flagged 1 and live).
+template <typename T>
+__device__ __forceinline__ int remove_list(const NodeWs<T>& w, const int* list, int cnt) {
+  int edges = 0;
+  for (int k = threadIdx.x; k < cnt; k += blockDim.x) edges += remove_marked_edges(w, list[k], 1);
+  edges = block_sum(edges, w.bs);  // also a barrier
+  for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
+    int u = list[k];
+    w.deg[u] = 0;
+    w.flag[u] = 0;
+  }
+  __syncthreads();
+  return edges;
+}
+
+// ---------------------------------------------------------------------------
+// rule sweeps
+// ---------------------------------------------------------------------------
+
+// pure.py:82 degree_one_pass.  Returns {applied, forced, edges, new_pos}.
+template <typename T>
+__device__ PassRet degree_one_pass(const NodeWs<T>& w, int lo, int hi, int* out, int pos) {
+  int b, e;
+  my_chunk(lo, hi, &b, &e);
+  int cnt = 0;
+  for (int v = b; v < e; ++v) cnt += (w.deg[v] == 1);
+  int ncand;
+  int at = block_exscan(cnt, w.bs, &ncand);
+  if (ncand == 0) return PassRet{0, 0, 0, pos};
+  for (int v = b; v < e; ++v) {
+    if (w.deg[v] == 1) {
+      int u = -1;
+      for (int i = w.off[v]; i < w.off[v + 1]; ++i) {
+        int x = w.nbr[i];
+        if (w.deg[x] > 0) {
+          u = x;
+          break;
+        }
+      }
+      w.ia[v] = u;
+      w.lst[at++] = v;
+      atomicMin(&w.tmin[u], v);
+    }
+  }
+  __syncthreads();
+  // decide, in candidate order (chunks of the candidate list)
+  int cb, ce;
+  my_chunk(0, ncand - 1, &cb, &ce);
+  int napp = 0;
+  for (int k = cb; k < ce; ++k) {
+    int v = w.lst[k];
+    int u = w.ia[v];
+    bool app = (w.tmin[u] == v) && !(w.deg[u] == 1 && w.ia[u] == v && u < v);
+    w.ic[k] = app;
+    napp += app;
+  }
+  int total;
+  int oat = block_exscan(napp, w.bs, &total);
+  for (int k = cb; k < ce; ++k) {
+    if (w.ic[k]) {
+      int u = w.ia[w.lst[k]];
+      out[pos + oat++] = u;
+      w.flag[u] = 1;
+    }
+  }
+  __syncthreads();
+  int edges = remove_list(w, out + pos, total);
+  for (int k = threadIdx.x; k < ncand; k += blockDim.x) w.tmin[w.ia[w.lst[k]]] = kInf;
+  __syncthreads();
+  return PassRet{total, total, edges, pos + total};
+}
+
+// pure.py:113 degree_two_triangle_pass
+template <typename T>
+__device__ PassRet degree_two_triangle_pass(const NodeWs<T>& w, int lo, int hi, int* out, int pos) {
+  int b, e;
+  my_chunk(lo, hi, &b, &e);
+  int cnt = 0;
+  for (int v = b; v < e; ++v) {
+    if (w.deg[v] == 2) {
+      int u = -1, x2 = -1;
+      for (int i = w.off[v]; i < w.off[v + 1]; ++i) {
+        int x = w.nbr[i];
+        if (w.deg[x] > 0) {
+          if (u < 0) {
+            u = x;
+          } else {
+            x2 = x;
+            break;
+          }
+        }
+      }
+      bool ok = x2 >= 0 && adjacent_static(w, u, x2);
+      w.ia[v] = u;
+      w.ib[v] = x2;
+      w.ic[v] = ok;
+      cnt += ok;
+    }
+  }
+  int nvalid;
+  int at = block_exscan(cnt, w.bs, &nvalid);
+  if (nvalid == 0) return PassRet{0, 0, 0, pos};
+  for (int v = b; v < e; ++v)
+    if (w.deg[v] == 2 && w.ic[v]) w.lst[at++] = v;
+  __syncthreads();
+  // in-order conflict resolution (sequential semantics), lane 0
+  if (threadIdx.x == 0) {
+    int p = pos, applied = 0;
+    for (int k = 0; k < nvalid; ++k) {
+      int v = w.lst[k];
+      int u = w.ia[v], x2 = w.ib[v];
+      if (!w.flag[v] && !w.flag[u] && !w.flag[x2]) {
+        w.flag[u] = 1;
+        w.flag[x2] = 1;
+        out[p++] = u;
+        out[p++] = x2;
+        ++applied;
+      }
+    }
+    w.bs->bc[0] = applied;
+  }
+  __syncthreads();
+  int applied = w.bs->bc[0];
+  int edges = remove_list(w, out + pos, 2 * applied);
+  return PassRet{applied, 2 * applied, edges, pos + 2 * applied};
+}
+
+// pure.py:158 high_degree_pass.
+template <typename T>
+__device__ PassRet high_degree_pass(const NodeWs<T>& w, int lo, int hi, int budget, int* out,
+                                    int pos) {
+  int b, e;
+  my_chunk(lo, hi, &b, &e);
+  int cnt = 0;
+  for (int v = b; v < e; ++v) {
+    int d = w.deg[v];
+    cnt += (d > 0 && d > budget);
+  }
+  int ncand;
+  int at = block_exscan(cnt, w.bs, &ncand);
+  if (ncand == 0) return PassRet{0, 0, 0, pos};
+  for (int v = b; v < e; ++v) {
+    int d = w.deg[v];
+    if (d > 0 && d > budget) w.lst[at++] = v;
+  }
+  __syncthreads();
+  // sequential phase: warp 0, in candidate order, while the budget is >= 0
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int i = 0, bud = budget, p = pos, applied = 0, edges = 0;
+    while (i < ncand && bud >= 0) {
+      int c = w.lst[i];
+      int d = ldv(w.deg, c);
+      if (d > 0 && d > bud) {
+        for (int j = w.off[c] + lane; j < w.off[c + 1]; j += 32) {
+          int x = w.nbr[j];
+          if (ldv(w.deg, x) > 0) deg_dec(w.deg, x);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          w.deg[c] = 0;
+          out[p] = c;
+        }
+        __syncwarp();
+        ++p;
+        ++applied;
+        edges += d;
+        --bud;
+      }
+      ++i;
+    }
+    if (lane == 0) {
+      w.bs->bc[0] = i;
+      w.bs->bc[1] = p;
+      w.bs->bc[2] = applied;
+      w.bs->bc[3] = edges;
+    }
+  }
+  __syncthreads();
+  const int i0 = w.bs->bc[0];
+  int p = w.bs->bc[1], applied = w.bs->bc[2], edges = w.bs->bc[3];
+  __syncthreads();
+  if (i0 < ncand) {
+    // closed form for the remaining candidates R = lst[i0:]: c applies iff
+    // it has a live neighbour x with x not in R or x > c
+    const int nr = ncand - i0;
+    for (int k = threadIdx.x; k < nr; k += blockDim.x) w.flag[w.lst[i0 + k]] = 2;
+    __syncthreads();
+    int cb, ce;
+    my_chunk(0, nr - 1, &cb, &ce);
+    int napp = 0;
+    for (int k = cb; k < ce; ++k) {
+      int c = w.lst[i0 + k];
+      bool app = false;
+      if (w.deg[c] > 0) {
+        for (int j = w.off[c]; j < w.off[c + 1]; ++j) {
+          int x = w.nbr[j];
+          if (w.deg[x] > 0 && (w.flag[x] != 2 || x > c)) {
+            app = true;
+            break;
+          }
+        }
+      }
+      w.ic[k] = app;
+      napp += app;
+    }
+    int total;
+    int oat = block_exscan(napp, w.bs, &total);
+    for (int k = cb; k < ce; ++k)
+      if (w.ic[k]) out[p + oat++] = w.lst[i0 + k];
+    __syncthreads();
+    for (int k = threadIdx.x; k < nr; k += blockDim.x) w.flag[w.lst[i0 + k]] = w.ic[k] ? 1 : 0;
+    __syncthreads();
+    edges += remove_list(w, out + p, total);
+    p += total;
+    applied += total;
+  }
+  return PassRet{applied, applied, edges, p};
+}
+
+// pure.py:230 recompute_bounds -> (lo, hi); empty -> (max(n,1), 0)
+template <typename T>
+__device__ void recompute_bounds(const NodeWs<T>& w, int* lo, int* hi) {
+  int l = *lo, h = *hi;
+  int mn = kInf, mx = -1;
+  if (l <= h) {
+    for (int v = l + threadIdx.x; v <= h; v += blockDim.x) {
+      if (w.deg[v] > 0) {
+        mn = min(mn, v);
+        mx = max(mx, v);
+      }
+    }
+  }
+  mn = block_min(mn, w.bs);
+  mx = block_max(mx, w.bs);
+  if (mx < 0) {
+    *lo = w.n > 1 ? w.n : 1;
+    *hi = 0;
+  } else {
+    *lo = mn;
+    *hi = mx;
+  }
+}
+
+struct FixRet {
+  int forced, d1, d2t, hd, edges, lo, hi, pos;
+};
+
+// pure.py:188 reduce_fixpoint
+template <typename T>
+__device__ FixRet reduce_fixpoint(const NodeWs<T>& w, int lo, int hi, int budget, int* out,
+                                  int pos) {
+  FixRet r{0, 0, 0, 0, 0, lo, hi, pos};
+  while (true) {
+    int cycle = 0;
+    while (true) {
+      PassRet a = degree_one_pass(w, lo, hi, out, r.pos);
+      r.d1 += a.applied;
+      r.forced += a.forced;
+      r.edges += a.edges;
+      r.pos = a.pos;
+      cycle += a.applied;
+      if (a.applied == 0) break;
+    }
+    PassRet t = degree_two_triangle_pass(w, lo, hi, out, r.pos);
+    r.d2t += t.applied;
+    r.forced += t.forced;
+    r.edges += t.edges;
+    r.pos = t.pos;
+    cycle += t.applied;
+    PassRet h = high_degree_pass(w, lo, hi, budget - r.forced, out, r.pos);
+    r.hd += h.applied;
+    r.forced += h.forced;
+    r.edges += h.edges;
+    r.pos = h.pos;
+    cycle += h.applied;
+    if (cycle == 0) break;
+  }
+  int l = lo, h = hi;
+  recompute_bounds(w, &l, &h);
+  r.lo = l;
+  r.hi = h;
+  return r;
+}
+
+// pure.py:241 select_max_degree: lowest-index live vertex of max degree, or -1
+template <typename T>
+__device__ int select_max_degree(const NodeWs<T>& w, int lo, int hi) {
+  long long best = -1;
+  if (lo <= hi) {
+    for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x) {
+      int d = w.deg[v];
+      if (d > 0) {
+        long long key = ((long long)d << 32) | (long long)(unsigned)(0x7fffffff - v);
+        best = key > best ? key : best;
+      }
+    }
+  }
+  best = block_max64(best, w.bs);
+  if (best < 0) return -1;
+  return 0x7fffffff - (int)(best & 0xffffffffLL);
+}
+
+template <typename T>
+__device__ int count_live(const NodeWs<T>& w, int lo, int hi) {
+  int c = 0;
+  if (lo <= hi)
+    for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x) c += (w.deg[v] > 0);
+  return block_sum(c, w.bs);
+}
+
+// pure.py:30 remove_vertex (single vertex, whole block): returns edges removed
+template <typename T>
+__device__ int remove_vertex(const NodeWs<T>& w, int v) {
+  int d = w.deg[v];
+  __syncthreads();
+  if (d == 0) return 0;
+  for (int j = w.off[v] + threadIdx.x; j < w.off[v + 1]; j += blockDim.x) {
+    int x = w.nbr[j];
+    if (ldv(w.deg, x) > 0) deg_dec(w.deg, x);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) w.deg[v] = 0;
+  __syncthreads();
+  return d;
+}
+
+// pure.py:47 remove_neighbors: force every live neighbour of v; returns
+// {removed, edges}; forced ids appended to out[pos..] in adjacency order.
+template <typename T>
+__device__ void remove_neighbors(const NodeWs<T>& w, int v, int* out, int pos, int* removed,
+                                 int* edges) {
+  const int b = w.off[v], e = w.off[v + 1];
+  // compact live neighbours (adjacency order) into out
+  int cb, ce;
+  my_chunk(b, e - 1, &cb, &ce);
+  int cnt = 0;
+  for (int j = cb; j < ce; ++j) cnt += (w.deg[w.nbr[j]] > 0);
+  int total;
+  int at = block_exscan(cnt, w.bs, &total);
+  for (int j = cb; j < ce; ++j) {
+    int x = w.nbr[j];
+    if (w.deg[x] > 0) {
+      out[pos + at++] = x;
+      w.flag[x] = 1;
+    }
+  }
+  __syncthreads();
+  *edges = remove_list(w, out + pos, total);
+  *removed = total;
+}
+
+// ---------------------------------------------------------------------------
+// connected components of the live subgraph (union-find in the workspace)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int uf_find(int* par, int x) {
+  int p = ((volatile int*)par)[x];
+  while (p != x) {
+    int gp = ((volatile int*)par)[p];
+    if (gp != p) ((volatile int*)par)[x] = gp;  // path halving, benign race
+    x = p;
+    p = gp;
+  }
+  return x;
+}
+
+__device__ __forceinline__ void uf_union(int* par, int a, int b) {
+  while (true) {
+    a = uf_find(par, a);
+    b = uf_find(par, b);
+    if (a == b) return;
+    if (a > b) {
+      int t = a;
+      a = b;
+      b = t;
+    }
+    // hook the larger root under the smaller: roots stay component minima
+    if (atomicCAS(&par[b], b, a) == b) return;
+  }
+}
+
+// Labels every live vertex in [lo, hi] with its component's minimum vertex
+// (ia[v]) and returns the number of components.
+template <typename T>
+__device__ int label_components(const NodeWs<T>& w, int lo, int hi) {
+  int* par = w.ia;
+  for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x) par[v] = v;
+  __syncthreads();
+  for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x) {
+    if (w.deg[v] > 0) {
+      for (int j = w.off[v]; j < w.off[v + 1]; ++j) {
+        int x = w.nbr[j];
+        if (x > v && w.deg[x] > 0) uf_union(par, v, x);
+      }
+    }
+  }
+  __syncthreads();
+  int roots = 0;
+  for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x) {
+    if (w.deg[v] > 0) {
+      int r = uf_find(par, v);
+      roots += (r == v);
+    }
+  }
+  roots = block_sum(roots, w.bs);
+  // full compression
+  for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x)
+    if (w.deg[v] > 0) par[v] = uf_find(par, v);
+  __syncthreads();
+  return roots;
+}
+
+struct CompInfo {
+  int size, degsum, mindeg, maxdeg, vmin, vmax;
+};
+
+// After label_components with ncomp > 1: component j (in increasing order of
+// its minimum vertex, i.e. the reference's discovery order) gets
+//   root lst[j], size ib[j], degsum ic[j], mindeg tmp..., see below.
+// Uses ia (labels), id (root -> ordinal), lst (ordinal -> root) and packs the
+// four aggregates into ib/ic (size, degsum) and two halves of tmin-free arrays.
+// Aggregates are written to agg[5*ncomp] (caller-provided int scratch).
+template <typename T>
+__device__ void component_aggregates(const NodeWs<T>& w, int lo, int hi, int ncomp, int* agg) {
+  int b, e;
+  my_chunk(lo, hi, &b, &e);
+  int cnt = 0;
+  for (int v = b; v < e; ++v) cnt += (w.deg[v] > 0 && w.ia[v] == v);
+  int tot;
+  int at = block_exscan(cnt, w.bs, &tot);
+  for (int v = b; v < e; ++v) {
+    if (w.deg[v] > 0 && w.ia[v] == v) {
+      w.lst[at] = v;
+      w.id[v] = at;
+      ++at;
+    }
+  }
+  for (int j = threadIdx.x; j < ncomp; j += blockDim.x) {
+    agg[5 * j + 0] = 0;
+    agg[5 * j + 1] = 0;
+    agg[5 * j + 2] = kInf;
+    agg[5 * j + 3] = 0;
+    agg[5 * j + 4] = 0;
+  }
+  __syncthreads();
+  for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x) {
+    int d = w.deg[v];
+    if (d > 0) {
+      int j = w.id[w.ia[v]];
+      atomicAdd(&agg[5 * j + 0], 1);
+      atomicAdd(&agg[5 * j + 1], d);
+      atomicMin(&agg[5 * j + 2], d);
+      atomicMax(&agg[5 * j + 3], d);
+      atomicMax(&agg[5 * j + 4], v);
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace vcg

@@ -1,0 +1,408 @@
+// Persistent search kernel: one resident block per worker, one search node per
+// block at a time.  See search.cuh for the coordination structures and
+// node_ops.cuh for the exact-semantics block-parallel node operations.
+#include "search.cuh"
+
+namespace vcg {
+
+struct BlockState {
+  NodeHdr hdr;   // current node
+  int best_s;    // scope best snapshot at node start
+  int qpos_lo, qpos_hi;
+  int flag;
+  int gen;       // number of general components in a split
+  int parent;
+  int child_base;
+  int v;
+};
+
+template <typename T>
+struct Worker {
+  const SearchParams& P;
+  NodeWs<T> w;
+  BlockState* st;
+  char* my_stack;
+  int top;   // block-uniform private stack height
+  // thread-0 statistics
+  unsigned long long nodes, comp_branches, pushes, pops, rules[6];
+  int max_depth;
+
+  __device__ Worker(const SearchParams& p, NodeWs<T> ws, BlockState* s)
+      : P(p), w(ws), st(s), top(0), nodes(0), comp_branches(0), pushes(0), pops(0), max_depth(0) {
+    for (int i = 0; i < 6; ++i) rules[i] = 0;
+    my_stack = P.stacks + (long long)blockIdx.x * P.stack_cap * P.slot_bytes;
+  }
+
+  __device__ char* stack_slot(int i) const { return my_stack + (long long)i * P.slot_bytes; }
+  __device__ char* queue_slot(long long pos) const {
+    return P.q.data + (pos % P.q.cap) * P.slot_bytes;
+  }
+
+  // engine.py:413 _offload_or_push: pick where the next child record goes.
+  // Returns the destination; *qpos >= 0 means a reserved worklist slot.
+  __device__ char* choose_dest(long long* qpos) {
+    if (threadIdx.x == 0) {
+      long long pos = -1;
+      if (P.share && q_length(P.q) < P.threshold) pos = q_reserve_push(P.q);
+      if (pos < 0 && top >= P.stack_cap) {
+        // private stack full: the worklist must take it (SPEC offloadOrPush)
+        unsigned spins = 0;
+        while ((pos = q_reserve_push(P.q)) < 0) {
+          __nanosleep(256);
+          if (++spins > (1u << 24)) {
+            atomicExch(&P.ctl->error, 2);
+            atomicExch(&P.ctl->stop, 1);
+            break;
+          }
+        }
+      }
+      st->qpos_lo = (int)(pos & 0xffffffffLL);
+      st->qpos_hi = (int)(pos >> 32);
+    }
+    __syncthreads();
+    long long pos = ((long long)st->qpos_hi << 32) | (unsigned)st->qpos_lo;
+    *qpos = pos;
+    if (pos >= 0) return queue_slot(pos);
+    if (top >= P.stack_cap) return nullptr;  // error path (stop set)
+    return stack_slot(top);
+  }
+
+  __device__ void commit_dest(long long qpos, const NodeHdr& h, char* dst) {
+    if (threadIdx.x == 0 && dst) *(NodeHdr*)dst = h;
+    __syncthreads();
+    if (qpos >= 0) {
+      if (threadIdx.x == 0) {
+        q_publish_push(P.q, qpos);
+        ++pushes;
+      }
+    } else if (dst) {
+      ++top;
+      if (threadIdx.x == 0 && top > max_depth) max_depth = top;
+    }
+  }
+
+  // ---------------------------------------------------------------- split --
+  // engine.py:334 _try_component_split
+  __device__ bool try_split() {
+    NodeHdr& h = st->hdr;
+    const int lo = h.lo, hi = h.hi;
+    int ncomp = label_components(w, lo, hi);
+    if (ncomp <= 1) return false;
+    int* agg = w.ib;
+    component_aggregates(w, lo, hi, ncomp, agg);
+    if (threadIdx.x == 0) {
+      ++comp_branches;
+      atomicAdd(&P.hist[ncomp < P.n + 1 ? ncomp : P.n + 1], 1ull);
+      int G = 0, spec = 0;
+      for (int j = 0; j < ncomp; ++j) {
+        int size = agg[5 * j], mn = agg[5 * j + 2], mx = agg[5 * j + 3];
+        // reductions.py:160 classify_special_component
+        if (mn == mx && mn == size - 1) {
+          spec += size - 1;
+          ++rules[4];
+          agg[5 * j + 2] = -1;  // mark special
+        } else if (mn == mx && mn == 2 && size >= 3) {
+          spec += (size + 1) / 2;
+          ++rules[5];
+          agg[5 * j + 2] = -2;
+        } else {
+          ++G;
+        }
+      }
+      const Registry& R = P.reg;
+      const int scope = h.scope;
+      atomicAdd(&R.live[scope], 1);  // slot for the parent entry's finalisation
+      int base = atomicAdd(R.count, 1 + G);
+      if (base + 1 + G > R.cap) {
+        atomicExch(&P.ctl->error, 1);
+        atomicExch(&P.ctl->stop, 1);
+        base = -1;
+      } else {
+        const int p = base;
+        R.kind[p] = 1;
+        R.sum[p] = h.S + spec;
+        R.sum_ach[p] = 1;
+        R.init_sum[p] = h.S;
+        R.folded[p] = spec;
+        R.live[p] = 1 + G;
+        R.link[p] = scope;
+        R.first_child[p] = p + 1;
+        R.nchild[p] = G;
+        R.disc_done[p] = 0;
+        R.key[p] = 0;
+        R.child_folded[p] = 0;
+        int running = h.S, g = 0;
+        for (int j = 0; j < ncomp; ++j) {
+          int size = agg[5 * j];
+          int mark = agg[5 * j + 2];
+          if (mark == -1) {
+            running += size - 1;
+          } else if (mark == -2) {
+            running += (size + 1) / 2;
+          } else {
+            int init = st->best_s - running;
+            if (size - 1 < init) init = size - 1;
+            if (init < 1) init = 1;
+            const bool ach = init == size - 1;
+            const int c = p + 1 + g;
+            R.kind[c] = 0;
+            R.key[c] = init * 2 + (ach ? 0 : 1);
+            R.live[c] = 1;
+            R.link[c] = p;
+            R.child_folded[c] = 0;
+            R.disc_done[c] = 0;
+            agg[5 * j + 2] = c;  // component -> its child entry
+            ++g;
+          }
+        }
+        __threadfence();
+      }
+      st->gen = G;
+      st->parent = base;
+    }
+    __syncthreads();
+    const int parent = st->parent;
+    if (parent >= 0) {
+      for (int j = 0; j < ncomp; ++j) {
+        const int c = agg[5 * j + 2];
+        if (c < 0) continue;  // special: folded into the parent sum
+        const int root = w.lst[j];
+        const int size_deg = agg[5 * j + 1];
+        const int vmax = agg[5 * j + 4];
+        long long qpos;
+        char* dst = choose_dest(&qpos);
+        if (!dst) break;
+        T* dd = (T*)(dst + sizeof(NodeHdr));
+        for (int v = threadIdx.x; v < P.n; v += blockDim.x) {
+          T val = 0;
+          if (v >= lo && v <= hi && w.deg[v] > 0 && w.ia[v] == root) val = w.deg[v];
+          dd[v] = val;
+        }
+        NodeHdr ch;
+        ch.S = 0;
+        ch.E = size_deg / 2;
+        ch.lo = P.use_bounds ? root : 0;
+        ch.hi = P.use_bounds ? vmax : P.n - 1;
+        ch.scope = c;
+        ch.depth = h.depth + 1;
+        ch.pad0 = ch.pad1 = 0;
+        commit_dest(qpos, ch, dst);
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) {
+        __threadfence();
+        st_release(&P.reg.disc_done[parent], 1);
+        if (atomicSub(&P.reg.live[parent], 1) == 1) reg_cascade(P, parent);
+      }
+    }
+    if (threadIdx.x == 0) reg_finish(P, h.scope);
+    __syncthreads();
+    return true;
+  }
+
+  // ------------------------------------------------------------- process --
+  // engine.py:277 _process_node.  Returns true when the include child is
+  // left in shared memory to be processed next.
+  __device__ bool process() {
+    NodeHdr& h = st->hdr;
+    if (threadIdx.x == 0) {
+      ++nodes;
+      st->best_s = ld_relaxed(&P.reg.key[h.scope]) >> 1;
+    }
+    __syncthreads();
+    const int best_s = st->best_s;
+    const int budget = best_s - h.S - 1;
+    FixRet fr = reduce_fixpoint(w, h.lo, h.hi, budget, w.id, 0);
+    if (threadIdx.x == 0) {
+      rules[0] += fr.d1;
+      rules[1] += fr.d2t;
+      rules[2] += fr.hd;
+    }
+    int S = h.S + fr.forced;
+    int E = h.E - fr.edges;
+    int lo = fr.lo, hi = fr.hi;
+    if (!P.use_bounds && P.n) {
+      lo = 0;
+      hi = P.n - 1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      h.S = S;
+      h.E = E;
+      h.lo = lo;
+      h.hi = hi;
+    }
+    __syncthreads();
+    if (!P.disable_pruning) {
+      bool prune = S >= best_s;
+      if (!prune) {
+        long long rem = (long long)best_s - S - 1;
+        prune = (long long)E > rem * rem;
+      }
+      if (prune) {
+        if (threadIdx.x == 0) reg_finish(P, h.scope);
+        __syncthreads();
+        return false;
+      }
+    }
+    if (E == 0) {
+      if (threadIdx.x == 0) {
+        reg_submit(P, h.scope, S, true);
+        reg_finish(P, h.scope);
+      }
+      __syncthreads();
+      return false;
+    }
+    if (P.use_components && try_split()) return false;
+    const int v = select_max_degree(w, lo, hi);
+    if (v < 0) {
+      if (threadIdx.x == 0) {
+        atomicExch(&P.ctl->error, 3);
+        atomicExch(&P.ctl->stop, 1);
+      }
+      __syncthreads();
+      return false;
+    }
+    // engine.py:319 _branch_on_vertex
+    if (threadIdx.x == 0) atomicAdd(&P.reg.live[h.scope], 1);
+    long long qpos;
+    char* dst = choose_dest(&qpos);
+    if (dst) {
+      T* dd = (T*)(dst + sizeof(NodeHdr));
+      store_deg<T>(dst, w.deg, P.n);
+      __syncthreads();
+      NodeWs<T> wx = w;
+      wx.deg = dd;
+      int removed, edges;
+      remove_neighbors(wx, v, w.lst, 0, &removed, &edges);
+      NodeHdr ex = h;
+      ex.S = S + removed;
+      ex.E = E - edges;
+      ex.depth = h.depth + 1;
+      commit_dest(qpos, ex, dst);
+    }
+    __syncthreads();
+    int e2 = remove_vertex(w, v);
+    if (threadIdx.x == 0) {
+      h.S = S + 1;
+      h.E = E - e2;
+      h.depth += 1;
+      if (top + 1 > max_depth) max_depth = top + 1;
+    }
+    __syncthreads();
+    return true;
+  }
+
+  __device__ void flush_stats() {
+    if (threadIdx.x != 0) return;
+    Ctl* c = P.ctl;
+    atomicAdd(&c->nodes, nodes);
+    atomicAdd(&c->comp_branches, comp_branches);
+    atomicAdd(&c->pushes, pushes);
+    atomicAdd(&c->pops, pops);
+    for (int i = 0; i < 6; ++i) atomicAdd(&c->rules[i], rules[i]);
+    atomicMax(&c->max_depth, max_depth);
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(1024) search_kernel(SearchParams P) {
+  extern __shared__ __align__(16) unsigned char dsmem[];
+  __shared__ BlockScratch bs;
+  __shared__ BlockState st;
+  char* base = P.ws_in_smem ? (char*)dsmem : P.gws + (long long)blockIdx.x * P.gws_bytes;
+  NodeWs<T> ws = carve_ws<T>(base, P.n, &bs, P.off, P.nbr);
+  for (int i = threadIdx.x; i < P.n; i += blockDim.x) {
+    ws.tmin[i] = kInf;
+    ws.flag[i] = 0;
+  }
+  // zero the degree-array padding once; load_node only overwrites [0, n)
+  {
+    const long long words = deg_bytes<T>(P.n > 0 ? P.n : 1) / 4;
+    for (long long i = threadIdx.x; i < words; i += blockDim.x) ((unsigned*)ws.deg)[i] = 0;
+  }
+  __syncthreads();
+  Worker<T> wk(P, ws, &st);
+  if (blockIdx.x == 0 && P.root_in_stack) {
+    wk.top = 1;
+    wk.max_depth = 1;
+  }
+  bool cont = false;
+  unsigned backoff = 32;
+  while (true) {
+    if (threadIdx.x == 0) {
+      int stop = ld_relaxed(&P.ctl->stop);
+      if (!stop && P.deadline_ns && globaltimer() > P.deadline_ns) {
+        atomicExch(&P.ctl->timed_out, 1);
+        atomicExch(&P.ctl->stop, 1);
+        stop = 1;
+      }
+      st.flag = stop;
+    }
+    __syncthreads();
+    if (st.flag) break;
+    if (!cont) {
+      if (wk.top > 0) {
+        wk.top -= 1;
+        load_node<T>(wk.stack_slot(wk.top), &st.hdr, ws.deg, P.n);
+        __syncthreads();
+      } else {
+        if (threadIdx.x == 0) {
+          long long pos = q_reserve_pop(P.q);
+          st.qpos_lo = (int)(pos & 0xffffffffLL);
+          st.qpos_hi = (int)(pos >> 32);
+        }
+        __syncthreads();
+        long long pos = ((long long)st.qpos_hi << 32) | (unsigned)st.qpos_lo;
+        if (pos < 0) {
+          if (threadIdx.x == 0) __nanosleep(backoff);
+          backoff = backoff < 4096 ? backoff * 2 : 4096;
+          __syncthreads();
+          continue;
+        }
+        backoff = 32;
+        load_node<T>(wk.queue_slot(pos), &st.hdr, ws.deg, P.n);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          q_release_pop(P.q, pos);
+          ++wk.pops;
+        }
+      }
+    }
+    cont = wk.process();
+  }
+  // stop: release the registry slots of abandoned work (engine.py:235-243)
+  if (threadIdx.x == 0) {
+    if (cont) reg_finish(P, st.hdr.scope);
+    for (int i = wk.top - 1; i >= 0; --i) {
+      const NodeHdr* hh = (const NodeHdr*)wk.stack_slot(i);
+      reg_finish(P, __ldcg(&hh->scope));
+    }
+  }
+  wk.flush_stats();
+}
+
+// single-block drain of the worklist after the search kernel (engine.py:216)
+__global__ void drain_kernel(SearchParams P) {
+  if (threadIdx.x != 0) return;
+  while (true) {
+    long long pos = q_reserve_pop(P.q);
+    if (pos < 0) break;
+    const NodeHdr* hh = (const NodeHdr*)(P.q.data + (pos % P.q.cap) * P.slot_bytes);
+    int scope = __ldcg(&hh->scope);
+    q_release_pop(P.q, pos);
+    reg_finish(P, scope);
+  }
+}
+
+__global__ void queue_init_kernel(unsigned long long* seq, long long cap) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cap;
+       i += (long long)gridDim.x * blockDim.x)
+    seq[i] = (unsigned long long)i;
+}
+
+template __global__ void search_kernel<uint8_t>(SearchParams);
+template __global__ void search_kernel<uint16_t>(SearchParams);
+template __global__ void search_kernel<uint32_t>(SearchParams);
+
+}  // namespace vcg

@@ -1,0 +1,273 @@
+// Persistent component-aware branch-and-reduce search (north star (2)-(4)).
+//
+// One resident thread block = one worker of the reference engine
+// (vcsolver/engine.py:160 _Engine).  Each block loops: take a node (the
+// include child it just produced, else the top of its private stack in HBM,
+// else the global worklist), reduce it in shared memory, prune / submit /
+// split into components / branch on the max-degree vertex.  Coordination is
+// only through:
+//   * the global worklist -- a bounded MPMC ring (Vyukov sequence numbers)
+//     holding whole node records (engine.py:413 _offload_or_push policy);
+//   * the component branch registry -- struct-of-arrays entries updated with
+//     device-scope atomics (registry.py; SPEC registry module), whose
+//     live-descendant counters hand finalisation to the last finisher
+//     (engine.py:424-462 _finish/_cascade/_submit, :464 _pvc_propagate);
+//   * the stop/found flags.
+#pragma once
+
+#include "node_ops.cuh"
+
+namespace vcg {
+
+// node record header, 32 bytes, followed by deg[n] (padded to 16 B)
+struct NodeHdr {
+  int S, E, lo, hi, scope, depth, pad0, pad1;
+};
+
+struct Registry {
+  int* key;           // child: best*2 + !achieved (atomicMin == atomic_min_best)
+  int* live;          // child: live_nodes; parent: live_comps
+  int* link;          // child: parent entry (-1 at root); parent: ancestor
+  int* kind;          // 0 child, 1 parent
+  int* sum;           // parent
+  int* sum_ach;       // parent: 1 while every folded term was achieved
+  int* init_sum;      // parent (diagnostics / conservation check)
+  int* folded;        // parent: total of in-place solved (special) components
+  int* first_child;   // parent: children are [first_child, first_child+nchild)
+  int* nchild;        // parent
+  int* disc_done;     // parent
+  int* child_folded;  // child: its best has been added to the parent sum
+  int* count;         // arena size (device counter)
+  int cap;
+};
+
+struct Ctl {
+  int stop, found, timed_out, error;
+  int max_depth, pad0, pad1, pad2;
+  unsigned long long nodes, comp_branches, pushes, pops;
+  unsigned long long rules[6];  // degree_one, d2t, high_degree, crown, clique, cycle
+};
+
+struct Queue {
+  unsigned long long* seq;
+  unsigned long long* head;
+  unsigned long long* tail;
+  char* data;
+  long long cap;
+};
+
+struct SearchParams {
+  int n;
+  const int* off;
+  const int* nbr;
+  char* stacks;           // gridDim.x * stack_cap * slot_bytes
+  long long stack_cap;
+  long long slot_bytes;
+  Queue q;
+  Registry reg;
+  Ctl* ctl;
+  unsigned long long* hist;  // [n + 2] components-per-branch histogram
+  char* gws;              // global workspace (when the workspace does not fit smem)
+  long long gws_bytes;    // per block
+  int ws_in_smem;
+  int share;              // offload to the worklist at all
+  long long threshold;    // worklist length below which nodes are offloaded
+  int use_components, use_bounds, disable_pruning;
+  int pvc;
+  int k_red;
+  int root_index;
+  int root_in_stack;
+  unsigned long long deadline_ns;  // 0 = none
+};
+
+template <typename T>
+__host__ __device__ inline long long deg_bytes(int n) {
+  return (((long long)n * (long long)sizeof(T)) + 15) & ~15LL;
+}
+
+// workspace bytes for one block (deg + flag + 7 int arrays)
+template <typename T>
+__host__ __device__ inline long long ws_bytes(int n) {
+  long long nn = n > 0 ? n : 1;
+  return deg_bytes<T>(n > 0 ? n : 1) + ((nn + 15) & ~15LL) + 7LL * 4LL * ((nn + 3) & ~3LL);
+}
+
+template <typename T>
+__device__ inline NodeWs<T> carve_ws(char* base, int n, BlockScratch* bs, const int* off,
+                                     const int* nbr) {
+  long long nn = n > 0 ? n : 1;
+  long long ni = (nn + 3) & ~3LL;
+  NodeWs<T> w;
+  char* p = base;
+  w.deg = (T*)p;
+  p += deg_bytes<T>((int)nn);
+  w.flag = (uint8_t*)p;
+  p += (nn + 15) & ~15LL;
+  int* ip = (int*)p;
+  w.tmin = ip;
+  w.ia = ip + ni;
+  w.id = ip + 2 * ni;
+  w.lst = ip + 3 * ni;
+  w.ib = ip + 4 * ni;  // ib, ic and the spare that follows are contiguous:
+  w.ic = ip + 5 * ni;  // component aggregates (5 ints x <= n/2 comps) use them
+  w.bs = bs;
+  w.off = off;
+  w.nbr = nbr;
+  w.n = n;
+  return w;
+}
+
+// ------------------------------------------------------------------ queue --
+
+// Reserve a ring position for a push; -1 when full.  Thread 0 only.
+__device__ inline long long q_reserve_push(const Queue& q) {
+  unsigned long long pos = ld_relaxed_u64(q.tail);
+  while (true) {
+    unsigned long long s = ld_acquire_u64(&q.seq[pos % q.cap]);
+    long long dif = (long long)s - (long long)pos;
+    if (dif == 0) {
+      unsigned long long prev = atomicCAS(q.tail, pos, pos + 1);
+      if (prev == pos) return (long long)pos;
+      pos = prev;
+    } else if (dif < 0) {
+      return -1;
+    } else {
+      pos = ld_relaxed_u64(q.tail);
+    }
+  }
+}
+
+__device__ inline void q_publish_push(const Queue& q, long long pos) {
+  __threadfence();
+  st_release_u64(&q.seq[pos % q.cap], (unsigned long long)pos + 1);
+}
+
+// Reserve a ring position for a pop; -1 when empty.  Thread 0 only.
+__device__ inline long long q_reserve_pop(const Queue& q) {
+  unsigned long long pos = ld_relaxed_u64(q.head);
+  while (true) {
+    unsigned long long s = ld_acquire_u64(&q.seq[pos % q.cap]);
+    long long dif = (long long)s - (long long)(pos + 1);
+    if (dif == 0) {
+      unsigned long long prev = atomicCAS(q.head, pos, pos + 1);
+      if (prev == pos) return (long long)pos;
+      pos = prev;
+    } else if (dif < 0) {
+      return -1;
+    } else {
+      pos = ld_relaxed_u64(q.head);
+    }
+  }
+}
+
+__device__ inline void q_release_pop(const Queue& q, long long pos) {
+  __threadfence();
+  st_release_u64(&q.seq[pos % q.cap], (unsigned long long)pos + (unsigned long long)q.cap);
+}
+
+__device__ inline long long q_length(const Queue& q) {
+  long long t = (long long)ld_relaxed_u64(q.tail);
+  long long h = (long long)ld_relaxed_u64(q.head);
+  return t > h ? t - h : 0;
+}
+
+// --------------------------------------------------------------- registry --
+
+__device__ inline void reg_submit(const SearchParams& P, int idx, int value, bool achieved);
+
+// engine.py:464 _pvc_propagate.  Children are read before the parent sum so
+// a child that finishes concurrently is counted twice (a safe over-estimate)
+// rather than not at all.
+__device__ inline void pvc_propagate(const SearchParams& P, int idx) {
+  const Registry& R = P.reg;
+  while (true) {
+    int p = ld_relaxed(&R.link[idx]);
+    if (p < 0) return;
+    if (!ld_acquire(&R.disc_done[p])) return;
+    long long total = 0;
+    int fc = R.first_child[p], nc = R.nchild[p];
+    for (int c = fc; c < fc + nc; ++c) {
+      int live = ld_relaxed(&R.live[c]);
+      int folded = ld_acquire(&R.child_folded[c]);
+      if (live > 0 || !folded) {
+        int key = ld_relaxed(&R.key[c]);
+        if (key & 1) return;  // live component whose bound is not achieved
+        total += key >> 1;
+      }
+    }
+    __threadfence();
+    if (!ld_relaxed(&R.sum_ach[p])) return;
+    total += ld_relaxed(&R.sum[p]);
+    int anc = R.link[p];
+    atomicMin(&R.key[anc], (int)(total * 2));
+    idx = anc;
+  }
+}
+
+// engine.py:453 _submit
+__device__ inline void reg_submit(const SearchParams& P, int idx, int value, bool achieved) {
+  atomicMin(&P.reg.key[idx], value * 2 + (achieved ? 0 : 1));
+  if (!P.pvc) return;
+  if (idx != P.root_index) pvc_propagate(P, idx);
+  int best = ld_relaxed(&P.reg.key[P.root_index]) >> 1;
+  if (best <= P.k_red) {
+    atomicExch(&P.ctl->found, 1);
+    atomicExch(&P.ctl->stop, 1);
+  }
+}
+
+// engine.py:428 _cascade: run completion upward from a quiesced entry.
+__device__ inline void reg_cascade(const SearchParams& P, int idx) {
+  const Registry& R = P.reg;
+  while (true) {
+    if (R.kind[idx] == 0) {
+      int p = R.link[idx];
+      if (p < 0) {
+        atomicExch(&P.ctl->stop, 1);  // root scope finished
+        return;
+      }
+      int key = ld_relaxed(&R.key[idx]);
+      atomicAdd(&R.sum[p], key >> 1);
+      if (key & 1) atomicAnd(&R.sum_ach[p], 0);
+      __threadfence();
+      st_release(&R.child_folded[idx], 1);
+      if (atomicSub(&R.live[p], 1) != 1) return;
+      idx = p;
+    } else {
+      __threadfence();
+      int total = ld_relaxed(&R.sum[idx]);
+      int ach = ld_relaxed(&R.sum_ach[idx]);
+      int anc = R.link[idx];
+      reg_submit(P, anc, total, ach != 0);
+      if (atomicSub(&R.live[anc], 1) != 1) return;
+      idx = anc;
+    }
+  }
+}
+
+__device__ inline void reg_finish(const SearchParams& P, int scope) {
+  __threadfence();
+  if (atomicSub(&P.reg.live[scope], 1) == 1) reg_cascade(P, scope);
+}
+
+// ------------------------------------------------------------ node moves --
+
+template <typename T>
+__device__ inline void load_node(const char* src, NodeHdr* hdr, T* deg, int n) {
+  const uint4* s = (const uint4*)src;
+  if (threadIdx.x < 2) ((uint4*)hdr)[threadIdx.x] = __ldcg(s + threadIdx.x);
+  const long long words = deg_bytes<T>(n) / 16;
+  const uint4* sd = s + 2;
+  uint4* dd = (uint4*)deg;
+  for (long long i = threadIdx.x; i < words; i += blockDim.x) dd[i] = __ldcg(sd + i);
+}
+
+template <typename T>
+__device__ inline void store_deg(char* dst, const T* deg, int n) {
+  const long long words = deg_bytes<T>(n) / 16;
+  uint4* dd = (uint4*)(dst + sizeof(NodeHdr));
+  const uint4* sd = (const uint4*)deg;
+  for (long long i = threadIdx.x; i < words; i += blockDim.x) __stcg(dd + i, sd[i]);
+}
+
+}  // namespace vcg

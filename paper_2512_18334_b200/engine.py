@@ -1,0 +1,274 @@
+"""solve(): the reference's solve pipeline driving the B200 search kernel.
+
+Mirrors ``vcsolver.engine`` (engine.py:45-659): same ``SolverConfig`` fields,
+same ``SolveResult`` / ``Stats`` shapes and the same phase logic (root
+reduction, PVC early exits, root bound initialisation, search, result
+assembly).  The search itself is ``vcg_search`` -- one persistent CUDA kernel
+in which every resident thread block is one worker of the reference engine.
+
+Differences from the reference, by design:
+* ``workers`` counts thread blocks; 0 (the default) fills every resident
+  block slot of the GPU.  ``deterministic=True`` runs one block and replays
+  the reference's single-worker schedule exactly (same statistics).
+* The registry lives in HBM; ``SolveResult.registry`` is a summary object
+  exposing the reference's diagnostics (quiescence / conservation).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .graph import StaticGraph
+from .preprocess import Preprocessed, greedy_bound, root_reduce
+
+RULE_KEYS = (
+    "degree_one",
+    "degree_two_triangle",
+    "high_degree",
+    "crown",
+    "clique_component",
+    "cycle_component",
+)
+
+
+@dataclass
+class SolverConfig:
+    """engine.py:45 SolverConfig (``workers`` = GPU thread blocks, 0 = all)."""
+
+    mode: str = "mvc"
+    k: int | None = None
+    workers: int = 0
+    use_components: bool = True
+    use_root_reduce: bool = True
+    use_bounds: bool = True
+    use_crown: bool = True
+    load_balance: bool = True
+    deterministic: bool = False
+    width: int | None = None
+    record_cover: bool = False
+    timeout: float | None = None
+    worklist_threshold: int | None = None
+    threads: int = 0  # block size; 0 = chosen from the reduced graph size
+    check_registry: bool = False
+    _disable_pruning: bool = False
+
+    def validate(self) -> None:
+        if self.mode not in ("mvc", "pvc"):
+            raise ValueError(f"unknown mode {self.mode!r}")
+        if self.mode == "pvc":
+            if self.k is None or self.k < 0:
+                raise ValueError("pvc mode needs a non-negative k")
+        if self.workers < 0:
+            raise ValueError("workers must be >= 0")
+        if self.timeout is not None and self.timeout <= 0:
+            raise ValueError("timeout must be positive")
+        if self.worklist_threshold is not None and self.worklist_threshold < 1:
+            raise ValueError("worklist threshold must be >= 1")
+
+
+@dataclass
+class Stats:
+    """engine.py:79 Stats (Table III/IV counters)."""
+
+    tree_nodes_visited: int = 0
+    component_branches: int = 0
+    components_per_branch: dict[int, int] = field(default_factory=dict)
+    rule_counts: dict[str, int] = field(default_factory=dict)
+    root_vertices_before: int = 0
+    root_vertices_after: int = 0
+    degree_width: int = 0
+    max_stack_depth: int = 0
+    worklist_pushes: int = 0
+    worklist_pops: int = 0
+    phase_seconds: dict[str, float] = field(default_factory=dict)
+
+    def as_dict(self) -> dict:
+        return {
+            "tree_nodes_visited": self.tree_nodes_visited,
+            "component_branches": self.component_branches,
+            "components_per_branch": dict(sorted(self.components_per_branch.items())),
+            "rule_counts": dict(self.rule_counts),
+            "root_vertices_before": self.root_vertices_before,
+            "root_vertices_after": self.root_vertices_after,
+            "degree_width": self.degree_width,
+            "max_stack_depth": self.max_stack_depth,
+            "worklist_pushes": self.worklist_pushes,
+            "worklist_pops": self.worklist_pops,
+            "phase_seconds": dict(self.phase_seconds),
+        }
+
+
+class RegistrySummary:
+    """Post-solve view of the device registry (registry.py:522-548 diagnostics)."""
+
+    def __init__(self, entries: int, violations: int | None):
+        self.entries = entries
+        self._violations = violations
+
+    def __len__(self) -> int:
+        return self.entries
+
+    def quiescence_violations(self) -> list[str]:
+        if self._violations is None:
+            raise RuntimeError("solve with check_registry=True to audit the registry")
+        return [f"{self._violations} registry entries violate quiescence/conservation"] \
+            if self._violations else []
+
+    conservation_violations = quiescence_violations
+
+
+@dataclass
+class SolveResult:
+    """engine.py:109 SolveResult."""
+
+    cover_size: int | None
+    found: bool
+    exact: bool
+    cover: list[int] | None
+    stats: Stats
+    mode: str
+    k: int | None = None
+    registry: RegistrySummary | None = None
+    root_index: int | None = None
+    forced: list[int] = field(default_factory=list)
+    search_ms: float = 0.0  # device time of the search kernel
+
+
+def run_search(rg: StaticGraph, cfg: SolverConfig, width: int, best_init: int,
+               achieved_init: bool, k_red: int | None):
+    """One vcg_search call; returns (SearchResult_t, histogram dict)."""
+    sc = _lib.SearchConfig_t()
+    sc.width = width
+    sc.pvc = int(k_red is not None)
+    sc.k_red = int(k_red) if k_red is not None else -1
+    sc.best_init = int(best_init)
+    sc.best_init_achieved = int(achieved_init)
+    sc.use_components = int(cfg.use_components)
+    sc.use_bounds = int(cfg.use_bounds)
+    sc.disable_pruning = int(cfg._disable_pruning)
+    sc.deterministic = int(cfg.deterministic)
+    sc.load_balance = int(cfg.load_balance)
+    sc.workers = int(cfg.workers)
+    sc.threads = int(cfg.threads)
+    sc.worklist_threshold = int(cfg.worklist_threshold or 0)
+    sc.timeout = float(cfg.timeout or 0.0)
+    sc.check_registry = int(cfg.check_registry)
+    res = _lib.SearchResult_t()
+    hist = np.zeros(rg.num_vertices + 2, dtype=np.int64)
+    _lib.check(_lib.lib.vcg_search(rg.device().handle, C.byref(sc), C.byref(res),
+                                   hist.ctypes.data))
+    if res.error:
+        raise _lib.GpuError(f"search kernel reported device error {res.error}")
+    h = {int(i): int(c) for i, c in enumerate(hist) if c}
+    return res, h
+
+
+def _assemble_cover(g: StaticGraph, pre: Preprocessed, local: list[int]) -> list[int]:
+    """engine.py:550 -- map a reduced-graph cover to original ids and verify it."""
+    cover = sorted(set(pre.forced) | {int(pre.vertex_map[v]) for v in local})
+    covered = np.zeros(g.num_vertices, dtype=bool)
+    covered[cover] = True
+    heads = np.repeat(np.arange(g.num_vertices), np.diff(g.offsets))
+    if not np.all(covered[heads] | covered[g.neighbors]):
+        raise RuntimeError("reconstructed cover misses an edge")
+    return cover
+
+
+def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
+    """engine.py:561 solve: MVC, or PVC's decision form with budget k."""
+    cfg = config if config is not None else SolverConfig()
+    cfg.validate()
+    stats = Stats()
+    stats.rule_counts = dict.fromkeys(RULE_KEYS, 0)
+    stats.root_vertices_before = g.num_vertices
+    stats.phase_seconds = {"root_reduce": 0.0, "search": 0.0, "reconstruct": 0.0}
+
+    t0 = time.perf_counter()
+    bound = cfg.k if cfg.mode == "pvc" else None
+    pre = root_reduce(g, enabled=cfg.use_root_reduce, crown=cfg.use_crown, bound=bound,
+                      width_override=cfg.width)
+    stats.phase_seconds["root_reduce"] = time.perf_counter() - t0
+    for key, val in pre.rule_counts.items():
+        stats.rule_counts[key] = stats.rule_counts.get(key, 0) + val
+    stats.root_vertices_after = pre.graph.num_vertices
+    stats.degree_width = pre.width
+    rg = pre.graph
+
+    result = SolveResult(cover_size=None, found=False, exact=True, cover=None, stats=stats,
+                         mode=cfg.mode, k=cfg.k, forced=list(pre.forced))
+
+    if cfg.mode == "pvc" and pre.forced_count > cfg.k:
+        return result
+
+    if rg.num_edges == 0:
+        result.found = True
+        result.cover_size = pre.forced_count
+        if cfg.record_cover:
+            result.cover = _assemble_cover(g, pre, [])
+            result.cover_size = len(result.cover)
+        return result
+
+    k_red = cfg.k - pre.forced_count if cfg.mode == "pvc" else None
+    greedy_reduced = pre.greedy_reduced
+    if cfg.mode == "pvc":
+        if greedy_reduced <= k_red:
+            result.found = True
+            result.cover_size = pre.forced_count + greedy_reduced
+            if cfg.record_cover:
+                _, members = greedy_bound(rg, members=True)
+                result.cover = _assemble_cover(g, pre, members)
+                result.cover_size = len(result.cover)
+            return result
+        best_init = min(greedy_reduced, k_red + 1)
+        achieved_init = greedy_reduced <= k_red + 1
+    else:
+        cap = pre.greedy_original - pre.forced_count
+        best_init = max(1, min(greedy_reduced, cap))
+        achieved_init = greedy_reduced <= cap
+
+    t1 = time.perf_counter()
+    res, hist = run_search(rg, cfg, pre.width, best_init, achieved_init, k_red)
+    stats.phase_seconds["search"] = time.perf_counter() - t1
+    result.search_ms = float(res.kernel_ms)
+    stats.tree_nodes_visited = int(res.tree_nodes_visited)
+    stats.component_branches = int(res.component_branches)
+    stats.components_per_branch = hist
+    for i, key in enumerate(RULE_KEYS):
+        if key == "crown":
+            continue
+        stats.rule_counts[key] = stats.rule_counts.get(key, 0) + int(res.rule_counts[i])
+    stats.max_stack_depth = int(res.max_stack_depth)
+    stats.worklist_pushes = int(res.worklist_pushes)
+    stats.worklist_pops = int(res.worklist_pops)
+    result.registry = RegistrySummary(int(res.registry_entries),
+                                      int(res.registry_violations) if cfg.check_registry else None)
+    result.root_index = 0
+
+    best = int(res.best)
+    timed_out = bool(res.timed_out)
+    if cfg.mode == "mvc":
+        result.found = True
+        result.cover_size = pre.forced_count + best
+        result.exact = not timed_out
+        have_target = True
+    else:
+        found = bool(res.found) or best <= k_red
+        result.found = found
+        result.exact = found or not timed_out
+        result.cover_size = pre.forced_count + best if found else None
+        have_target = found
+
+    if cfg.record_cover and have_target and result.exact:
+        t2 = time.perf_counter()
+        from .witness import witness_cover
+
+        local = witness_cover(rg, pre.width, best, cfg)
+        result.cover = _assemble_cover(g, pre, local)
+        result.cover_size = len(result.cover)
+        stats.phase_seconds["reconstruct"] = time.perf_counter() - t2
+    return result

@@ -1,0 +1,92 @@
+"""Root reduction + compaction (mirror of vcsolver.preprocess, preprocess.py:321-468).
+
+The lightweight rules run to a fixpoint on the device, the crown rule's
+matching runs natively on the host, survivors are compacted into a fresh CSR
+on the device (``vcg_root_reduce``), and the degree width is the smallest of
+8/16/32 bits that holds the reduced maximum degree (§4.4).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .graph import SUPPORTED_WIDTHS, DeviceGraph, StaticGraph, width_capacity
+
+ROOT_RULE_KEYS = ("degree_one", "degree_two_triangle", "high_degree", "crown")
+
+
+def greedy_bound(g: StaticGraph, members: bool = False):
+    """preprocess.py:348 -- max-degree greedy cover size (optionally the picks)."""
+    if g.num_vertices == 0 or g.num_edges == 0:
+        return (0, []) if members else 0
+    out = np.zeros(g.num_vertices, dtype=np.int32) if members else None
+    size = C.c_int64()
+    _lib.check(_lib.lib.vcg_greedy_bound(g.device().handle,
+                                         out.ctypes.data if members else None, C.byref(size)))
+    if members:
+        return int(size.value), out[: size.value].tolist()
+    return int(size.value)
+
+
+def select_width(max_degree: int, override: int | None = None) -> int:
+    """preprocess.py:362 -- smallest supported width whose capacity fits."""
+    if override is not None:
+        if override not in SUPPORTED_WIDTHS:
+            raise ValueError(
+                f"unsupported degree width {override}; choose one of {SUPPORTED_WIDTHS}")
+        if max_degree > width_capacity(override):
+            raise ValueError(f"max degree {max_degree} does not fit degree width {override}")
+        return override
+    for width in SUPPORTED_WIDTHS:
+        if max_degree <= width_capacity(width):
+            return width
+    raise ValueError(f"max degree {max_degree} exceeds every supported width")
+
+
+@dataclass
+class Preprocessed:
+    """preprocess.py:380 -- result of the root reduction pass."""
+
+    graph: StaticGraph
+    vertex_map: np.ndarray  # reduced id -> original id
+    forced: list[int]
+    greedy_original: int
+    greedy_reduced: int
+    width: int
+    rule_counts: dict[str, int] = field(default_factory=dict)
+    seconds: dict[str, float] = field(default_factory=dict)
+
+    @property
+    def forced_count(self) -> int:
+        return len(self.forced)
+
+
+def root_reduce(g: StaticGraph, enabled: bool = True, crown: bool = True,
+                bound: int | None = None, width_override: int | None = None) -> Preprocessed:
+    """preprocess.py:397 root_reduce on the device."""
+    n = g.num_vertices
+    info = _lib.Preprocessed_t()
+    forced = np.zeros(max(n, 1), dtype=np.int32)
+    vmap = np.zeros(max(n, 1), dtype=np.int64)
+    h = C.c_void_p()
+    _lib.check(_lib.lib.vcg_root_reduce(
+        g.device().handle, int(enabled), int(crown), int(bound is not None),
+        int(bound) if bound is not None else 0, C.byref(info), forced.ctypes.data,
+        vmap.ctypes.data, C.byref(h)))
+    reduced = StaticGraph.from_device(DeviceGraph(h.value))
+    md = int(info.max_degree_reduced)
+    return Preprocessed(
+        graph=reduced,
+        vertex_map=vmap[: info.n_reduced].copy(),
+        forced=forced[: info.forced_count].tolist(),
+        greedy_original=int(info.greedy_original),
+        greedy_reduced=int(info.greedy_reduced),
+        width=select_width(md, width_override),
+        rule_counts=dict(zip(ROOT_RULE_KEYS, (int(x) for x in info.rule_counts))),
+        seconds={"device_reduce": info.seconds[0], "crown": info.seconds[1],
+                 "compaction": info.seconds[2]},
+    )

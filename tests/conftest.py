@@ -1,4 +1,5 @@
 import os
+import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -11,3 +12,6 @@ if HERE not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    # the product package loads its in-tree CUDA library at import: make sure
+    # it is built (nvcc cross-compiles for sm_100a without a GPU)
+    subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "paper_2512_18334_b200", "csrc")])

@@ -1,0 +1,112 @@
+"""End-to-end parity of the GPU solver with the reference (tests/golden/
+solve.json, root_reduce.json, workloads.json -- all produced by running
+vcsolver itself, see tests/golden/make_golden.py).
+
+* deterministic mode (one block) replays the reference's single-worker
+  schedule: answers AND every statistic must be identical;
+* parallel mode (every resident block): answers identical, registry
+  quiescent and conserved."""
+
+from __future__ import annotations
+
+import pytest
+
+from helpers import assert_valid_cover, csr, golden, stats_without_time
+
+pytestmark = pytest.mark.gpu
+
+_CFG = {
+    "det": dict(deterministic=True),
+    "w1": dict(workers=1),
+    "det_nocomp": dict(deterministic=True, use_components=False),
+    "det_noroot": dict(deterministic=True, use_root_reduce=False),
+    "det_nobounds": dict(deterministic=True, use_bounds=False),
+    "det_nocrown": dict(deterministic=True, use_crown=False),
+    "w1_nolb": dict(workers=1, load_balance=False),
+}
+
+
+def _graph(case):
+    import paper_2512_18334_b200 as vc
+
+    n, off, nbr = csr(case["n"], case["edges"])
+    return vc.StaticGraph(n, off, nbr)
+
+
+def test_root_reduce_bit_exact():
+    import paper_2512_18334_b200 as vc
+
+    for case in golden("root_reduce.json"):
+        g = _graph(case)
+        pre = vc.root_reduce(g, bound=case["bound"])
+        assert pre.forced == case["forced"]
+        assert pre.vertex_map.tolist() == case["vertex_map"]
+        assert pre.rule_counts == case["rule_counts"]
+        assert pre.greedy_original == case["greedy_original"]
+        assert pre.greedy_reduced == case["greedy_reduced"]
+        assert pre.width == case["width"]
+        rn = len(case["vertex_map"])
+        _, roff, rnbr = csr(rn, case["reduced_edges"])
+        assert pre.graph.offsets.tolist() == roff.tolist()
+        assert pre.graph.neighbors.tolist() == rnbr.tolist()
+        if "greedy_members" in case:
+            assert vc.greedy_bound(g, members=True)[1] == case["greedy_members"]
+
+
+def test_deterministic_solve_matches_reference_stats():
+    import paper_2512_18334_b200 as vc
+
+    for case in golden("solve.json"):
+        g = _graph(case)
+        for cname, run in case["runs"].items():
+            kw = dict(_CFG[cname])
+            if "workers" in kw:  # reference workers=1 == one block
+                kw["workers"] = 1
+            r = vc.solve(g, vc.SolverConfig(check_registry=True, **kw))
+            assert r.cover_size == run["cover_size"], (case["name"], cname)
+            assert r.found == run["found"]
+            assert stats_without_time(r.stats.as_dict()) == run["stats"], (case["name"], cname)
+            if r.registry is not None:
+                assert r.registry.quiescence_violations() == []
+        for k, exp in case["pvc"].items():
+            r = vc.solve(g, vc.SolverConfig(mode="pvc", k=int(k), deterministic=True))
+            assert r.found == exp["found"], (case["name"], k)
+            assert r.cover_size == exp["cover_size"]
+            assert stats_without_time(r.stats.as_dict()) == exp["stats"], (case["name"], k)
+
+
+def test_parallel_solve_answers_match_reference():
+    import paper_2512_18334_b200 as vc
+
+    for case in golden("solve.json"):
+        g = _graph(case)
+        want = case["runs"]["det"]["cover_size"]
+        r = vc.solve(g, vc.SolverConfig(check_registry=True))
+        assert r.cover_size == want, case["name"]
+        assert r.exact
+        if r.registry is not None:
+            assert r.registry.quiescence_violations() == []
+        for k, exp in case["pvc"].items():
+            r = vc.solve(g, vc.SolverConfig(mode="pvc", k=int(k)))
+            assert r.found == exp["found"], (case["name"], k)
+            if exp["found"]:
+                assert r.cover_size <= int(k)
+
+
+@pytest.mark.parametrize("name", ["er200", "rgg2000"])
+def test_workloads_match_reference(name):
+    import paper_2512_18334_b200 as vc
+    from paper_2512_18334_b200 import synth
+
+    exp = golden("workloads.json")[name]
+    n, off, nbr = synth.WORKLOADS[name]()
+    g = vc.StaticGraph(n, off, nbr)
+    r = vc.solve(g, vc.SolverConfig(deterministic=True))
+    assert r.cover_size == exp["mvc"]
+    assert stats_without_time(r.stats.as_dict()) == exp["stats"]
+    r = vc.solve(g, vc.SolverConfig(check_registry=True))
+    assert r.cover_size == exp["mvc"]
+    assert r.registry.quiescence_violations() == []
+    for k, e in exp["pvc"].items():
+        r = vc.solve(g, vc.SolverConfig(mode="pvc", k=int(k)))
+        assert r.found == e["found"], k
