@@ -115,6 +115,9 @@ typedef struct {
   double kernel_ms;           /* device time of the search kernel (CUDA events) */
   int workers;
   int threads;
+  int64_t records_loaded;     /* node records read from HBM (stack + worklist pops) */
+  int64_t records_stored;     /* node records written to HBM (children offloaded) */
+  int64_t slot_bytes;         /* bytes per node record (32 B header + degree array) */
 } vcg_search_result;
 
 /* Run the persistent search kernel.  hist_out (nullable, capacity n+2)
@@ -134,7 +137,11 @@ int vcg_node_op(int op, int width, int64_t n, const int64_t* offsets, const int3
                 int64_t pos, int64_t* ret);
 
 const char* vcg_last_error(void);
+/* Number of kernels this library has launched so far (process-wide). */
+int64_t vcg_launch_count(void);
 int vcg_device_count(void);
+/* Make `device` current for this thread's subsequent calls. */
+int vcg_set_device(int device);
 /* Device time in ms of the last vcg_root_reduce phases etc. is in the structs. */
 
 #ifdef __cplusplus

@@ -48,13 +48,15 @@ class SearchResult_t(C.Structure):
         ("worklist_pushes", I64), ("worklist_pops", I64), ("max_stack_depth", I64),
         ("rule_counts", I64 * 6), ("registry_entries", I64), ("registry_violations", I64),
         ("kernel_ms", C.c_double), ("workers", C.c_int), ("threads", C.c_int),
+        ("records_loaded", I64), ("records_stored", I64), ("slot_bytes", I64),
     ]
 
 
 EXPORTS = (
     "vcg_graph_create", "vcg_graph_destroy", "vcg_graph_num_vertices", "vcg_graph_num_edges",
     "vcg_graph_download", "vcg_induced_subgraph", "vcg_greedy_bound", "vcg_root_reduce",
-    "vcg_search", "vcg_node_op", "vcg_last_error", "vcg_device_count",
+    "vcg_search", "vcg_node_op", "vcg_last_error", "vcg_device_count", "vcg_launch_count",
+    "vcg_set_device",
 )
 
 
@@ -77,6 +79,7 @@ def _load():
     lib.vcg_last_error.restype = C.c_char_p
     lib.vcg_graph_num_vertices.restype = I64
     lib.vcg_graph_num_edges.restype = I64
+    lib.vcg_launch_count.restype = I64
     lib.vcg_graph_create.argtypes = [I64, P, P, C.POINTER(P)]
     lib.vcg_graph_destroy.argtypes = [P]
     lib.vcg_graph_num_vertices.argtypes = [P]
@@ -102,3 +105,12 @@ def check(rc: int) -> None:
 
 def device_count() -> int:
     return int(lib.vcg_device_count())
+
+
+def launch_count() -> int:
+    """Kernels launched by the library so far in this process."""
+    return int(lib.vcg_launch_count())
+
+
+def set_device(device: int) -> None:
+    check(lib.vcg_set_device(int(device)))

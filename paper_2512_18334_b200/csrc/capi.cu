@@ -25,6 +25,10 @@ __global__ void queue_init_kernel(unsigned long long* seq, long long cap);
 }  // namespace vcg
 
 static thread_local std::string g_err;
+static unsigned long long g_launches = 0;  // kernels this library launched
+#define COUNT_LAUNCH(k) (g_launches += (k))
+
+extern "C" int64_t vcg_launch_count(void) { return (int64_t)g_launches; }
 
 static int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -44,6 +48,11 @@ extern "C" int vcg_device_count(void) {
   int c = 0;
   if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
   return c;
+}
+
+extern "C" int vcg_set_device(int device) {
+  if (cudaSetDevice(device) != cudaSuccess) return fail(VCG_ENODEV, "cudaSetDevice failed");
+  return 0;
 }
 
 static int need_device() {
@@ -204,6 +213,7 @@ static int exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t count, De
   size_t bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int)count);
   if (tmp.ensure(bytes)) return VCG_ERESOURCE;
+  COUNT_LAUNCH(2);  // cub single-pass scan: init + scan kernels
   CK(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, (int)count));
   return 0;
 }
@@ -223,6 +233,7 @@ static int compact_flagged(const vcg_graph* g, DevBuf& flag, vcg_graph** out,
   const int blocks = (int)std::min<int64_t>(((int64_t)n * 32 + threads - 1) / threads, 148 * 16);
   CK(cudaMemset(cnt.p, 0, (size_t)(nk + 1) * 4));
   if (n) {
+    COUNT_LAUNCH(1);
     k_count_kept<<<blocks > 0 ? blocks : 1, threads>>>(n, g->d_off.as<int32_t>(),
                                                        g->d_nbr.as<int32_t>(), flag.as<int32_t>(),
                                                        newid.as<int32_t>(), vmap.as<int32_t>(),
@@ -247,6 +258,7 @@ static int compact_flagged(const vcg_graph* g, DevBuf& flag, vcg_graph** out,
     return VCG_ERESOURCE;
   }
   if (n && nk) {
+    COUNT_LAUNCH(1);
     k_gather_kept<<<blocks > 0 ? blocks : 1, threads>>>(
         n, g->d_off.as<int32_t>(), g->d_nbr.as<int32_t>(), flag.as<int32_t>(),
         newid.as<int32_t>(), r->d_off.as<int32_t>(), r->d_nbr.as<int32_t>());
@@ -277,6 +289,7 @@ extern "C" int vcg_induced_subgraph(const vcg_graph* g, const int64_t* keep, int
   CK(cudaMemset(flag.p, 0, (size_t)(g->n + 1) * 4));
   if (nkeep) {
     CK(cudaMemcpy(dkeep.p, keep, nkeep * 8, cudaMemcpyHostToDevice));
+    COUNT_LAUNCH(1);
     k_flag_from_list<<<(int)std::min<int64_t>((nkeep + 255) / 256, 4096), 256>>>(
         dkeep.as<int64_t>(), nkeep, flag.as<int32_t>());
     CK(cudaGetLastError());
@@ -406,6 +419,7 @@ static int node_op_t(int op, int64_t n, const int64_t* offsets, const int32_t* n
   if (m2) CK(cudaMemcpy(dnbr.p, neighbors, m2 * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ddeg.p, degt.data(), n * sizeof(T), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dout.p, out, ocap * 4, cudaMemcpyHostToDevice));
+  COUNT_LAUNCH(1);
   k_node_op<T><<<1, 128>>>(op, (int)n, doff.as<int32_t>(), dnbr.as<int32_t>(), ddeg.as<T>(),
                            dws.as<char>(), (int)lo, (int)hi, (int)budget, (int)v,
                            dout.as<int32_t>(), (int)pos, dret.as<long long>());
@@ -513,6 +527,7 @@ extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int h
       int64_t progressed = 0;
       auto t0 = std::chrono::steady_clock::now();
       long long ret[8];
+      COUNT_LAUNCH(1);
       k_root_fixpoint<<<1, 1024>>>(n, g->d_off.as<int32_t>(), g->d_nbr.as<int32_t>(),
                                    ws.as<char>(), lo, hi, (int)(bound0 - forced_count),
                                    dout.as<int32_t>(), 0, dret.as<long long>(), first);
@@ -567,6 +582,7 @@ extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int h
     (void)pos;
     if (forced_out)
       for (size_t i = 0; i < forced.size(); ++i) forced_out[i] = forced[i];
+    COUNT_LAUNCH(1);
     k_flags_from_deg<<<(n + 256) / 256 + 1, 256>>>(ws.as<uint32_t>(), n, flag.as<int32_t>());
     CK(cudaGetLastError());
   }
@@ -714,6 +730,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   CK(cudaMemset(C.qctl.p, 0, 64));
   CK(cudaMemset(C.ctl.p, 0, sizeof(Ctl)));
   CK(cudaMemset(C.hist.p, 0, (size_t)(n + 2) * 8));
+  COUNT_LAUNCH(1);
   queue_init_kernel<<<256, 256>>>(P.q.seq, qcap);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
@@ -728,6 +745,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
     unsigned long long now = 0;
     DevBuf t;
     if (t.ensure(8)) return VCG_ERESOURCE;
+    COUNT_LAUNCH(1);
     k_read_timer<<<1, 1>>>(t.as<unsigned long long>());
     CK(cudaMemcpy(&now, t.p, 8, cudaMemcpyDeviceToHost));
     P.deadline_ns = now + (unsigned long long)(limit * 1e9);
@@ -737,6 +755,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
+  COUNT_LAUNCH(2);  // search + drain
   search_kernel<T><<<blocks, threads, dsmem>>>(P);
   cudaEventRecord(e1);
   cudaError_t le = cudaGetLastError();
@@ -769,6 +788,9 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   res->kernel_ms = ms;
   res->workers = blocks;
   res->threads = threads;
+  res->records_loaded = (int64_t)ctl.rec_in;
+  res->records_stored = (int64_t)ctl.rec_out;
+  res->slot_bytes = slot;
   if (hist_out) {
     std::vector<unsigned long long> h(n + 2);
     CK(cudaMemcpy(h.data(), C.hist.p, (size_t)(n + 2) * 8, cudaMemcpyDeviceToHost));

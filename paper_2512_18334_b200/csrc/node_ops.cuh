@@ -587,6 +587,12 @@ __device__ int remove_vertex(const NodeWs<T>& w, int v) {
 template <typename T>
 __device__ void remove_neighbors(const NodeWs<T>& w, int v, int* out, int pos, int* removed,
                                  int* edges) {
+  if (w.deg[v] == 0) {  // pure.py:55: a dead vertex has no live neighbours to force
+    *removed = 0;
+    *edges = 0;
+    __syncthreads();
+    return;
+  }
   const int b = w.off[v], e = w.off[v + 1];
   // compact live neighbours (adjacency order) into out
   int cb, ce;

@@ -24,11 +24,12 @@ struct Worker {
   char* my_stack;
   int top;   // block-uniform private stack height
   // thread-0 statistics
-  unsigned long long nodes, comp_branches, pushes, pops, rules[6];
+  unsigned long long nodes, comp_branches, pushes, pops, rules[6], rec_in, rec_out;
   int max_depth;
 
   __device__ Worker(const SearchParams& p, NodeWs<T> ws, BlockState* s)
-      : P(p), w(ws), st(s), top(0), nodes(0), comp_branches(0), pushes(0), pops(0), max_depth(0) {
+      : P(p), w(ws), st(s), top(0), nodes(0), comp_branches(0), pushes(0), pops(0), rec_in(0),
+        rec_out(0), max_depth(0) {
     for (int i = 0; i < 6; ++i) rules[i] = 0;
     my_stack = P.stacks + (long long)blockIdx.x * P.stack_cap * P.slot_bytes;
   }
@@ -68,7 +69,10 @@ struct Worker {
   }
 
   __device__ void commit_dest(long long qpos, const NodeHdr& h, char* dst) {
-    if (threadIdx.x == 0 && dst) *(NodeHdr*)dst = h;
+    if (threadIdx.x == 0 && dst) {
+      *(NodeHdr*)dst = h;
+      ++rec_out;
+    }
     __syncthreads();
     if (qpos >= 0) {
       if (threadIdx.x == 0) {
@@ -302,6 +306,8 @@ struct Worker {
     atomicAdd(&c->pops, pops);
     for (int i = 0; i < 6; ++i) atomicAdd(&c->rules[i], rules[i]);
     atomicMax(&c->max_depth, max_depth);
+    atomicAdd(&c->rec_in, rec_in);
+    atomicAdd(&c->rec_out, rec_out);
   }
 };
 
@@ -345,6 +351,7 @@ __global__ void __launch_bounds__(1024) search_kernel(SearchParams P) {
       if (wk.top > 0) {
         wk.top -= 1;
         load_node<T>(wk.stack_slot(wk.top), &st.hdr, ws.deg, P.n);
+        if (threadIdx.x == 0) ++wk.rec_in;
         __syncthreads();
       } else {
         if (threadIdx.x == 0) {
@@ -366,6 +373,7 @@ __global__ void __launch_bounds__(1024) search_kernel(SearchParams P) {
         if (threadIdx.x == 0) {
           q_release_pop(P.q, pos);
           ++wk.pops;
+          ++wk.rec_in;
         }
       }
     }

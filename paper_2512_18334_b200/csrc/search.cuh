@@ -46,6 +46,7 @@ struct Ctl {
   int max_depth, pad0, pad1, pad2;
   unsigned long long nodes, comp_branches, pushes, pops;
   unsigned long long rules[6];  // degree_one, d2t, high_degree, crown, clique, cycle
+  unsigned long long rec_in, rec_out;  // node records read from / written to HBM
 };
 
 struct Queue {
