@@ -21,7 +21,7 @@ namespace vcg {
 template <typename T>
 __global__ void search_kernel(SearchParams P);
 __global__ void drain_kernel(SearchParams P);
-__global__ void queue_init_kernel(unsigned long long* seq, long long cap);
+__global__ void search_init_kernel(SearchParams P, int root_key, unsigned long long timeout_ns);
 }  // namespace vcg
 
 static thread_local std::string g_err;
@@ -605,7 +605,6 @@ extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int h
 
 // ----------------------------------------------------------------- search --
 
-__global__ void k_read_timer(unsigned long long* t) { *t = globaltimer(); }
 
 template <typename T>
 static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_search_result* res,
@@ -697,13 +696,6 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   P.root_in_stack = 1;
 
   // root scope entry + root node record (engine.py:183-188)
-  int root_fields[12] = {0};
-  root_fields[0] = (int)(cfg->best_init * 2 + (cfg->best_init_achieved ? 0 : 1));  // key
-  root_fields[1] = 1;    // live
-  root_fields[2] = -1;   // link
-  for (int f = 0; f < 12; ++f) CK(cudaMemcpy(rb + (size_t)f * reg_cap, &root_fields[f], 4, cudaMemcpyHostToDevice));
-  int one = 1;
-  CK(cudaMemcpy(R.count, &one, 4, cudaMemcpyHostToDevice));
   std::vector<char> rec(slot, 0);
   NodeHdr* hh = (NodeHdr*)rec.data();
   T* rdeg = (T*)(rec.data() + sizeof(NodeHdr));
@@ -726,34 +718,24 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   hh->hi = hi;
   hh->scope = 0;
   hh->depth = 0;
-  CK(cudaMemcpy(C.stacks.p, rec.data(), slot, cudaMemcpyHostToDevice));
-  CK(cudaMemset(C.qctl.p, 0, 64));
-  CK(cudaMemset(C.ctl.p, 0, sizeof(Ctl)));
-  CK(cudaMemset(C.hist.p, 0, (size_t)(n + 2) * 8));
-  COUNT_LAUNCH(1);
-  queue_init_kernel<<<256, 256>>>(P.q.seq, qcap);
-  CK(cudaGetLastError());
-  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpyAsync(C.stacks.p, rec.data(), slot, cudaMemcpyHostToDevice, 0));
   double limit = cfg->timeout;
   if (limit <= 0) {
     // safety watchdog for test/bench runs: a protocol bug must not hang the GPU
     const char* wd = getenv("VCG_WATCHDOG_S");
     if (wd) limit = atof(wd);
   }
-  if (limit > 0) {
-    // %globaltimer is ns since an arbitrary epoch: read it on the device
-    unsigned long long now = 0;
-    DevBuf t;
-    if (t.ensure(8)) return VCG_ERESOURCE;
-    COUNT_LAUNCH(1);
-    k_read_timer<<<1, 1>>>(t.as<unsigned long long>());
-    CK(cudaMemcpy(&now, t.p, 8, cudaMemcpyDeviceToHost));
-    P.deadline_ns = now + (unsigned long long)(limit * 1e9);
-  }
+  const unsigned long long timeout_ns = limit > 0 ? (unsigned long long)(limit * 1e9) : 0ull;
+  const int root_key = (int)(cfg->best_init * 2 + (cfg->best_init_achieved ? 0 : 1));
+  COUNT_LAUNCH(1);
+  search_init_kernel<<<256, 256>>>(P, root_key, timeout_ns);
+  CK(cudaGetLastError());
 
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
+  static cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (!e0) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+  }
   cudaEventRecord(e0);
   COUNT_LAUNCH(2);  // search + drain
   search_kernel<T><<<blocks, threads, dsmem>>>(P);
@@ -764,17 +746,13 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   CK(cudaDeviceSynchronize());
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
 
   Ctl ctl;
   CK(cudaMemcpy(&ctl, C.ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost));
-  int root_key = 0, count = 0;
-  CK(cudaMemcpy(&root_key, R.key, 4, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(&count, R.count, 4, cudaMemcpyDeviceToHost));
+  const int final_key = ctl.root_key, count = ctl.reg_count;
   memset(res, 0, sizeof(*res));
-  res->best = root_key >> 1;
-  res->best_achieved = !(root_key & 1);
+  res->best = final_key >> 1;
+  res->best_achieved = !(final_key & 1);
   res->found = ctl.found;
   res->timed_out = ctl.timed_out;
   res->error = ctl.error;

@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(1024) search_kernel(SearchParams P) {
   while (true) {
     if (threadIdx.x == 0) {
       int stop = ld_relaxed(&P.ctl->stop);
-      if (!stop && P.deadline_ns && globaltimer() > P.deadline_ns) {
+      if (!stop && P.ctl->deadline_ns && globaltimer() > P.ctl->deadline_ns) {
         atomicExch(&P.ctl->timed_out, 1);
         atomicExch(&P.ctl->stop, 1);
         stop = 1;
@@ -386,11 +386,22 @@ __global__ void __launch_bounds__(1024) search_kernel(SearchParams P) {
       const NodeHdr* hh = (const NodeHdr*)wk.stack_slot(i);
       reg_finish(P, __ldcg(&hh->scope));
     }
+    // every block helps empty the worklist (the host drain kernel only picks
+    // up records pushed by blocks that were still finishing a node)
+    while (true) {
+      long long pos = q_reserve_pop(P.q);
+      if (pos < 0) break;
+      const NodeHdr* hh = (const NodeHdr*)(P.q.data + (pos % P.q.cap) * P.slot_bytes);
+      int scope = __ldcg(&hh->scope);
+      q_release_pop(P.q, pos);
+      reg_finish(P, scope);
+    }
   }
   wk.flush_stats();
 }
 
-// single-block drain of the worklist after the search kernel (engine.py:216)
+// single-thread drain of records pushed after the in-kernel drain
+// (engine.py:216), then publish the result words for one readback
 __global__ void drain_kernel(SearchParams P) {
   if (threadIdx.x != 0) return;
   while (true) {
@@ -401,12 +412,35 @@ __global__ void drain_kernel(SearchParams P) {
     q_release_pop(P.q, pos);
     reg_finish(P, scope);
   }
+  __threadfence();
+  P.ctl->root_key = ld_relaxed(&P.reg.key[P.root_index]);
+  P.ctl->reg_count = ld_relaxed(P.reg.count);
 }
 
-__global__ void queue_init_kernel(unsigned long long* seq, long long cap) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cap;
-       i += (long long)gridDim.x * blockDim.x)
-    seq[i] = (unsigned long long)i;
+// one launch resets every per-solve structure: root registry entry, arena
+// counter, worklist ring, control block (with the deadline) and histogram
+__global__ void search_init_kernel(SearchParams P, int root_key, unsigned long long timeout_ns) {
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < P.q.cap; i += nth) P.q.seq[i] = (unsigned long long)i;
+  for (long long i = tid; i < P.n + 2; i += nth) P.hist[i] = 0ull;
+  if (tid == 0) {
+    const Registry& R = P.reg;
+    const int r = P.root_index;
+    R.key[r] = root_key;
+    R.live[r] = 1;
+    R.link[r] = -1;
+    R.kind[r] = 0;
+    R.sum[r] = R.sum_ach[r] = R.init_sum[r] = R.folded[r] = 0;
+    R.first_child[r] = R.nchild[r] = R.disc_done[r] = R.child_folded[r] = 0;
+    *R.count = 1;
+    *P.q.head = 0ull;
+    *P.q.tail = 0ull;
+    Ctl* c = P.ctl;
+    unsigned long long* cw = (unsigned long long*)c;
+    for (size_t i = 0; i < sizeof(Ctl) / 8; ++i) cw[i] = 0ull;
+    c->deadline_ns = timeout_ns ? globaltimer() + timeout_ns : 0ull;
+  }
 }
 
 template __global__ void search_kernel<uint8_t>(SearchParams);

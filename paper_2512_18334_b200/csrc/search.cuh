@@ -47,6 +47,8 @@ struct Ctl {
   unsigned long long nodes, comp_branches, pushes, pops;
   unsigned long long rules[6];  // degree_one, d2t, high_degree, crown, clique, cycle
   unsigned long long rec_in, rec_out;  // node records read from / written to HBM
+  unsigned long long deadline_ns;      // %globaltimer deadline, 0 = none
+  int root_key, reg_count;             // written by the drain kernel for readback
 };
 
 struct Queue {
@@ -78,7 +80,6 @@ struct SearchParams {
   int k_red;
   int root_index;
   int root_in_stack;
-  unsigned long long deadline_ns;  // 0 = none
 };
 
 template <typename T>
