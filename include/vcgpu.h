@@ -118,6 +118,8 @@ typedef struct {
   int64_t records_loaded;     /* node records read from HBM (stack + worklist pops) */
   int64_t records_stored;     /* node records written to HBM (children offloaded) */
   int64_t slot_bytes;         /* bytes per node record (32 B header + degree array) */
+  int64_t phase_cycles[10];   /* SM cycles summed over blocks: idle, load, reduce, label,
+                                 split, select, exclude, include, registry, other */
 } vcg_search_result;
 
 /* Run the persistent search kernel.  hist_out (nullable, capacity n+2)

@@ -49,7 +49,12 @@ class SearchResult_t(C.Structure):
         ("rule_counts", I64 * 6), ("registry_entries", I64), ("registry_violations", I64),
         ("kernel_ms", C.c_double), ("workers", C.c_int), ("threads", C.c_int),
         ("records_loaded", I64), ("records_stored", I64), ("slot_bytes", I64),
+        ("phase_cycles", I64 * 10),
     ]
+
+
+PHASES = ("idle", "load", "reduce", "label", "split", "select", "exclude", "include",
+          "registry", "other")
 
 
 EXPORTS = (

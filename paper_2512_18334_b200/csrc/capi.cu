@@ -55,6 +55,25 @@ extern "C" int vcg_set_device(int device) {
   return 0;
 }
 
+static bool trace_on() {
+  static int on = -1;
+  if (on < 0) on = getenv("VCG_TRACE") ? 1 : 0;
+  return on == 1;
+}
+struct Tracer {
+  const char* what;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+  explicit Tracer(const char* w) : what(w) {}
+  void mark(const char* step) {
+    if (!trace_on()) return;
+    cudaDeviceSynchronize();
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[vcg %s] %-22s %8.3f ms\n", what, step,
+            std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+  }
+};
+
 static int need_device() {
   int c = 0;
   cudaError_t e = cudaGetDeviceCount(&c);
@@ -611,16 +630,22 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
                     int64_t* hist_out) {
   vcg_graph* g = const_cast<vcg_graph*>(gc);
   SearchCtx& C = search_ctx();
+  Tracer tr("search");
   const int n = (int)g->n;
   int dev = 0;
   CK(cudaGetDevice(&dev));
-  cudaDeviceProp prop;
-  CK(cudaGetDeviceProperties(&prop, dev));
+  // cudaGetDeviceProperties costs tens of ms per call: cache two attributes
+  static int cached_dev = -1, sm_count = 0, smem_optin = 0;
+  if (cached_dev != dev) {
+    CK(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cached_dev = dev;
+  }
 
   int threads = cfg->threads;
   if (threads <= 0) threads = n <= 512 ? 64 : n <= 4096 ? 128 : n <= 32768 ? 256 : 512;
   const long long wsb = ws_total<T>(n);
-  const long long smem_limit = (long long)prop.sharedMemPerBlockOptin - 2048;
+  const long long smem_limit = (long long)smem_optin - 2048;
   const int in_smem = wsb <= smem_limit;
   const size_t dsmem = in_smem ? (size_t)wsb : 0;
   CK(cudaFuncSetAttribute(search_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -628,7 +653,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, search_kernel<T>, threads, dsmem));
   if (per_sm < 1) return fail(VCG_ERESOURCE, "search kernel does not fit on an SM");
-  const int resident = per_sm * prop.multiProcessorCount;
+  const int resident = per_sm * sm_count;
   int blocks = cfg->deterministic ? 1 : (cfg->workers > 0 ? cfg->workers : resident);
   if (blocks > resident) blocks = resident;
 
@@ -640,8 +665,8 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   const int share = cfg->load_balance && !cfg->deterministic;
   long long threshold = cfg->worklist_threshold > 0 ? cfg->worklist_threshold : 2LL * blocks;
   long long qcap = std::max<long long>(4 * threshold + 1024, 4096);
-  const long long q_budget = 8LL << 30;
-  if (qcap * slot > q_budget) qcap = std::max(threshold + 64, q_budget / slot);
+  const long long q_budget = 4LL << 30;
+  if (qcap * slot > q_budget) qcap = std::max(4096LL, q_budget / slot);
   const int reg_cap = (int)std::min<long long>(1LL << 23, std::max<long long>(1LL << 16, (long long)n * 1024));
 
   if (C.stacks.ensure((size_t)(stack_cap * slot * blocks)) || C.qseq.ensure((size_t)qcap * 8) ||
@@ -651,6 +676,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
       (!in_smem && C.gws.ensure((size_t)(wsb * blocks))))
     return VCG_ERESOURCE;
 
+  tr.mark("alloc");
   SearchParams P;
   memset(&P, 0, sizeof(P));
   P.n = n;
@@ -730,6 +756,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   COUNT_LAUNCH(1);
   search_init_kernel<<<256, 256>>>(P, root_key, timeout_ns);
   CK(cudaGetLastError());
+  tr.mark("init");
 
   static cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (!e0) {
@@ -742,8 +769,10 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   cudaEventRecord(e1);
   cudaError_t le = cudaGetLastError();
   if (le != cudaSuccess) return fail(VCG_ECUDA, std::string("search launch: ") + cudaGetErrorString(le));
+  tr.mark("search_kernel");
   drain_kernel<<<1, 32>>>(P);
   CK(cudaDeviceSynchronize());
+  tr.mark("drain");
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
 
@@ -769,11 +798,13 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   res->records_loaded = (int64_t)ctl.rec_in;
   res->records_stored = (int64_t)ctl.rec_out;
   res->slot_bytes = slot;
+  for (int i = 0; i < 10; ++i) res->phase_cycles[i] = (int64_t)ctl.phase[i];
   if (hist_out) {
     std::vector<unsigned long long> h(n + 2);
     CK(cudaMemcpy(h.data(), C.hist.p, (size_t)(n + 2) * 8, cudaMemcpyDeviceToHost));
     for (int i = 0; i < n + 2; ++i) hist_out[i] = (int64_t)h[i];
   }
+  tr.mark("readback");
   if (cfg->check_registry && count > 0) {
     // registry quiescence + conservation (SPEC registry invariants)
     std::vector<int> f[12];

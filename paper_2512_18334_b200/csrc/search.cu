@@ -26,11 +26,23 @@ struct Worker {
   // thread-0 statistics
   unsigned long long nodes, comp_branches, pushes, pops, rules[6], rec_in, rec_out;
   int max_depth;
+  unsigned long long ph[10];
+  long long last_clk;
+
+  __device__ void tick(int phase) {
+    if (threadIdx.x == 0) {
+      long long now = clock64();
+      ph[phase] += (unsigned long long)(now - last_clk);
+      last_clk = now;
+    }
+  }
 
   __device__ Worker(const SearchParams& p, NodeWs<T> ws, BlockState* s)
       : P(p), w(ws), st(s), top(0), nodes(0), comp_branches(0), pushes(0), pops(0), rec_in(0),
         rec_out(0), max_depth(0) {
     for (int i = 0; i < 6; ++i) rules[i] = 0;
+    for (int i = 0; i < 10; ++i) ph[i] = 0;
+    last_clk = clock64();
     my_stack = P.stacks + (long long)blockIdx.x * P.stack_cap * P.slot_bytes;
   }
 
@@ -92,6 +104,7 @@ struct Worker {
     const int lo = h.lo, hi = h.hi;
     int ncomp = label_components(w, lo, hi);
     if (ncomp <= 1) return false;
+    tick(PH_LABEL);
     int* agg = w.ib;
     component_aggregates(w, lo, hi, ncomp, agg);
     if (threadIdx.x == 0) {
@@ -201,6 +214,7 @@ struct Worker {
     }
     if (threadIdx.x == 0) reg_finish(P, h.scope);
     __syncthreads();
+    tick(PH_SPLIT);
     return true;
   }
 
@@ -214,9 +228,11 @@ struct Worker {
       st->best_s = ld_relaxed(&P.reg.key[h.scope]) >> 1;
     }
     __syncthreads();
+    tick(PH_REGISTRY);
     const int best_s = st->best_s;
     const int budget = best_s - h.S - 1;
     FixRet fr = reduce_fixpoint(w, h.lo, h.hi, budget, w.id, 0);
+    tick(PH_REDUCE);
     if (threadIdx.x == 0) {
       rules[0] += fr.d1;
       rules[1] += fr.d2t;
@@ -246,6 +262,7 @@ struct Worker {
       if (prune) {
         if (threadIdx.x == 0) reg_finish(P, h.scope);
         __syncthreads();
+        tick(PH_REGISTRY);
         return false;
       }
     }
@@ -255,10 +272,13 @@ struct Worker {
         reg_finish(P, h.scope);
       }
       __syncthreads();
+      tick(PH_REGISTRY);
       return false;
     }
     if (P.use_components && try_split()) return false;
+    tick(PH_LABEL);
     const int v = select_max_degree(w, lo, hi);
+    tick(PH_SELECT);
     if (v < 0) {
       if (threadIdx.x == 0) {
         atomicExch(&P.ctl->error, 3);
@@ -286,6 +306,7 @@ struct Worker {
       commit_dest(qpos, ex, dst);
     }
     __syncthreads();
+    tick(PH_EXCLUDE);
     int e2 = remove_vertex(w, v);
     if (threadIdx.x == 0) {
       h.S = S + 1;
@@ -294,6 +315,7 @@ struct Worker {
       if (top + 1 > max_depth) max_depth = top + 1;
     }
     __syncthreads();
+    tick(PH_INCLUDE);
     return true;
   }
 
@@ -308,11 +330,12 @@ struct Worker {
     atomicMax(&c->max_depth, max_depth);
     atomicAdd(&c->rec_in, rec_in);
     atomicAdd(&c->rec_out, rec_out);
+    for (int i = 0; i < 10; ++i) atomicAdd(&c->phase[i], ph[i]);
   }
 };
 
 template <typename T>
-__global__ void __launch_bounds__(1024) search_kernel(SearchParams P) {
+__global__ void __launch_bounds__(512, 1) search_kernel(SearchParams P) {
   extern __shared__ __align__(16) unsigned char dsmem[];
   __shared__ BlockScratch bs;
   __shared__ BlockState st;
@@ -347,6 +370,7 @@ __global__ void __launch_bounds__(1024) search_kernel(SearchParams P) {
     }
     __syncthreads();
     if (st.flag) break;
+    wk.tick(PH_OTHER);
     if (!cont) {
       if (wk.top > 0) {
         wk.top -= 1;
@@ -365,6 +389,7 @@ __global__ void __launch_bounds__(1024) search_kernel(SearchParams P) {
           if (threadIdx.x == 0) __nanosleep(backoff);
           backoff = backoff < 4096 ? backoff * 2 : 4096;
           __syncthreads();
+          wk.tick(PH_IDLE);
           continue;
         }
         backoff = 32;
@@ -377,6 +402,7 @@ __global__ void __launch_bounds__(1024) search_kernel(SearchParams P) {
         }
       }
     }
+    wk.tick(PH_LOAD);
     cont = wk.process();
   }
   // stop: release the registry slots of abandoned work (engine.py:235-243)

@@ -49,7 +49,12 @@ struct Ctl {
   unsigned long long rec_in, rec_out;  // node records read from / written to HBM
   unsigned long long deadline_ns;      // %globaltimer deadline, 0 = none
   int root_key, reg_count;             // written by the drain kernel for readback
+  unsigned long long phase[10];        // SM cycles per phase, summed over blocks (thread 0)
 };
+
+// phases of a block's time (clock64 deltas taken by thread 0)
+enum Phase { PH_IDLE = 0, PH_LOAD, PH_REDUCE, PH_LABEL, PH_SPLIT, PH_SELECT, PH_EXCLUDE,
+             PH_INCLUDE, PH_REGISTRY, PH_OTHER };
 
 struct Queue {
   unsigned long long* seq;

@@ -137,6 +137,7 @@ class SolveResult:
     root_index: int | None = None
     forced: list[int] = field(default_factory=list)
     search_ms: float = 0.0  # device time of the search kernel
+    phase_cycles: dict = field(default_factory=dict)  # block time by phase (SM cycles)
 
 
 def run_search(rg: StaticGraph, cfg: SolverConfig, width: int, best_init: int,
@@ -235,6 +236,7 @@ def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
     res, hist = run_search(rg, cfg, pre.width, best_init, achieved_init, k_red)
     stats.phase_seconds["search"] = time.perf_counter() - t1
     result.search_ms = float(res.kernel_ms)
+    result.phase_cycles = dict(zip(_lib.PHASES, (int(x) for x in res.phase_cycles)))
     stats.tree_nodes_visited = int(res.tree_nodes_visited)
     stats.component_branches = int(res.component_branches)
     stats.components_per_branch = hist
