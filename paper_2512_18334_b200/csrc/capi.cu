@@ -643,11 +643,13 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   }
 
   int threads = cfg->threads;
-  if (threads <= 0) threads = n <= 512 ? 64 : n <= 4096 ? 128 : n <= 32768 ? 256 : 512;
+  if (threads <= 0) threads = n <= 256 ? 64 : n <= 512 ? 128 : n <= 32768 ? 256 : 512;
   const long long wsb = ws_total<T>(n);
   const long long smem_limit = (long long)smem_optin - 2048;
   const int in_smem = wsb <= smem_limit;
-  const size_t dsmem = in_smem ? (size_t)wsb : 0;
+  const long long csrb = csr_smem_bytes(n, g->m2);
+  const int csr_smem = in_smem && wsb + csrb <= smem_limit && !getenv("VCG_NO_SMEM_CSR");
+  const size_t dsmem = in_smem ? (size_t)(wsb + (csr_smem ? csrb : 0)) : 0;
   CK(cudaFuncSetAttribute(search_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)dsmem));
   int per_sm = 0;
@@ -680,6 +682,8 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   SearchParams P;
   memset(&P, 0, sizeof(P));
   P.n = n;
+  P.m2 = g->m2;
+  P.csr_in_smem = csr_smem;
   P.off = g->d_off.as<int32_t>();
   P.nbr = g->d_nbr.as<int32_t>();
   P.stacks = C.stacks.as<char>();
@@ -688,6 +692,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   P.q.seq = C.qseq.as<unsigned long long>();
   P.q.head = C.qctl.as<unsigned long long>();
   P.q.tail = C.qctl.as<unsigned long long>() + 1;
+  P.q.count = C.qctl.as<unsigned long long>() + 2;
   P.q.data = C.qdata.as<char>();
   P.q.cap = qcap;
   int* rb = C.reg.as<int>();

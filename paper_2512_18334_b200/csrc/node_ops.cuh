@@ -202,6 +202,7 @@ __device__ __forceinline__ void my_chunk(int lo, int hi, int* b, int* e) {
 template <typename T>
 struct NodeWs {
   T* deg;           // current node degree array [n] (4-byte aligned)
+  T* deg2;          // second degree buffer [n] (exclude child under construction)
   int* tmin;        // [n], kept == kInf between operations
   int* ia;          // [n] int scratch
   int* ib;          // [n]
@@ -610,6 +611,193 @@ __device__ void remove_neighbors(const NodeWs<T>& w, int v, int* out, int pos, i
   }
   __syncthreads();
   *edges = remove_list(w, out + pos, total);
+  *removed = total;
+}
+
+// ---------------------------------------------------------------------------
+// search-path variants: same forced SETS and counters as the ordered sweeps
+// above (so every statistic is unchanged), but the forced ids are appended in
+// arbitrary order -- the search only needs the counts -- which removes one
+// block scan per sweep, and the candidate counts of all three rules come from
+// one fused pass over the window.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void block_scan3(int a, int b, int c, BlockScratch* bs, int* a_before,
+                                            int* ta, int* tb, int* tc) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  int inc = a;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  int sb = warp_sum(b), sc = warp_sum(c);
+  __syncthreads();
+  if (lane == 31 || (int)threadIdx.x == (int)blockDim.x - 1) bs->v[wid] = inc;
+  if (lane == 0) {
+    bs->w[wid] = ((long long)sb << 32) | (unsigned)sc;
+  }
+  if (threadIdx.x == 0) bs->bc[8] = 0;  // append counter for the pass that follows
+  __syncthreads();
+  int before = 0, tot = 0;
+  long long t2 = 0, t3 = 0;
+  for (int i = 0; i < nw; ++i) {
+    int s = bs->v[i];
+    if (i < wid) before += s;
+    tot += s;
+    t2 += (int)(bs->w[i] >> 32);
+    t3 += (int)(bs->w[i] & 0xffffffffLL);
+  }
+  *a_before = before + inc - a;
+  *ta = tot;
+  *tb = (int)t2;
+  *tc = (int)t3;
+}
+
+template <typename T>
+__device__ __forceinline__ void deg_zero(T* deg, int x) {
+  if constexpr (sizeof(T) == 4) {
+    atomicExch((unsigned*)(deg + x), 0u);
+  } else {
+    uintptr_t a = (uintptr_t)(deg + x);
+    unsigned* w = (unsigned*)(a & ~(uintptr_t)3);
+    unsigned sh = (unsigned)(a & 3) * 8u;
+    unsigned mask = (sizeof(T) == 1 ? 0xffu : 0xffffu) << sh;
+    atomicAnd(w, ~mask);
+  }
+}
+
+// Remove the vertices list[0, cnt) (all flagged 1, all live) together.
+// Each remover zeroes its own entry atomically (flagged entries are never
+// decremented by others); flags are cleared after the barrier inside the
+// block_sum, before any later reader (every later reader is behind a barrier).
+template <typename T>
+__device__ __forceinline__ int remove_list_fast(const NodeWs<T>& w, const int* list, int cnt) {
+  int edges = 0;
+  for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
+    const int u = list[k];
+    const int b = w.off[u], end = w.off[u + 1];
+    for (int i = b; i < end; ++i) {
+      int x = w.nbr[i];
+      if (w.flag[x] == 1) {
+        if (x > u) ++edges;
+      } else if (ldv(w.deg, x) > 0) {
+        deg_dec(w.deg, x);
+        ++edges;
+      }
+    }
+    deg_zero(w.deg, u);
+  }
+  edges = block_sum(edges, w.bs);
+  for (int k = threadIdx.x; k < cnt; k += blockDim.x) w.flag[list[k]] = 0;
+  return edges;
+}
+
+// degree-one sweep with the candidate count/offsets already known
+template <typename T>
+__device__ PassRet degree_one_pass_fast(const NodeWs<T>& w, int b, int e, int at, int ncand,
+                                        int* rem) {
+  for (int v = b; v < e; ++v) {
+    if (w.deg[v] == 1) {
+      int u = -1;
+      for (int i = w.off[v]; i < w.off[v + 1]; ++i) {
+        int x = w.nbr[i];
+        if (w.deg[x] > 0) {
+          u = x;
+          break;
+        }
+      }
+      w.ia[v] = u;
+      w.lst[at++] = v;
+      atomicMin(&w.tmin[u], v);
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < ncand; k += blockDim.x) {
+    int v = w.lst[k];
+    int u = w.ia[v];
+    if ((w.tmin[u] == v) && !(w.deg[u] == 1 && w.ia[u] == v && u < v)) {
+      w.flag[u] = 1;
+      rem[atomicAdd(&w.bs->bc[8], 1)] = u;
+    }
+  }
+  __syncthreads();
+  const int total = w.bs->bc[8];
+  int edges = remove_list_fast(w, rem, total);
+  for (int k = threadIdx.x; k < ncand; k += blockDim.x) w.tmin[w.ia[w.lst[k]]] = kInf;
+  return PassRet{total, total, edges, 0};
+}
+
+// reduce_fixpoint (pure.py:188) for the search: identical forced sets and
+// counters; one fused scan decides which sweeps have candidates.
+template <typename T>
+__device__ FixRet reduce_fixpoint_fast(const NodeWs<T>& w, int lo, int hi, int budget) {
+  FixRet r{0, 0, 0, 0, 0, lo, hi, 0};
+  int b, e;
+  my_chunk(lo, hi, &b, &e);
+  int* rem = w.id;
+  while (true) {
+    int cycle = 0;
+    int c1 = 0, c2 = 0, ch = 0;
+    while (true) {
+      const int bud = budget - r.forced;
+      int t1 = 0, t2 = 0, th = 0;
+      for (int v = b; v < e; ++v) {
+        int d = w.deg[v];
+        t1 += (d == 1);
+        t2 += (d == 2);
+        th += (d > 0 && d > bud);
+      }
+      int at1;
+      block_scan3(t1, t2, th, w.bs, &at1, &c1, &c2, &ch);
+      if (c1 == 0) break;
+      PassRet a = degree_one_pass_fast(w, b, e, at1, c1, rem);
+      r.d1 += a.applied;
+      r.forced += a.forced;
+      r.edges += a.edges;
+      cycle += a.applied;
+    }
+    int tri = 0;
+    if (c2 > 0) {
+      PassRet t = degree_two_triangle_pass(w, lo, hi, rem, 0);
+      tri = t.applied;
+      r.d2t += t.applied;
+      r.forced += t.forced;
+      r.edges += t.edges;
+      cycle += t.applied;
+    }
+    if (tri > 0 || ch > 0) {
+      PassRet h = high_degree_pass(w, lo, hi, budget - r.forced, rem, 0);
+      r.hd += h.applied;
+      r.forced += h.forced;
+      r.edges += h.edges;
+      cycle += h.applied;
+    }
+    if (cycle == 0) break;
+  }
+  int l = lo, h = hi;
+  recompute_bounds(w, &l, &h);
+  r.lo = l;
+  r.hi = h;
+  return r;
+}
+
+// remove_neighbors (pure.py:47) for the search: forced set and counters only
+template <typename T>
+__device__ void remove_neighbors_fast(const NodeWs<T>& w, int v, int* rem, int* removed,
+                                      int* edges) {
+  if (threadIdx.x == 0) w.bs->bc[8] = 0;
+  __syncthreads();
+  for (int j = w.off[v] + threadIdx.x; j < w.off[v + 1]; j += blockDim.x) {
+    int x = w.nbr[j];
+    if (w.deg[x] > 0) {
+      w.flag[x] = 1;
+      rem[atomicAdd(&w.bs->bc[8], 1)] = x;
+    }
+  }
+  __syncthreads();
+  const int total = w.bs->bc[8];
+  *edges = remove_list_fast(w, rem, total);
   *removed = total;
 }
 

@@ -56,11 +56,11 @@ struct Worker {
   __device__ char* choose_dest(long long* qpos) {
     if (threadIdx.x == 0) {
       long long pos = -1;
-      if (P.share && q_length(P.q) < P.threshold) pos = q_reserve_push(P.q);
+      if (P.share) pos = q_reserve_push(P.q, P.threshold);
       if (pos < 0 && top >= P.stack_cap) {
         // private stack full: the worklist must take it (SPEC offloadOrPush)
         unsigned spins = 0;
-        while ((pos = q_reserve_push(P.q)) < 0) {
+        while ((pos = q_reserve_push(P.q, P.q.cap)) < 0) {
           __nanosleep(256);
           if (++spins > (1u << 24)) {
             atomicExch(&P.ctl->error, 2);
@@ -231,7 +231,7 @@ struct Worker {
     tick(PH_REGISTRY);
     const int best_s = st->best_s;
     const int budget = best_s - h.S - 1;
-    FixRet fr = reduce_fixpoint(w, h.lo, h.hi, budget, w.id, 0);
+    FixRet fr = reduce_fixpoint_fast(w, h.lo, h.hi, budget);
     tick(PH_REDUCE);
     if (threadIdx.x == 0) {
       rules[0] += fr.d1;
@@ -289,16 +289,22 @@ struct Worker {
     }
     // engine.py:319 _branch_on_vertex
     if (threadIdx.x == 0) atomicAdd(&P.reg.live[h.scope], 1);
+    // exclude child: built in the second shared-memory buffer, then stored
+    {
+      const long long words = deg_bytes<T>(P.n) / 16;
+      const uint4* a = (const uint4*)w.deg;
+      uint4* b2 = (uint4*)w.deg2;
+      for (long long i = threadIdx.x; i < words; i += blockDim.x) b2[i] = a[i];
+    }
+    __syncthreads();
+    NodeWs<T> wx = w;
+    wx.deg = w.deg2;
+    int removed, edges;
+    remove_neighbors_fast(wx, v, w.lst, &removed, &edges);
     long long qpos;
     char* dst = choose_dest(&qpos);
     if (dst) {
-      T* dd = (T*)(dst + sizeof(NodeHdr));
-      store_deg<T>(dst, w.deg, P.n);
-      __syncthreads();
-      NodeWs<T> wx = w;
-      wx.deg = dd;
-      int removed, edges;
-      remove_neighbors(wx, v, w.lst, 0, &removed, &edges);
+      store_deg<T>(dst, w.deg2, P.n);
       NodeHdr ex = h;
       ex.S = S + removed;
       ex.E = E - edges;
@@ -335,12 +341,21 @@ struct Worker {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(512, 1) search_kernel(SearchParams P) {
+__global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
   extern __shared__ __align__(16) unsigned char dsmem[];
   __shared__ BlockScratch bs;
   __shared__ BlockState st;
   char* base = P.ws_in_smem ? (char*)dsmem : P.gws + (long long)blockIdx.x * P.gws_bytes;
   NodeWs<T> ws = carve_ws<T>(base, P.n, &bs, P.off, P.nbr);
+  if (P.csr_in_smem) {
+    // the reduced CSR is read-only for the whole search: stage it on chip
+    int* soff = (int*)((char*)dsmem + ws_bytes<T>(P.n));
+    int* snbr = soff + (((P.n + 1) + 3) & ~3);
+    for (int i = threadIdx.x; i <= P.n; i += blockDim.x) soff[i] = P.off[i];
+    for (long long i = threadIdx.x; i < P.m2; i += blockDim.x) snbr[i] = P.nbr[i];
+    ws.off = soff;
+    ws.nbr = snbr;
+  }
   for (int i = threadIdx.x; i < P.n; i += blockDim.x) {
     ws.tmin[i] = kInf;
     ws.flag[i] = 0;
@@ -462,6 +477,7 @@ __global__ void search_init_kernel(SearchParams P, int root_key, unsigned long l
     *R.count = 1;
     *P.q.head = 0ull;
     *P.q.tail = 0ull;
+    *P.q.count = 0ull;
     Ctl* c = P.ctl;
     unsigned long long* cw = (unsigned long long*)c;
     for (size_t i = 0; i < sizeof(Ctl) / 8; ++i) cw[i] = 0ull;

@@ -60,12 +60,15 @@ struct Queue {
   unsigned long long* seq;
   unsigned long long* head;
   unsigned long long* tail;
+  unsigned long long* count;  // records claimed by producers minus by consumers
   char* data;
   long long cap;
 };
 
 struct SearchParams {
   int n;
+  long long m2;           // 2 * edges of the reduced graph
+  int csr_in_smem;        // stage off/nbr in shared memory (after the workspace)
   const int* off;
   const int* nbr;
   char* stacks;           // gridDim.x * stack_cap * slot_bytes
@@ -92,11 +95,16 @@ __host__ __device__ inline long long deg_bytes(int n) {
   return (((long long)n * (long long)sizeof(T)) + 15) & ~15LL;
 }
 
-// workspace bytes for one block (deg + flag + 7 int arrays)
+// workspace bytes for one block (2 degree buffers + flag + 7 int arrays)
 template <typename T>
 __host__ __device__ inline long long ws_bytes(int n) {
   long long nn = n > 0 ? n : 1;
-  return deg_bytes<T>(n > 0 ? n : 1) + ((nn + 15) & ~15LL) + 7LL * 4LL * ((nn + 3) & ~3LL);
+  return 2 * deg_bytes<T>(n > 0 ? n : 1) + ((nn + 15) & ~15LL) + 7LL * 4LL * ((nn + 3) & ~3LL);
+}
+
+// bytes of the reduced CSR staged in shared memory (int32 offsets + neighbours)
+__host__ __device__ inline long long csr_smem_bytes(int n, long long m2) {
+  return ((4LL * (n + 1) + 15) & ~15LL) + ((4LL * m2 + 15) & ~15LL);
 }
 
 template <typename T>
@@ -107,6 +115,8 @@ __device__ inline NodeWs<T> carve_ws(char* base, int n, BlockScratch* bs, const 
   NodeWs<T> w;
   char* p = base;
   w.deg = (T*)p;
+  p += deg_bytes<T>((int)nn);
+  w.deg2 = (T*)p;
   p += deg_bytes<T>((int)nn);
   w.flag = (uint8_t*)p;
   p += (nn + 15) & ~15LL;
@@ -125,23 +135,30 @@ __device__ inline NodeWs<T> carve_ws(char* base, int n, BlockScratch* bs, const 
 }
 
 // ------------------------------------------------------------------ queue --
+// Broker-queue ring (count guard + fetch-and-add tickets): a producer first
+// claims a unit of `count` (which doubles as the length check of the offload
+// policy), then a tail ticket; a consumer claims a unit of `count` only when
+// one is there, then a head ticket, so the ticket's producer is guaranteed to
+// be committed.  Per-slot sequence numbers hand each slot between the two.
+// No CAS loops: every operation is O(1) atomics, contention-free retries.
 
-// Reserve a ring position for a push; -1 when full.  Thread 0 only.
-__device__ inline long long q_reserve_push(const Queue& q) {
-  unsigned long long pos = ld_relaxed_u64(q.tail);
-  while (true) {
-    unsigned long long s = ld_acquire_u64(&q.seq[pos % q.cap]);
-    long long dif = (long long)s - (long long)pos;
-    if (dif == 0) {
-      unsigned long long prev = atomicCAS(q.tail, pos, pos + 1);
-      if (prev == pos) return (long long)pos;
-      pos = prev;
-    } else if (dif < 0) {
-      return -1;
-    } else {
-      pos = ld_relaxed_u64(q.tail);
-    }
+__device__ __forceinline__ long long atom_add_ll(unsigned long long* p, long long v) {
+  return (long long)atomicAdd(p, (unsigned long long)v);
+}
+
+// Claim a push slot if fewer than `limit` records are queued; -1 otherwise.
+__device__ inline long long q_reserve_push(const Queue& q, long long limit) {
+  if (limit > q.cap) limit = q.cap;
+  if ((long long)ld_relaxed_u64(q.count) >= limit) return -1;
+  long long c = atom_add_ll(q.count, 1);
+  if (c >= limit) {
+    atom_add_ll(q.count, -1);
+    return -1;
   }
+  long long pos = atom_add_ll(q.tail, 1);
+  // the slot is free once its previous consumer has released it
+  while ((long long)ld_acquire_u64(&q.seq[pos % q.cap]) != pos) __nanosleep(32);
+  return pos;
 }
 
 __device__ inline void q_publish_push(const Queue& q, long long pos) {
@@ -149,33 +166,22 @@ __device__ inline void q_publish_push(const Queue& q, long long pos) {
   st_release_u64(&q.seq[pos % q.cap], (unsigned long long)pos + 1);
 }
 
-// Reserve a ring position for a pop; -1 when empty.  Thread 0 only.
+// Claim a queued record; -1 when none.
 __device__ inline long long q_reserve_pop(const Queue& q) {
-  unsigned long long pos = ld_relaxed_u64(q.head);
-  while (true) {
-    unsigned long long s = ld_acquire_u64(&q.seq[pos % q.cap]);
-    long long dif = (long long)s - (long long)(pos + 1);
-    if (dif == 0) {
-      unsigned long long prev = atomicCAS(q.head, pos, pos + 1);
-      if (prev == pos) return (long long)pos;
-      pos = prev;
-    } else if (dif < 0) {
-      return -1;
-    } else {
-      pos = ld_relaxed_u64(q.head);
-    }
+  if ((long long)ld_relaxed_u64(q.count) <= 0) return -1;
+  long long c = atom_add_ll(q.count, -1);
+  if (c <= 0) {
+    atom_add_ll(q.count, 1);
+    return -1;
   }
+  long long pos = atom_add_ll(q.head, 1);
+  // the ticket's producer is committed: wait for its publication
+  while ((long long)ld_acquire_u64(&q.seq[pos % q.cap]) != pos + 1) __nanosleep(32);
+  return pos;
 }
 
 __device__ inline void q_release_pop(const Queue& q, long long pos) {
-  __threadfence();
   st_release_u64(&q.seq[pos % q.cap], (unsigned long long)pos + (unsigned long long)q.cap);
-}
-
-__device__ inline long long q_length(const Queue& q) {
-  long long t = (long long)ld_relaxed_u64(q.tail);
-  long long h = (long long)ld_relaxed_u64(q.head);
-  return t > h ? t - h : 0;
 }
 
 // --------------------------------------------------------------- registry --
@@ -252,10 +258,19 @@ __device__ inline void reg_cascade(const SearchParams& P, int idx) {
   }
 }
 
-__device__ inline void reg_finish(const SearchParams& P, int scope) {
-  __threadfence();
-  if (atomicSub(&P.reg.live[scope], 1) == 1) reg_cascade(P, scope);
+// release: this node's submissions are visible before its slot is returned;
+// acquire: the last finisher sees every other finisher's submissions
+__device__ __forceinline__ int atom_dec_acq_rel(int* p) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], -1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
 }
+
+__device__ inline void reg_finish(const SearchParams& P, int scope) {
+  if (atom_dec_acq_rel(&P.reg.live[scope]) == 1) reg_cascade(P, scope);
+}
+
+
 
 // ------------------------------------------------------------ node moves --
 
