@@ -18,7 +18,7 @@
 using namespace vcg;
 
 namespace vcg {
-template <typename T>
+template <typename T, bool kSmem>
 __global__ void search_kernel(SearchParams P);
 __global__ void drain_kernel(SearchParams P);
 __global__ void search_init_kernel(SearchParams P, int root_key, unsigned long long timeout_ns);
@@ -650,10 +650,10 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   const long long csrb = csr_smem_bytes(n, g->m2);
   const int csr_smem = in_smem && wsb + csrb <= smem_limit && !getenv("VCG_NO_SMEM_CSR");
   const size_t dsmem = in_smem ? (size_t)(wsb + (csr_smem ? csrb : 0)) : 0;
-  CK(cudaFuncSetAttribute(search_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)dsmem));
+  auto kern = in_smem ? search_kernel<T, true> : search_kernel<T, false>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
   int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, search_kernel<T>, threads, dsmem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, dsmem));
   if (per_sm < 1) return fail(VCG_ERESOURCE, "search kernel does not fit on an SM");
   const int resident = per_sm * sm_count;
   int blocks = cfg->deterministic ? 1 : (cfg->workers > 0 ? cfg->workers : resident);
@@ -770,7 +770,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   }
   cudaEventRecord(e0);
   COUNT_LAUNCH(2);  // search + drain
-  search_kernel<T><<<blocks, threads, dsmem>>>(P);
+  kern<<<blocks, threads, dsmem>>>(P);
   cudaEventRecord(e1);
   cudaError_t le = cudaGetLastError();
   if (le != cudaSuccess) return fail(VCG_ECUDA, std::string("search launch: ") + cudaGetErrorString(le));

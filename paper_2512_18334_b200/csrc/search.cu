@@ -340,14 +340,17 @@ struct Worker {
   }
 };
 
-template <typename T>
+// kSmem: the workspace (and, when it fits, the CSR) lives in shared memory;
+// a compile-time choice so every workspace access is an LDS/STS/ATOMS rather
+// than a generic-address access.
+template <typename T, bool kSmem>
 __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
   extern __shared__ __align__(16) unsigned char dsmem[];
   __shared__ BlockScratch bs;
   __shared__ BlockState st;
-  char* base = P.ws_in_smem ? (char*)dsmem : P.gws + (long long)blockIdx.x * P.gws_bytes;
+  char* base = kSmem ? (char*)dsmem : P.gws + (long long)blockIdx.x * P.gws_bytes;
   NodeWs<T> ws = carve_ws<T>(base, P.n, &bs, P.off, P.nbr);
-  if (P.csr_in_smem) {
+  if (kSmem && P.csr_in_smem) {
     // the reduced CSR is read-only for the whole search: stage it on chip
     int* soff = (int*)((char*)dsmem + ws_bytes<T>(P.n));
     int* snbr = soff + (((P.n + 1) + 3) & ~3);
@@ -485,8 +488,11 @@ __global__ void search_init_kernel(SearchParams P, int root_key, unsigned long l
   }
 }
 
-template __global__ void search_kernel<uint8_t>(SearchParams);
-template __global__ void search_kernel<uint16_t>(SearchParams);
-template __global__ void search_kernel<uint32_t>(SearchParams);
+template __global__ void search_kernel<uint8_t, true>(SearchParams);
+template __global__ void search_kernel<uint16_t, true>(SearchParams);
+template __global__ void search_kernel<uint32_t, true>(SearchParams);
+template __global__ void search_kernel<uint8_t, false>(SearchParams);
+template __global__ void search_kernel<uint16_t, false>(SearchParams);
+template __global__ void search_kernel<uint32_t, false>(SearchParams);
 
 }  // namespace vcg
