@@ -228,11 +228,12 @@ def run_b200(args):
     orig = _eng.run_search
 
     def run_search_probe(*a, **kw):
-        res, h = orig(*a, **kw)
+        out = orig(*a, **kw)
+        res = out[0]
         rec["bytes"] += (res.records_loaded + res.records_stored) * res.slot_bytes
         rec["kernel_ms"] += res.kernel_ms
         rec["launches"] += 1
-        return res, h
+        return out
 
     _eng.run_search = run_search_probe
 

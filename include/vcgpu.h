@@ -96,6 +96,9 @@ typedef struct {
   int64_t worklist_threshold; /* 0 = 2 * workers (engine.py:182) */
   double timeout;             /* seconds; 0 = none */
   int check_registry;         /* verify quiescence + conservation afterwards */
+  int record_cover;           /* nodes carry cover bitsets; witnesses are recorded */
+  int32_t* cover_out;         /* record_cover: receives a cover of the reduced graph
+                                 (capacity n) whose size is <= best */
 } vcg_search_config;
 
 typedef struct {
@@ -120,6 +123,8 @@ typedef struct {
   int64_t slot_bytes;         /* bytes per node record (32 B header + degree array) */
   int64_t phase_cycles[10];   /* SM cycles summed over blocks: idle, load, reduce, label,
                                  split, select, exclude, include, registry, other */
+  int64_t cover_size;         /* record_cover: entries written to cover_out, -1 if the
+                                 root's best has no recorded witness */
 } vcg_search_result;
 
 /* Run the persistent search kernel.  hist_out (nullable, capacity n+2)

@@ -37,7 +37,8 @@ class SearchConfig_t(C.Structure):
         ("best_init_achieved", C.c_int), ("use_components", C.c_int), ("use_bounds", C.c_int),
         ("disable_pruning", C.c_int), ("deterministic", C.c_int), ("load_balance", C.c_int),
         ("workers", C.c_int), ("threads", C.c_int), ("worklist_threshold", I64),
-        ("timeout", C.c_double), ("check_registry", C.c_int),
+        ("timeout", C.c_double), ("check_registry", C.c_int), ("record_cover", C.c_int),
+        ("cover_out", C.c_void_p),
     ]
 
 
@@ -49,7 +50,7 @@ class SearchResult_t(C.Structure):
         ("rule_counts", I64 * 6), ("registry_entries", I64), ("registry_violations", I64),
         ("kernel_ms", C.c_double), ("workers", C.c_int), ("threads", C.c_int),
         ("records_loaded", I64), ("records_stored", I64), ("slot_bytes", I64),
-        ("phase_cycles", I64 * 10),
+        ("phase_cycles", I64 * 10), ("cover_size", I64),
     ]
 
 

@@ -105,7 +105,7 @@ struct DevBuf {
 };
 
 struct SearchCtx {
-  DevBuf stacks, qseq, qdata, qctl, reg, ctl, hist, gws;
+  DevBuf stacks, qseq, qdata, qctl, reg, ctl, hist, gws, wbits, wcount;
 };
 
 struct vcg_graph {
@@ -659,7 +659,8 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   int blocks = cfg->deterministic ? 1 : (cfg->workers > 0 ? cfg->workers : resident);
   if (blocks > resident) blocks = resident;
 
-  const long long slot = (long long)sizeof(NodeHdr) + deg_bytes<T>(n);
+  const long long slot = (long long)sizeof(NodeHdr) + deg_bytes<T>(n) +
+                         (cfg->record_cover ? bits_bytes(n) : 0);
   // private stack: depth <= n + 1 (SPEC preprocess: stack bound), capped by memory
   long long stack_cap = (long long)n + 2;
   const long long stack_budget = 16LL << 30;
@@ -673,7 +674,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
 
   if (C.stacks.ensure((size_t)(stack_cap * slot * blocks)) || C.qseq.ensure((size_t)qcap * 8) ||
       C.qdata.ensure((size_t)(qcap * slot)) || C.qctl.ensure(64) ||
-      C.reg.ensure((size_t)reg_cap * 4 * 12 + 64) || C.ctl.ensure(sizeof(Ctl)) ||
+      C.reg.ensure((size_t)reg_cap * (4 * 13 + 8) + 64) || C.ctl.ensure(sizeof(Ctl)) ||
       C.hist.ensure((size_t)(n + 2) * 8) ||
       (!in_smem && C.gws.ensure((size_t)(wsb * blocks))))
     return VCG_ERESOURCE;
@@ -709,8 +710,22 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   R.nchild = rb + 9 * reg_cap;
   R.disc_done = rb + 10 * reg_cap;
   R.child_folded = rb + 11 * reg_cap;
-  R.count = rb + 12 * reg_cap;
+  R.pwrec = rb + 12 * reg_cap;
+  R.count = rb + 13 * reg_cap;
+  R.wkey = (unsigned long long*)(rb + 13 * reg_cap + 16);  // 64-byte aligned
   R.cap = reg_cap;
+  const int record = cfg->record_cover != 0;
+  const int nw = (n + 31) / 32;
+  int wcap = 0;
+  if (record) {
+    wcap = (int)std::min<long long>(1LL << 22, std::max<long long>(4096, (1LL << 30) / (nw * 4LL)));
+    if (C.wbits.ensure((size_t)wcap * nw * 4) || C.wcount.ensure(64)) return VCG_ERESOURCE;
+  }
+  P.record = record;
+  P.nw = nw;
+  P.wbits = C.wbits.as<unsigned>();
+  P.wcount = C.wcount.as<int>();
+  P.wcap = wcap;
   P.ctl = C.ctl.as<Ctl>();
   P.hist = C.hist.as<unsigned long long>();
   P.gws = C.gws.as<char>();
@@ -810,6 +825,54 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
     for (int i = 0; i < n + 2; ++i) hist_out[i] = (int64_t)h[i];
   }
   tr.mark("readback");
+  res->cover_size = -1;
+  if (record && cfg->cover_out) {
+    // expand the root's witness tree: leaf records are scoped cover bitsets,
+    // composite witnesses are a split's record plus its children's witnesses
+    std::vector<unsigned long long> wkey(count);
+    std::vector<int> pw(count), fc(count), nc(count);
+    CK(cudaMemcpy(wkey.data(), R.wkey, (size_t)count * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(pw.data(), R.pwrec, (size_t)count * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(fc.data(), R.first_child, (size_t)count * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(nc.data(), R.nchild, (size_t)count * 4, cudaMemcpyDeviceToHost));
+    int wn = 0;
+    CK(cudaMemcpy(&wn, P.wcount, 4, cudaMemcpyDeviceToHost));
+    wn = std::min(wn, wcap);
+    std::vector<unsigned> bits((size_t)wn * nw);
+    if (wn) CK(cudaMemcpy(bits.data(), P.wbits, bits.size() * 4, cudaMemcpyDeviceToHost));
+    std::vector<unsigned> cover(nw, 0u);
+    const unsigned long long root_w = wkey[0];
+    bool ok = root_w != kNoWitness && (long long)(root_w >> 32) <= res->best;
+    std::vector<int> stack;
+    if (ok) stack.push_back(0);
+    while (ok && !stack.empty()) {
+      const int e = stack.back();
+      stack.pop_back();
+      const unsigned long long wk = wkey[e];
+      if (wk == kNoWitness) {
+        ok = false;
+        break;
+      }
+      const unsigned wid = (unsigned)(wk & 0xffffffffu);
+      int rec = (int)wid;
+      if (wid & kComposite) {
+        const int p = (int)(wid & ~kComposite);
+        rec = pw[p];
+        for (int c = fc[p]; c < fc[p] + nc[p]; ++c) stack.push_back(c);
+      }
+      if (rec < 0 || rec >= wn) {
+        ok = false;
+        break;
+      }
+      for (int i = 0; i < nw; ++i) cover[i] |= bits[(size_t)rec * nw + i];
+    }
+    if (ok) {
+      int64_t k = 0;
+      for (int v = 0; v < n; ++v)
+        if (cover[v >> 5] >> (v & 31) & 1u) cfg->cover_out[k++] = v;
+      res->cover_size = k;
+    }
+  }
   if (cfg->check_registry && count > 0) {
     // registry quiescence + conservation (SPEC registry invariants)
     std::vector<int> f[12];

@@ -58,6 +58,11 @@ __device__ __forceinline__ void deg_dec(T* deg, int x) {
   }
 }
 
+// record-cover mode: vertex u joins the node's (scoped) cover
+__device__ __forceinline__ void mark_inc(unsigned* inc, int u) {
+  if (inc) atomicOr(&inc[u >> 5], 1u << (u & 31));
+}
+
 __device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -210,6 +215,8 @@ struct NodeWs {
   int* lst;         // [n]
   int* id;          // [n]
   uint8_t* flag;    // [n], kept == 0 between operations
+  unsigned* inc;    // cover-membership bitset of the node (record-cover mode), else null
+  unsigned* inc2;   // bitset of the exclude child under construction
   BlockScratch* bs;
   const int* off;   // static CSR (reduced graph), int32 offsets
   const int* nbr;
@@ -266,6 +273,7 @@ __device__ __forceinline__ int remove_list(const NodeWs<T>& w, const int* list, 
     int u = list[k];
     w.deg[u] = 0;
     w.flag[u] = 0;
+    mark_inc(w.inc, u);
   }
   __syncthreads();
   return edges;
@@ -417,6 +425,7 @@ __device__ PassRet high_degree_pass(const NodeWs<T>& w, int lo, int hi, int budg
         __syncwarp();
         if (lane == 0) {
           w.deg[c] = 0;
+          mark_inc(w.inc, c);
           out[p] = c;
         }
         __syncwarp();
@@ -578,7 +587,10 @@ __device__ int remove_vertex(const NodeWs<T>& w, int v) {
     if (ldv(w.deg, x) > 0) deg_dec(w.deg, x);
   }
   __syncthreads();
-  if (threadIdx.x == 0) w.deg[v] = 0;
+  if (threadIdx.x == 0) {
+    w.deg[v] = 0;
+    mark_inc(w.inc, v);
+  }
   __syncthreads();
   return d;
 }
@@ -687,6 +699,7 @@ __device__ __forceinline__ int remove_list_fast(const NodeWs<T>& w, const int* l
       }
     }
     deg_zero(w.deg, u);
+    mark_inc(w.inc, u);
   }
   edges = block_sum(edges, w.bs);
   for (int k = threadIdx.x; k < cnt; k += blockDim.x) w.flag[list[k]] = 0;

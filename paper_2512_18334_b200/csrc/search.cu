@@ -26,6 +26,7 @@ struct Worker {
   // thread-0 statistics
   unsigned long long nodes, comp_branches, pushes, pops, rules[6], rec_in, rec_out;
   int max_depth;
+  long long payload;  // bytes of a record after its header: deg (+ inclusion bitset)
   unsigned long long ph[10];
   long long last_clk;
 
@@ -43,6 +44,7 @@ struct Worker {
     for (int i = 0; i < 6; ++i) rules[i] = 0;
     for (int i = 0; i < 10; ++i) ph[i] = 0;
     last_clk = clock64();
+    payload = deg_bytes<T>(P.n) + (P.record ? bits_bytes(P.n) : 0);
     my_stack = P.stacks + (long long)blockIdx.x * P.stack_cap * P.slot_bytes;
   }
 
@@ -95,6 +97,99 @@ struct Worker {
       ++top;
       if (threadIdx.x == 0 && top > max_depth) max_depth = top;
     }
+  }
+
+  // ------------------------------------------------------ record cover --
+  // Witness of a split: arena record of the splitting node's scoped cover
+  // plus closed-form covers of its clique (all but the root) and chordless
+  // cycle (every other vertex) components; one record per general component
+  // holding its all-but-one cover (the child's achieved initial bound).
+  __device__ void record_split_witness(int ncomp, const int* agg, int parent) {
+    const int G = st->gen;
+    if (threadIdx.x == 0) {
+      int wb = atomicAdd(P.wcount, 1 + G);
+      if (wb + 1 + G > P.wcap) {
+        atomicExch(&P.ctl->error, 4);
+        atomicExch(&P.ctl->stop, 1);
+        wb = -1;
+      }
+      st->child_base = wb;
+    }
+    __syncthreads();
+    const int wb = st->child_base;
+    if (wb < 0) return;
+    unsigned* rec0 = P.wbits + (long long)wb * P.nw;
+    for (int i = threadIdx.x; i < P.nw; i += blockDim.x) rec0[i] = w.inc[i];
+    for (long long i = threadIdx.x; i < (long long)G * P.nw; i += blockDim.x) rec0[P.nw + i] = 0u;
+    __syncthreads();
+    const int lo = st->hdr.lo, hi = st->hdr.hi;
+    for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x) {
+      if (w.deg[v] == 0) continue;
+      const int j = w.id[w.ia[v]];
+      if (v == w.lst[j]) continue;  // the component root stays out
+      const int mark = agg[5 * j + 2];
+      unsigned* rec = nullptr;
+      if (mark == -1) rec = rec0;
+      else if (mark >= 0) rec = rec0 + (long long)(1 + (mark - parent - 1)) * P.nw;
+      if (rec) atomicOr(&rec[v >> 5], 1u << (v & 31));
+    }
+    if (threadIdx.x == 0) {
+      for (int j = 0; j < ncomp; ++j) {
+        if (agg[5 * j + 2] != -2) continue;
+        // chordless cycle: walk it, take positions 0, 2, 4, ... (ceil(L/2))
+        const int L = agg[5 * j];
+        int prev = -1, v = w.lst[j];
+        for (int i = 0; i < L; ++i) {
+          if ((i & 1) == 0) atomicOr(&rec0[v >> 5], 1u << (v & 31));
+          int nxt = -1;
+          for (int k = w.off[v]; k < w.off[v + 1]; ++k) {
+            const int x = w.nbr[k];
+            if (w.deg[x] > 0 && x != prev) {
+              nxt = x;
+              break;
+            }
+          }
+          prev = v;
+          v = nxt;
+        }
+      }
+      P.reg.pwrec[parent] = wb;
+      for (int j = 0; j < ncomp; ++j) {
+        const int c = agg[5 * j + 2];
+        if (c < 0) continue;
+        const int key = P.reg.key[c];
+        if (!(key & 1))  // achieved initial bound == all-but-one
+          P.reg.wkey[c] = ((unsigned long long)(unsigned)(key >> 1) << 32) |
+                          (unsigned)(wb + 1 + (c - parent - 1));
+      }
+      __threadfence();
+    }
+    __syncthreads();
+  }
+
+  // leaf in record mode: store the scoped cover if it improves the scope
+  __device__ unsigned long long record_leaf_witness(int scope, int S) {
+    if (threadIdx.x == 0) {
+      const int key = ld_relaxed(&P.reg.key[scope]);
+      int wid = -1;
+      if (S * 2 < key) {
+        wid = atomicAdd(P.wcount, 1);
+        if (wid >= P.wcap) {
+          atomicExch(&P.ctl->error, 4);
+          atomicExch(&P.ctl->stop, 1);
+          wid = -1;
+        }
+      }
+      st->v = wid;
+    }
+    __syncthreads();
+    const int wid = st->v;
+    if (wid < 0) return kNoWitness;
+    unsigned* rec = P.wbits + (long long)wid * P.nw;
+    for (int i = threadIdx.x; i < P.nw; i += blockDim.x) rec[i] = w.inc[i];
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence();
+    return (unsigned long long)(unsigned)wid;
   }
 
   // ---------------------------------------------------------------- split --
@@ -168,6 +263,7 @@ struct Worker {
             R.link[c] = p;
             R.child_folded[c] = 0;
             R.disc_done[c] = 0;
+            if (P.record) R.wkey[c] = kNoWitness;
             agg[5 * j + 2] = c;  // component -> its child entry
             ++g;
           }
@@ -179,6 +275,7 @@ struct Worker {
     }
     __syncthreads();
     const int parent = st->parent;
+    if (parent >= 0 && P.record) record_split_witness(ncomp, agg, parent);
     if (parent >= 0) {
       for (int j = 0; j < ncomp; ++j) {
         const int c = agg[5 * j + 2];
@@ -194,6 +291,10 @@ struct Worker {
           T val = 0;
           if (v >= lo && v <= hi && w.deg[v] > 0 && w.ia[v] == root) val = w.deg[v];
           dd[v] = val;
+        }
+        if (P.record) {  // a component child starts a fresh cover scope
+          unsigned* db = (unsigned*)(dst + sizeof(NodeHdr) + deg_bytes<T>(P.n));
+          for (int i = threadIdx.x; i < P.nw; i += blockDim.x) db[i] = 0u;
         }
         NodeHdr ch;
         ch.S = 0;
@@ -267,8 +368,9 @@ struct Worker {
       }
     }
     if (E == 0) {
+      const unsigned long long wid = P.record ? record_leaf_witness(h.scope, S) : kNoWitness;
       if (threadIdx.x == 0) {
-        reg_submit(P, h.scope, S, true);
+        reg_submit(P, h.scope, S, true, wid);
         reg_finish(P, h.scope);
       }
       __syncthreads();
@@ -291,7 +393,7 @@ struct Worker {
     if (threadIdx.x == 0) atomicAdd(&P.reg.live[h.scope], 1);
     // exclude child: built in the second shared-memory buffer, then stored
     {
-      const long long words = deg_bytes<T>(P.n) / 16;
+      const long long words = payload / 16;  // [deg | inc] -> [deg2 | inc2]
       const uint4* a = (const uint4*)w.deg;
       uint4* b2 = (uint4*)w.deg2;
       for (long long i = threadIdx.x; i < words; i += blockDim.x) b2[i] = a[i];
@@ -299,12 +401,13 @@ struct Worker {
     __syncthreads();
     NodeWs<T> wx = w;
     wx.deg = w.deg2;
+    wx.inc = w.inc2;
     int removed, edges;
     remove_neighbors_fast(wx, v, w.lst, &removed, &edges);
     long long qpos;
     char* dst = choose_dest(&qpos);
     if (dst) {
-      store_deg<T>(dst, w.deg2, P.n);
+      store_payload(dst, w.deg2, payload);
       NodeHdr ex = h;
       ex.S = S + removed;
       ex.E = E - edges;
@@ -363,6 +466,10 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
     ws.tmin[i] = kInf;
     ws.flag[i] = 0;
   }
+  if (!P.record) {
+    ws.inc = nullptr;
+    ws.inc2 = nullptr;
+  }
   // zero the degree-array padding once; load_node only overwrites [0, n)
   {
     const long long words = deg_bytes<T>(P.n > 0 ? P.n : 1) / 4;
@@ -392,7 +499,7 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
     if (!cont) {
       if (wk.top > 0) {
         wk.top -= 1;
-        load_node<T>(wk.stack_slot(wk.top), &st.hdr, ws.deg, P.n);
+        load_node(wk.stack_slot(wk.top), &st.hdr, ws.deg, wk.payload);
         if (threadIdx.x == 0) ++wk.rec_in;
         __syncthreads();
       } else {
@@ -411,7 +518,7 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
           continue;
         }
         backoff = 32;
-        load_node<T>(wk.queue_slot(pos), &st.hdr, ws.deg, P.n);
+        load_node(wk.queue_slot(pos), &st.hdr, ws.deg, wk.payload);
         __syncthreads();
         if (threadIdx.x == 0) {
           q_release_pop(P.q, pos);
@@ -477,6 +584,10 @@ __global__ void search_init_kernel(SearchParams P, int root_key, unsigned long l
     R.kind[r] = 0;
     R.sum[r] = R.sum_ach[r] = R.init_sum[r] = R.folded[r] = 0;
     R.first_child[r] = R.nchild[r] = R.disc_done[r] = R.child_folded[r] = 0;
+    if (P.record) {
+      R.wkey[r] = kNoWitness;
+      *P.wcount = 0;
+    }
     *R.count = 1;
     *P.q.head = 0ull;
     *P.q.tail = 0ull;

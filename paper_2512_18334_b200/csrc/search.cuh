@@ -37,6 +37,8 @@ struct Registry {
   int* nchild;        // parent
   int* disc_done;     // parent
   int* child_folded;  // child: its best has been added to the parent sum
+  unsigned long long* wkey;  // record-cover: (value << 32 | witness) of the best achieved
+  int* pwrec;         // record-cover: parent entry's arena record (path + special covers)
   int* count;         // arena size (device counter)
   int cap;
 };
@@ -88,6 +90,11 @@ struct SearchParams {
   int k_red;
   int root_index;
   int root_in_stack;
+  int record;             // record-cover mode: nodes carry inclusion bitsets
+  int nw;                 // bitset words per record
+  unsigned* wbits;        // witness arena [wcap][nw]
+  int* wcount;
+  int wcap;
 };
 
 template <typename T>
@@ -95,11 +102,18 @@ __host__ __device__ inline long long deg_bytes(int n) {
   return (((long long)n * (long long)sizeof(T)) + 15) & ~15LL;
 }
 
-// workspace bytes for one block (2 degree buffers + flag + 7 int arrays)
+// record-cover bitset bytes (one bit per reduced vertex), 16-byte padded
+__host__ __device__ inline long long bits_bytes(int n) {
+  long long nw = ((long long)(n > 0 ? n : 1) + 31) / 32;
+  return (nw * 4 + 15) & ~15LL;
+}
+
+// workspace bytes for one block: [deg | inc | deg2 | inc2 | flag | 7 int arrays]
 template <typename T>
 __host__ __device__ inline long long ws_bytes(int n) {
   long long nn = n > 0 ? n : 1;
-  return 2 * deg_bytes<T>(n > 0 ? n : 1) + ((nn + 15) & ~15LL) + 7LL * 4LL * ((nn + 3) & ~3LL);
+  return 2 * (deg_bytes<T>((int)nn) + bits_bytes((int)nn)) + ((nn + 15) & ~15LL) +
+         7LL * 4LL * ((nn + 3) & ~3LL);
 }
 
 // bytes of the reduced CSR staged in shared memory (int32 offsets + neighbours)
@@ -116,8 +130,12 @@ __device__ inline NodeWs<T> carve_ws(char* base, int n, BlockScratch* bs, const 
   char* p = base;
   w.deg = (T*)p;
   p += deg_bytes<T>((int)nn);
+  w.inc = (unsigned*)p;
+  p += bits_bytes((int)nn);
   w.deg2 = (T*)p;
   p += deg_bytes<T>((int)nn);
+  w.inc2 = (unsigned*)p;
+  p += bits_bytes((int)nn);
   w.flag = (uint8_t*)p;
   p += (nn + 15) & ~15LL;
   int* ip = (int*)p;
@@ -186,7 +204,17 @@ __device__ inline void q_release_pop(const Queue& q, long long pos) {
 
 // --------------------------------------------------------------- registry --
 
-__device__ inline void reg_submit(const SearchParams& P, int idx, int value, bool achieved);
+constexpr unsigned long long kNoWitness = ~0ull;
+constexpr unsigned kComposite = 1u << 31;  // witness id tag: "parent entry p + its children"
+
+__device__ inline void reg_submit(const SearchParams& P, int idx, int value, bool achieved,
+                                  unsigned long long wid);
+
+__device__ __forceinline__ void note_witness(const SearchParams& P, int idx, int value,
+                                             unsigned long long wid) {
+  if (P.record && wid != kNoWitness)
+    atomicMin(&P.reg.wkey[idx], ((unsigned long long)(unsigned)value << 32) | wid);
+}
 
 // engine.py:464 _pvc_propagate.  Children are read before the parent sum so
 // a child that finishes concurrently is counted twice (a safe over-estimate)
@@ -213,12 +241,15 @@ __device__ inline void pvc_propagate(const SearchParams& P, int idx) {
     total += ld_relaxed(&R.sum[p]);
     int anc = R.link[p];
     atomicMin(&R.key[anc], (int)(total * 2));
+    note_witness(P, anc, (int)total, kComposite | (unsigned)p);
     idx = anc;
   }
 }
 
 // engine.py:453 _submit
-__device__ inline void reg_submit(const SearchParams& P, int idx, int value, bool achieved) {
+__device__ inline void reg_submit(const SearchParams& P, int idx, int value, bool achieved,
+                                  unsigned long long wid) {
+  if (achieved) note_witness(P, idx, value, wid);
   atomicMin(&P.reg.key[idx], value * 2 + (achieved ? 0 : 1));
   if (!P.pvc) return;
   if (idx != P.root_index) pvc_propagate(P, idx);
@@ -251,7 +282,7 @@ __device__ inline void reg_cascade(const SearchParams& P, int idx) {
       int total = ld_relaxed(&R.sum[idx]);
       int ach = ld_relaxed(&R.sum_ach[idx]);
       int anc = R.link[idx];
-      reg_submit(P, anc, total, ach != 0);
+      reg_submit(P, anc, total, ach != 0, kComposite | (unsigned)idx);
       if (atomicSub(&R.live[anc], 1) != 1) return;
       idx = anc;
     }
@@ -274,21 +305,21 @@ __device__ inline void reg_finish(const SearchParams& P, int scope) {
 
 // ------------------------------------------------------------ node moves --
 
-template <typename T>
-__device__ inline void load_node(const char* src, NodeHdr* hdr, T* deg, int n) {
+// payload = degree array (+ inclusion bitset in record-cover mode); the
+// shared-memory layout keeps them contiguous, like the record
+__device__ inline void load_node(const char* src, NodeHdr* hdr, void* payload, long long bytes) {
   const uint4* s = (const uint4*)src;
   if (threadIdx.x < 2) ((uint4*)hdr)[threadIdx.x] = __ldcg(s + threadIdx.x);
-  const long long words = deg_bytes<T>(n) / 16;
+  const long long words = bytes / 16;
   const uint4* sd = s + 2;
-  uint4* dd = (uint4*)deg;
+  uint4* dd = (uint4*)payload;
   for (long long i = threadIdx.x; i < words; i += blockDim.x) dd[i] = __ldcg(sd + i);
 }
 
-template <typename T>
-__device__ inline void store_deg(char* dst, const T* deg, int n) {
-  const long long words = deg_bytes<T>(n) / 16;
+__device__ inline void store_payload(char* dst, const void* payload, long long bytes) {
+  const long long words = bytes / 16;
   uint4* dd = (uint4*)(dst + sizeof(NodeHdr));
-  const uint4* sd = (const uint4*)deg;
+  const uint4* sd = (const uint4*)payload;
   for (long long i = threadIdx.x; i < words; i += blockDim.x) __stcg(dd + i, sd[i]);
 }
 

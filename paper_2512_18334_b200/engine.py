@@ -141,8 +141,12 @@ class SolveResult:
 
 
 def run_search(rg: StaticGraph, cfg: SolverConfig, width: int, best_init: int,
-               achieved_init: bool, k_red: int | None):
-    """One vcg_search call; returns (SearchResult_t, histogram dict)."""
+               achieved_init: bool, k_red: int | None, record: bool = False):
+    """One vcg_search call; returns (SearchResult_t, histogram dict, cover or None).
+
+    With ``record`` the nodes carry scoped cover bitsets and the kernel
+    records witnesses, so a cover of the root's best comes back with the
+    search itself (components stay on, unlike the reference's witness pass)."""
     sc = _lib.SearchConfig_t()
     sc.width = width
     sc.pvc = int(k_red is not None)
@@ -159,6 +163,11 @@ def run_search(rg: StaticGraph, cfg: SolverConfig, width: int, best_init: int,
     sc.worklist_threshold = int(cfg.worklist_threshold or 0)
     sc.timeout = float(cfg.timeout or 0.0)
     sc.check_registry = int(cfg.check_registry)
+    cover = None
+    if record:
+        cover = np.zeros(max(rg.num_vertices, 1), dtype=np.int32)
+        sc.record_cover = 1
+        sc.cover_out = cover.ctypes.data
     res = _lib.SearchResult_t()
     hist = np.zeros(rg.num_vertices + 2, dtype=np.int64)
     _lib.check(_lib.lib.vcg_search(rg.device().handle, C.byref(sc), C.byref(res),
@@ -166,7 +175,28 @@ def run_search(rg: StaticGraph, cfg: SolverConfig, width: int, best_init: int,
     if res.error:
         raise _lib.GpuError(f"search kernel reported device error {res.error}")
     h = {int(i): int(c) for i, c in enumerate(hist) if c}
-    return res, h
+    local = cover[: res.cover_size].tolist() if record and res.cover_size >= 0 else None
+    return res, h, local
+
+
+def witness_cover(rg: StaticGraph, cfg: SolverConfig, width: int, target: int,
+                  recorded: list[int] | None) -> list[int]:
+    """engine.py:514 _witness_cover: a concrete cover of size <= target.
+
+    Normally the search's own recorded witness; when the root's best is an
+    initial bound no leaf attained (the greedy cover, or the all-forced cap),
+    the greedy members or a recording PVC pass at k = target supply it."""
+    if recorded is not None and len(recorded) <= target:
+        return recorded
+    greedy, members = greedy_bound(rg, members=True)
+    if greedy <= target:
+        return members
+    sub = SolverConfig(mode="pvc", k=target, workers=cfg.workers, threads=cfg.threads,
+                       use_components=cfg.use_components, use_bounds=cfg.use_bounds)
+    res, _, local = run_search(rg, sub, width, target + 1, False, target, record=True)
+    if local is None or len(local) > target:
+        raise RuntimeError("cover reconstruction failed to reach the target size")
+    return local
 
 
 def _assemble_cover(g: StaticGraph, pre: Preprocessed, local: list[int]) -> list[int]:
@@ -233,7 +263,8 @@ def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
         achieved_init = greedy_reduced <= cap
 
     t1 = time.perf_counter()
-    res, hist = run_search(rg, cfg, pre.width, best_init, achieved_init, k_red)
+    res, hist, recorded = run_search(rg, cfg, pre.width, best_init, achieved_init, k_red,
+                                     record=cfg.record_cover)
     stats.phase_seconds["search"] = time.perf_counter() - t1
     result.search_ms = float(res.kernel_ms)
     result.phase_cycles = dict(zip(_lib.PHASES, (int(x) for x in res.phase_cycles)))
@@ -267,9 +298,7 @@ def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
 
     if cfg.record_cover and have_target and result.exact:
         t2 = time.perf_counter()
-        from .witness import witness_cover
-
-        local = witness_cover(rg, pre.width, best, cfg)
+        local = witness_cover(rg, cfg, pre.width, best, recorded)
         result.cover = _assemble_cover(g, pre, local)
         result.cover_size = len(result.cover)
         stats.phase_seconds["reconstruct"] = time.perf_counter() - t2

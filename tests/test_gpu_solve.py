@@ -110,3 +110,40 @@ def test_workloads_match_reference(name):
     for k, e in exp["pvc"].items():
         r = vc.solve(g, vc.SolverConfig(mode="pvc", k=int(k)))
         assert r.found == e["found"], k
+
+
+def test_record_cover_is_valid_and_minimum():
+    """record_cover with components ON: the witness recorded during the
+    search expands to a valid cover of exactly the reported size (the
+    reference's witness pass turns components off, which is intractable on
+    rgg2000)."""
+    import paper_2512_18334_b200 as vc
+
+    for case in golden("solve.json")[::3]:
+        n, off, nbr = csr(case["n"], case["edges"])
+        g = vc.StaticGraph(n, off, nbr)
+        want = case["runs"]["det"]["cover_size"]
+        for kw in (dict(), dict(deterministic=True)):
+            r = vc.solve(g, vc.SolverConfig(record_cover=True, **kw))
+            assert r.cover_size == want, case["name"]
+            assert len(r.cover) == want
+            assert_valid_cover(n, off, nbr, r.cover)
+        r = vc.solve(g, vc.SolverConfig(mode="pvc", k=want, record_cover=True))
+        assert r.found and len(r.cover) <= want
+        assert_valid_cover(n, off, nbr, r.cover)
+
+
+@pytest.mark.parametrize("name", ["er200", "rgg2000"])
+def test_record_cover_on_workloads(name):
+    import paper_2512_18334_b200 as vc
+    from paper_2512_18334_b200 import synth
+
+    exp = golden("workloads.json")[name]
+    n, off, nbr = synth.WORKLOADS[name]()
+    g = vc.StaticGraph(n, off, nbr)
+    r = vc.solve(g, vc.SolverConfig(record_cover=True))
+    assert r.cover_size == exp["mvc"] == len(r.cover)
+    assert_valid_cover(n, off, nbr, r.cover)
+    r = vc.solve(g, vc.SolverConfig(mode="pvc", k=exp["mvc"], record_cover=True))
+    assert r.found and len(r.cover) <= exp["mvc"]
+    assert_valid_cover(n, off, nbr, r.cover)
