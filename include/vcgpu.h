@@ -73,6 +73,9 @@ typedef struct {
 
 /* Root reduction (lightweight rules on the device to a joint fixpoint with
  * the crown rule) and device compaction of the survivors.
+ * has_bound: 0 = no bound (MVC: the greedy cover of g is the bound),
+ * 1 = `bound` given (PVC; greedy_original is not computed, reported as -1),
+ * 2 = `bound` given and greedy_original computed as well.
  * forced_out: capacity n, original ids in forcing order.
  * vertex_map_out: capacity n, reduced id -> original id.
  * reduced_out: new graph handle (the input handle itself is never aliased). */
@@ -125,6 +128,8 @@ typedef struct {
                                  split, select, exclude, include, registry, other */
   int64_t cover_size;         /* record_cover: entries written to cover_out, -1 if the
                                  root's best has no recorded witness */
+  int64_t fix_cycles[4];      /* fixpoint profile (thread-0 cycles): scans, degree-one, */
+  int64_t fix_count[4];       /* triangle and high-degree sweeps, and their counts */
 } vcg_search_result;
 
 /* Run the persistent search kernel.  hist_out (nullable, capacity n+2)

@@ -51,6 +51,7 @@ class SearchResult_t(C.Structure):
         ("kernel_ms", C.c_double), ("workers", C.c_int), ("threads", C.c_int),
         ("records_loaded", I64), ("records_stored", I64), ("slot_bytes", I64),
         ("phase_cycles", I64 * 10), ("cover_size", I64),
+        ("fix_cycles", I64 * 4), ("fix_count", I64 * 4),
     ]
 
 

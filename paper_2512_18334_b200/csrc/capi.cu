@@ -4,6 +4,7 @@
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -160,10 +161,9 @@ extern "C" int64_t vcg_graph_num_edges(const vcg_graph* g) { return g ? g->m2 / 
 
 extern "C" int vcg_graph_download(const vcg_graph* g, int64_t* offsets, int32_t* neighbors) {
   if (!g) return fail(VCG_EINVAL, "null graph");
-  std::vector<int32_t> off32(g->n + 1);
-  CK(cudaMemcpy(off32.data(), g->d_off.p, (g->n + 1) * 4, cudaMemcpyDeviceToHost));
-  for (int64_t i = 0; i <= g->n; ++i) offsets[i] = off32[i];
-  if (g->m2) CK(cudaMemcpy(neighbors, g->d_nbr.p, g->m2 * 4, cudaMemcpyDeviceToHost));
+  // the host mirror is built together with the device CSR (create/compaction)
+  std::copy(g->h_off.begin(), g->h_off.end(), offsets);
+  std::copy(g->h_nbr.begin(), g->h_nbr.end(), neighbors);
   return 0;
 }
 
@@ -335,6 +335,7 @@ __global__ void k_node_op(int op, int n, const int32_t* off, const int32_t* nbr,
                           char* wsmem, int lo, int hi, int budget, int v, int32_t* out, int pos,
                           long long* ret) {
   __shared__ BlockScratch bs;
+  init_block_scratch(&bs);
   NodeWs<T> w = carve_ws<T>(wsmem, n, &bs, off, nbr);
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     w.deg[i] = deg_io[i];
@@ -382,11 +383,12 @@ __global__ void k_node_op(int op, int n, const int32_t* off, const int32_t* nbr,
     // component of v among live vertices of [lo, hi]
     int nc = label_components(w, lo, hi);
     (void)nc;
-    int root = w.ia[v];
+    compress_labels(w, lo, hi);
+    int root = w.par[v];
     int size = 0, dsum = 0, mn = kInf, mx = 0, vmn = kInf, vmx = -1;
     for (int x = lo + threadIdx.x; x <= hi; x += blockDim.x) {
       int d = w.deg[x];
-      if (d > 0 && w.ia[x] == root) {
+      if (d > 0 && w.par[x] == root) {
         ++size;
         dsum += d;
         mn = min(mn, d);
@@ -411,7 +413,7 @@ __global__ void k_node_op(int op, int n, const int32_t* off, const int32_t* nbr,
     if (threadIdx.x == 0) {
       int k = 0;
       for (int x = lo; x <= hi; ++x)
-        if (w.deg[x] > 0 && w.ia[x] == root) out[k++] = x;
+        if (w.deg[x] > 0 && w.par[x] == root) out[k++] = x;
     }
   }
   __syncthreads();
@@ -470,6 +472,7 @@ __global__ void k_root_fixpoint(int n, const int32_t* off, const int32_t* nbr, c
                                 int lo, int hi, int budget, int32_t* out, int pos, long long* ret,
                                 int init) {
   __shared__ BlockScratch bs;
+  init_block_scratch(&bs);
   NodeWs<uint32_t> w = carve_ws<uint32_t>(wsmem, n, &bs, off, nbr);
   if (init) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -504,9 +507,14 @@ extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int h
   if (int r = need_device()) return r;
   if (!g || !info || !reduced_out) return fail(VCG_EINVAL, "bad arguments");
   memset(info, 0, sizeof(*info));
+  Tracer tr("root");
   const int n = (int)g->n;
-  info->greedy_original = greedy_cover_host(g->n, g->h_off.data(), g->h_nbr.data(), nullptr);
+  // PVC (has_bound) never needs the greedy cover of the original graph; the
+  // public root_reduce() asks for it (has_bound == 2) to mirror the reference
+  info->greedy_original = has_bound == 1 ? -1
+                          : greedy_cover_host(g->n, g->h_off.data(), g->h_nbr.data(), nullptr);
   const int64_t bound0 = has_bound ? bound : info->greedy_original;
+  tr.mark("greedy_original");
   DevBuf flag;
   if (flag.ensure((size_t)(n + 1) * 4)) return VCG_ERESOURCE;
   std::vector<int64_t> vmap;
@@ -605,6 +613,7 @@ extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int h
     k_flags_from_deg<<<(n + 256) / 256 + 1, 256>>>(ws.as<uint32_t>(), n, flag.as<int32_t>());
     CK(cudaGetLastError());
   }
+  tr.mark("rules+crown");
   auto t2 = std::chrono::steady_clock::now();
   vcg_graph* red = nullptr;
   if (int r = compact_flagged(g, flag, &red, &vmap)) return r;
@@ -615,7 +624,9 @@ extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int h
   int64_t md = 0;
   for (int64_t v = 0; v < red->n; ++v) md = std::max<int64_t>(md, red->h_off[v + 1] - red->h_off[v]);
   info->max_degree_reduced = md;
+  tr.mark("compaction");
   info->greedy_reduced = greedy_cover_host(red->n, red->h_off.data(), red->h_nbr.data(), nullptr);
+  tr.mark("greedy_reduced");
   if (vertex_map_out)
     for (size_t i = 0; i < vmap.size(); ++i) vertex_map_out[i] = vmap[i];
   *reduced_out = red;
@@ -694,6 +705,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   P.q.head = C.qctl.as<unsigned long long>();
   P.q.tail = C.qctl.as<unsigned long long>() + 1;
   P.q.count = C.qctl.as<unsigned long long>() + 2;
+  P.q.err = &C.ctl.as<Ctl>()->error;
   P.q.data = C.qdata.as<char>();
   P.q.cap = qcap;
   int* rb = C.reg.as<int>();
@@ -732,6 +744,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   P.gws_bytes = wsb;
   P.ws_in_smem = in_smem;
   P.share = share;
+  P.batch_live = !cfg->deterministic && !getenv("VCG_NO_BATCH");
   P.threshold = threshold;
   P.use_components = cfg->use_components;
   P.use_bounds = cfg->use_bounds;
@@ -819,6 +832,10 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   res->records_stored = (int64_t)ctl.rec_out;
   res->slot_bytes = slot;
   for (int i = 0; i < 10; ++i) res->phase_cycles[i] = (int64_t)ctl.phase[i];
+  for (int i = 0; i < 4; ++i) {
+    res->fix_cycles[i] = (int64_t)ctl.rcyc[i];
+    res->fix_count[i] = (int64_t)ctl.rcnt[i];
+  }
   if (hist_out) {
     std::vector<unsigned long long> h(n + 2);
     CK(cudaMemcpy(h.data(), C.hist.p, (size_t)(n + 2) * 8, cudaMemcpyDeviceToHost));

@@ -12,22 +12,86 @@
 namespace vcg {
 
 // preprocess.py:348 greedy_bound -> pure.py:306 greedy_cover: repeatedly take
-// the lowest-index vertex of maximum residual degree.  Lazy max-heap keyed by
-// (degree desc, index asc); stale entries are skipped on pop.
+// the lowest-index vertex of maximum residual degree.
+//
+// Degree buckets as two-level bitsets (64-bit words + a summary word per 64
+// words): the pick is "highest non-empty bucket, lowest set bit", a vertex
+// moves one bucket down per removed neighbour.  O(m + picks * n/4096) time;
+// falls back to a lazy max-heap when buckets x n bits would exceed 256 MiB.
+namespace {
+
+struct Buckets {
+  int64_t words, sumw;
+  std::vector<uint64_t> bits, summary;  // [deg][words], [deg][sumw]
+  std::vector<int64_t> count;
+  Buckets(int64_t n, int64_t maxdeg)
+      : words((n + 63) / 64), sumw((words + 63) / 64),
+        bits((size_t)(maxdeg + 1) * words, 0), summary((size_t)(maxdeg + 1) * sumw, 0),
+        count(maxdeg + 1, 0) {}
+  void set(int64_t d, int64_t v) {
+    uint64_t& w = bits[(size_t)d * words + (v >> 6)];
+    if (!w) summary[(size_t)d * sumw + ((v >> 6) >> 6)] |= 1ull << ((v >> 6) & 63);
+    w |= 1ull << (v & 63);
+    ++count[d];
+  }
+  void clear(int64_t d, int64_t v) {
+    uint64_t& w = bits[(size_t)d * words + (v >> 6)];
+    w &= ~(1ull << (v & 63));
+    if (!w) summary[(size_t)d * sumw + ((v >> 6) >> 6)] &= ~(1ull << ((v >> 6) & 63));
+    --count[d];
+  }
+  int64_t lowest(int64_t d) const {
+    const uint64_t* sm = &summary[(size_t)d * sumw];
+    for (int64_t i = 0; i < sumw; ++i)
+      if (sm[i]) {
+        int64_t wi = i * 64 + __builtin_ctzll(sm[i]);
+        return wi * 64 + __builtin_ctzll(bits[(size_t)d * words + wi]);
+      }
+    return -1;
+  }
+};
+
+}  // namespace
+
 int64_t greedy_cover_host(int64_t n, const int64_t* off, const int32_t* nbr, int32_t* members) {
   if (n <= 0) return 0;
   std::vector<uint32_t> deg(n);
-  int64_t m2 = 0;
+  int64_t m2 = 0, maxdeg = 0;
   for (int64_t v = 0; v < n; ++v) {
     deg[v] = (uint32_t)(off[v + 1] - off[v]);
     m2 += deg[v];
+    maxdeg = std::max<int64_t>(maxdeg, deg[v]);
   }
   if (m2 == 0) return 0;
+  int64_t size = 0;
+  if ((maxdeg + 1) * ((n + 63) / 64) * 8 <= (256LL << 20)) {
+    Buckets b(n, maxdeg);
+    for (int64_t v = 0; v < n; ++v)
+      if (deg[v]) b.set(deg[v], v);
+    int64_t top = maxdeg;
+    while (true) {
+      while (top > 0 && b.count[top] == 0) --top;
+      if (top == 0) break;
+      const int64_t v = b.lowest(top);
+      b.clear(top, v);
+      for (int64_t i = off[v]; i < off[v + 1]; ++i) {
+        const int32_t u = nbr[i];
+        if (deg[u] > 0) {
+          b.clear(deg[u], u);
+          --deg[u];
+          if (deg[u]) b.set(deg[u], u);
+        }
+      }
+      deg[v] = 0;
+      if (members) members[size] = (int32_t)v;
+      ++size;
+    }
+    return size;
+  }
   using Key = std::pair<uint32_t, int64_t>;  // (degree, -index)
   std::priority_queue<Key> heap;
   for (int64_t v = 0; v < n; ++v)
     if (deg[v]) heap.push(Key(deg[v], -v));
-  int64_t size = 0;
   while (!heap.empty()) {
     Key k = heap.top();
     heap.pop();

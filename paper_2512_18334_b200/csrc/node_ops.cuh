@@ -102,8 +102,29 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 struct BlockScratch {
   int v[kMaxWarps + 8];
   long long w[kMaxWarps + 2];
+  int v2[kMaxWarps];
+  int v3[kMaxWarps];
+  long long w2[kMaxWarps];
   int bc[16];  // broadcast slots
+  // thread-0 profile of the fixpoint: cycles and counts of scans, degree-one,
+  // triangle and high-degree sweeps
+  unsigned long long rcyc[4];
+  unsigned long long rcnt[4];
+  // one-barrier reductions: per-warp partials, double-buffered per call
+  // (a warp can only reuse a buffer after the next call's barrier, by which
+  // time every warp has read it); the parity is per warp, so no cross-warp race
+  int red[2][8][kMaxWarps];
+  int wpar[kMaxWarps];
 };
+
+__device__ __forceinline__ void rprof(BlockScratch* bs, int i, long long* t) {
+  if (threadIdx.x == 0) {
+    long long now = clock64();
+    bs->rcyc[i] += (unsigned long long)(now - *t);
+    bs->rcnt[i] += 1;
+    *t = now;
+  }
+}
 
 __device__ __forceinline__ int warp_sum(int x) {
 #pragma unroll
@@ -111,39 +132,58 @@ __device__ __forceinline__ int warp_sum(int x) {
   return x;
 }
 
-__device__ __forceinline__ int block_sum(int x, BlockScratch* bs) {
+__device__ __forceinline__ int warp_parity(BlockScratch* bs) {
+  return ((volatile int*)bs->wpar)[threadIdx.x >> 5];
+}
+__device__ __forceinline__ void warp_parity_flip(BlockScratch* bs, int p) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) bs->wpar[threadIdx.x >> 5] = p ^ 1;
+  __syncwarp();
+}
+
+// op: 0 add, 1 min, 2 max.  K values reduced with one block barrier.
+template <int K>
+__device__ __forceinline__ void block_reduce(int (&x)[K], const int (&op)[K], BlockScratch* bs) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-  x = warp_sum(x);
+  const int p = warp_parity(bs);
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    int r = op[k] == 0   ? __reduce_add_sync(0xffffffffu, x[k])
+            : op[k] == 1 ? __reduce_min_sync(0xffffffffu, x[k])
+                         : __reduce_max_sync(0xffffffffu, x[k]);
+    if (lane == 0) bs->red[p][k][wid] = r;
+  }
   __syncthreads();
-  if (lane == 0) bs->v[wid] = x;
-  __syncthreads();
-  int t = 0;
-  for (int i = 0; i < nw; ++i) t += bs->v[i];
-  return t;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int ident = op[k] == 0 ? 0 : op[k] == 1 ? kInf : -kInf;
+    int y = lane < nw ? bs->red[p][k][lane] : ident;
+    x[k] = op[k] == 0   ? __reduce_add_sync(0xffffffffu, y)
+           : op[k] == 1 ? __reduce_min_sync(0xffffffffu, y)
+                        : __reduce_max_sync(0xffffffffu, y);
+  }
+  warp_parity_flip(bs, p);
+}
+
+__device__ __forceinline__ int block_sum(int x, BlockScratch* bs) {
+  int v[1] = {x};
+  const int op[1] = {0};
+  block_reduce<1>(v, op, bs);
+  return v[0];
 }
 
 __device__ __forceinline__ int block_min(int x, BlockScratch* bs) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x = min(x, __shfl_xor_sync(0xffffffffu, x, o));
-  __syncthreads();
-  if (lane == 0) bs->v[wid] = x;
-  __syncthreads();
-  int t = kInf;
-  for (int i = 0; i < nw; ++i) t = min(t, bs->v[i]);
-  return t;
+  int v[1] = {x};
+  const int op[1] = {1};
+  block_reduce<1>(v, op, bs);
+  return v[0];
 }
 
 __device__ __forceinline__ int block_max(int x, BlockScratch* bs) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
-  __syncthreads();
-  if (lane == 0) bs->v[wid] = x;
-  __syncthreads();
-  int t = -kInf;
-  for (int i = 0; i < nw; ++i) t = max(t, bs->v[i]);
-  return t;
+  int v[1] = {x};
+  const int op[1] = {2};
+  block_reduce<1>(v, op, bs);
+  return v[0];
 }
 
 __device__ __forceinline__ long long block_max64(long long x, BlockScratch* bs) {
@@ -214,6 +254,7 @@ struct NodeWs {
   int* ic;          // [n]
   int* lst;         // [n]
   int* id;          // [n]
+  int* par;         // [n] union-find parents (component labels)
   uint8_t* flag;    // [n], kept == 0 between operations
   unsigned* inc;    // cover-membership bitset of the node (record-cover mode), else null
   unsigned* inc2;   // bitset of the exclude child under construction
@@ -222,6 +263,12 @@ struct NodeWs {
   const int* nbr;
   int n;
 };
+
+// every kernel that uses the block collectives calls this first
+__device__ __forceinline__ void init_block_scratch(BlockScratch* bs) {
+  if (threadIdx.x < kMaxWarps) bs->wpar[threadIdx.x] = 0;
+  __syncthreads();
+}
 
 struct PassRet {
   int applied;
@@ -666,6 +713,37 @@ __device__ __forceinline__ void block_scan3(int a, int b, int c, BlockScratch* b
   *tc = (int)t3;
 }
 
+// block_scan3 plus the live window (min / max live index) and the
+// max-degree key ((deg << 32) | (INT_MAX - v): lowest index on ties) in the
+// same two barriers -- the last scan of a fixpoint describes the final state
+struct ScanStats {
+  int c1, c2, ch, lo, hi;
+  long long key;
+};
+
+__device__ __forceinline__ ScanStats block_scan_stats(int a, int b, int c, int mn, int mx,
+                                                      int dmax, int dmax_v, BlockScratch* bs) {
+  {
+    int v[6] = {a, b, c, mn, mx, dmax};
+    const int op[6] = {0, 0, 0, 1, 2, 2};
+    block_reduce<6>(v, op, bs);
+    a = v[0];
+    b = v[1];
+    c = v[2];
+    mn = v[3];
+    mx = v[4];
+    // lowest index among the vertices of maximum degree (pure.py:241 tie-break)
+    int w2[1] = {dmax == v[5] ? dmax_v : kInf};
+    const int op2[1] = {1};
+    block_reduce<1>(w2, op2, bs);
+    dmax = v[5];
+    dmax_v = w2[0];
+  }
+  long long key = dmax > 0 ? (((long long)dmax << 32) | (long long)(unsigned)(0x7fffffff - dmax_v))
+                           : -1;
+  return ScanStats{a, b, c, mn, mx, key};
+}
+
 template <typename T>
 __device__ __forceinline__ void deg_zero(T* deg, int x) {
   if constexpr (sizeof(T) == 4) {
@@ -708,8 +786,8 @@ __device__ __forceinline__ int remove_list_fast(const NodeWs<T>& w, const int* l
 
 // degree-one sweep with the candidate count/offsets already known
 template <typename T>
-__device__ PassRet degree_one_pass_fast(const NodeWs<T>& w, int b, int e, int at, int ncand,
-                                        int* rem) {
+__device__ PassRet degree_one_pass_fast(const NodeWs<T>& w, int b, int e, int ncand, int* rem) {
+  // candidates in any order: the decision below depends only on tmin
   for (int v = b; v < e; ++v) {
     if (w.deg[v] == 1) {
       int u = -1;
@@ -721,7 +799,7 @@ __device__ PassRet degree_one_pass_fast(const NodeWs<T>& w, int b, int e, int at
         }
       }
       w.ia[v] = u;
-      w.lst[at++] = v;
+      w.lst[atomicAdd(&w.bs->bc[8], 1)] = v;
       atomicMin(&w.tmin[u], v);
     }
   }
@@ -731,11 +809,11 @@ __device__ PassRet degree_one_pass_fast(const NodeWs<T>& w, int b, int e, int at
     int u = w.ia[v];
     if ((w.tmin[u] == v) && !(w.deg[u] == 1 && w.ia[u] == v && u < v)) {
       w.flag[u] = 1;
-      rem[atomicAdd(&w.bs->bc[8], 1)] = u;
+      rem[atomicAdd(&w.bs->bc[9], 1)] = u;
     }
   }
   __syncthreads();
-  const int total = w.bs->bc[8];
+  const int total = w.bs->bc[9];
   int edges = remove_list_fast(w, rem, total);
   for (int k = threadIdx.x; k < ncand; k += blockDim.x) w.tmin[w.ia[w.lst[k]]] = kInf;
   return PassRet{total, total, edges, 0};
@@ -744,43 +822,61 @@ __device__ PassRet degree_one_pass_fast(const NodeWs<T>& w, int b, int e, int at
 // reduce_fixpoint (pure.py:188) for the search: identical forced sets and
 // counters; one fused scan decides which sweeps have candidates.
 template <typename T>
-__device__ FixRet reduce_fixpoint_fast(const NodeWs<T>& w, int lo, int hi, int budget) {
+__device__ FixRet reduce_fixpoint_fast(const NodeWs<T>& w, int lo, int hi, int budget,
+                                      long long* maxkey) {
   FixRet r{0, 0, 0, 0, 0, lo, hi, 0};
   int b, e;
   my_chunk(lo, hi, &b, &e);
   int* rem = w.id;
+  ScanStats st{};
+  long long t0 = clock64();
   while (true) {
     int cycle = 0;
-    int c1 = 0, c2 = 0, ch = 0;
     while (true) {
       const int bud = budget - r.forced;
-      int t1 = 0, t2 = 0, th = 0;
+      int t1 = 0, t2 = 0, th = 0, mn = kInf, mx = -1, dm = 0, dv = kInf;
       for (int v = b; v < e; ++v) {
         int d = w.deg[v];
+        w.par[v] = v;  // union-find init for the component check that follows
         t1 += (d == 1);
         t2 += (d == 2);
         th += (d > 0 && d > bud);
+        if (d > 0) {
+          mn = min(mn, v);
+          mx = v;
+          if (d > dm) {  // ascending chunk: first maximum = lowest index
+            dm = d;
+            dv = v;
+          }
+        }
       }
-      int at1;
-      block_scan3(t1, t2, th, w.bs, &at1, &c1, &c2, &ch);
-      if (c1 == 0) break;
-      PassRet a = degree_one_pass_fast(w, b, e, at1, c1, rem);
+      if (threadIdx.x == 0) {  // list cursors of the sweep that follows
+        w.bs->bc[8] = 0;
+        w.bs->bc[9] = 0;
+      }
+      st = block_scan_stats(t1, t2, th, mn, mx, dm, dv, w.bs);
+      rprof(w.bs, 0, &t0);
+      if (st.c1 == 0) break;
+      PassRet a = degree_one_pass_fast(w, b, e, st.c1, rem);
+      rprof(w.bs, 1, &t0);
       r.d1 += a.applied;
       r.forced += a.forced;
       r.edges += a.edges;
       cycle += a.applied;
     }
     int tri = 0;
-    if (c2 > 0) {
+    if (st.c2 > 0) {
       PassRet t = degree_two_triangle_pass(w, lo, hi, rem, 0);
+      rprof(w.bs, 2, &t0);
       tri = t.applied;
       r.d2t += t.applied;
       r.forced += t.forced;
       r.edges += t.edges;
       cycle += t.applied;
     }
-    if (tri > 0 || ch > 0) {
+    if (tri > 0 || st.ch > 0) {
       PassRet h = high_degree_pass(w, lo, hi, budget - r.forced, rem, 0);
+      rprof(w.bs, 3, &t0);
       r.hd += h.applied;
       r.forced += h.forced;
       r.edges += h.edges;
@@ -788,10 +884,15 @@ __device__ FixRet reduce_fixpoint_fast(const NodeWs<T>& w, int lo, int hi, int b
     }
     if (cycle == 0) break;
   }
-  int l = lo, h = hi;
-  recompute_bounds(w, &l, &h);
-  r.lo = l;
-  r.hi = h;
+  // nothing changed since the last scan: its window and max-degree key are final
+  if (st.hi < 0) {  // pure.py:238 empty window
+    r.lo = w.n > 1 ? w.n : 1;
+    r.hi = 0;
+  } else {
+    r.lo = st.lo;
+    r.hi = st.hi;
+  }
+  *maxkey = st.key;
   return r;
 }
 
@@ -820,7 +921,9 @@ __device__ void remove_neighbors_fast(const NodeWs<T>& w, int v, int* rem, int* 
 
 __device__ __forceinline__ int uf_find(int* par, int x) {
   int p = ((volatile int*)par)[x];
+  unsigned guard = 0;
   while (p != x) {
+    if (++guard > (1u << 24)) __trap();  // a cycle in the forest: protocol bug
     int gp = ((volatile int*)par)[p];
     if (gp != p) ((volatile int*)par)[x] = gp;  // path halving, benign race
     x = p;
@@ -845,12 +948,15 @@ __device__ __forceinline__ void uf_union(int* par, int a, int b) {
 }
 
 // Labels every live vertex in [lo, hi] with its component's minimum vertex
-// (ia[v]) and returns the number of components.
+// (par[v] after compress_labels) and returns the number of components.
+// `inited`: par[v] == v already holds on [lo, hi] (the fixpoint's scan sets it).
 template <typename T>
-__device__ int label_components(const NodeWs<T>& w, int lo, int hi) {
-  int* par = w.ia;
-  for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x) par[v] = v;
-  __syncthreads();
+__device__ int label_components(const NodeWs<T>& w, int lo, int hi, bool inited = false) {
+  int* par = w.par;
+  if (!inited) {
+    for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x) par[v] = v;
+    __syncthreads();
+  }
   for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x) {
     if (w.deg[v] > 0) {
       for (int j = w.off[v]; j < w.off[v + 1]; ++j) {
@@ -861,18 +967,17 @@ __device__ int label_components(const NodeWs<T>& w, int lo, int hi) {
   }
   __syncthreads();
   int roots = 0;
-  for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x) {
-    if (w.deg[v] > 0) {
-      int r = uf_find(par, v);
-      roots += (r == v);
-    }
-  }
-  roots = block_sum(roots, w.bs);
-  // full compression
   for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x)
-    if (w.deg[v] > 0) par[v] = uf_find(par, v);
+    if (w.deg[v] > 0 && ((volatile int*)par)[v] == v) ++roots;
+  return block_sum(roots, w.bs);
+}
+
+// full path compression: par[v] = component minimum for every live v
+template <typename T>
+__device__ void compress_labels(const NodeWs<T>& w, int lo, int hi) {
+  for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x)
+    if (w.deg[v] > 0) w.par[v] = uf_find(w.par, v);
   __syncthreads();
-  return roots;
 }
 
 struct CompInfo {
@@ -890,11 +995,11 @@ __device__ void component_aggregates(const NodeWs<T>& w, int lo, int hi, int nco
   int b, e;
   my_chunk(lo, hi, &b, &e);
   int cnt = 0;
-  for (int v = b; v < e; ++v) cnt += (w.deg[v] > 0 && w.ia[v] == v);
+  for (int v = b; v < e; ++v) cnt += (w.deg[v] > 0 && w.par[v] == v);
   int tot;
   int at = block_exscan(cnt, w.bs, &tot);
   for (int v = b; v < e; ++v) {
-    if (w.deg[v] > 0 && w.ia[v] == v) {
+    if (w.deg[v] > 0 && w.par[v] == v) {
       w.lst[at] = v;
       w.id[v] = at;
       ++at;
@@ -911,7 +1016,7 @@ __device__ void component_aggregates(const NodeWs<T>& w, int lo, int hi, int nco
   for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x) {
     int d = w.deg[v];
     if (d > 0) {
-      int j = w.id[w.ia[v]];
+      int j = w.id[w.par[v]];
       atomicAdd(&agg[5 * j + 0], 1);
       atomicAdd(&agg[5 * j + 1], d);
       atomicMin(&agg[5 * j + 2], d);

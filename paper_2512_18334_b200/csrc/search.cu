@@ -26,6 +26,7 @@ struct Worker {
   // thread-0 statistics
   unsigned long long nodes, comp_branches, pushes, pops, rules[6], rec_in, rec_out;
   int max_depth;
+  LiveBatch lb;  // thread 0
   long long payload;  // bytes of a record after its header: deg (+ inclusion bitset)
   unsigned long long ph[10];
   long long last_clk;
@@ -45,6 +46,7 @@ struct Worker {
     for (int i = 0; i < 10; ++i) ph[i] = 0;
     last_clk = clock64();
     payload = deg_bytes<T>(P.n) + (P.record ? bits_bytes(P.n) : 0);
+    lb.enabled = P.batch_live;
     my_stack = P.stacks + (long long)blockIdx.x * P.stack_cap * P.slot_bytes;
   }
 
@@ -125,7 +127,7 @@ struct Worker {
     const int lo = st->hdr.lo, hi = st->hdr.hi;
     for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x) {
       if (w.deg[v] == 0) continue;
-      const int j = w.id[w.ia[v]];
+      const int j = w.id[w.par[v]];
       if (v == w.lst[j]) continue;  // the component root stays out
       const int mark = agg[5 * j + 2];
       unsigned* rec = nullptr;
@@ -197,8 +199,9 @@ struct Worker {
   __device__ bool try_split() {
     NodeHdr& h = st->hdr;
     const int lo = h.lo, hi = h.hi;
-    int ncomp = label_components(w, lo, hi);
+    int ncomp = label_components(w, lo, hi, /*inited=*/true);
     if (ncomp <= 1) return false;
+    compress_labels(w, lo, hi);
     tick(PH_LABEL);
     int* agg = w.ib;
     component_aggregates(w, lo, hi, ncomp, agg);
@@ -223,7 +226,7 @@ struct Worker {
       }
       const Registry& R = P.reg;
       const int scope = h.scope;
-      atomicAdd(&R.live[scope], 1);  // slot for the parent entry's finalisation
+      lb.inc(P, scope);  // slot for the parent entry's finalisation
       int base = atomicAdd(R.count, 1 + G);
       if (base + 1 + G > R.cap) {
         atomicExch(&P.ctl->error, 1);
@@ -289,7 +292,7 @@ struct Worker {
         T* dd = (T*)(dst + sizeof(NodeHdr));
         for (int v = threadIdx.x; v < P.n; v += blockDim.x) {
           T val = 0;
-          if (v >= lo && v <= hi && w.deg[v] > 0 && w.ia[v] == root) val = w.deg[v];
+          if (v >= lo && v <= hi && w.deg[v] > 0 && w.par[v] == root) val = w.deg[v];
           dd[v] = val;
         }
         if (P.record) {  // a component child starts a fresh cover scope
@@ -313,7 +316,7 @@ struct Worker {
         if (atomicSub(&P.reg.live[parent], 1) == 1) reg_cascade(P, parent);
       }
     }
-    if (threadIdx.x == 0) reg_finish(P, h.scope);
+    if (threadIdx.x == 0) lb.finish(P, h.scope, false);
     __syncthreads();
     tick(PH_SPLIT);
     return true;
@@ -324,15 +327,11 @@ struct Worker {
   // left in shared memory to be processed next.
   __device__ bool process() {
     NodeHdr& h = st->hdr;
-    if (threadIdx.x == 0) {
-      ++nodes;
-      st->best_s = ld_relaxed(&P.reg.key[h.scope]) >> 1;
-    }
-    __syncthreads();
-    tick(PH_REGISTRY);
+    if (threadIdx.x == 0) ++nodes;  // st->best_s was fetched with the record
     const int best_s = st->best_s;
     const int budget = best_s - h.S - 1;
-    FixRet fr = reduce_fixpoint_fast(w, h.lo, h.hi, budget);
+    long long maxkey;
+    FixRet fr = reduce_fixpoint_fast(w, h.lo, h.hi, budget, &maxkey);
     tick(PH_REDUCE);
     if (threadIdx.x == 0) {
       rules[0] += fr.d1;
@@ -361,7 +360,7 @@ struct Worker {
         prune = (long long)E > rem * rem;
       }
       if (prune) {
-        if (threadIdx.x == 0) reg_finish(P, h.scope);
+        if (threadIdx.x == 0) lb.finish(P, h.scope, false);
         __syncthreads();
         tick(PH_REGISTRY);
         return false;
@@ -371,7 +370,7 @@ struct Worker {
       const unsigned long long wid = P.record ? record_leaf_witness(h.scope, S) : kNoWitness;
       if (threadIdx.x == 0) {
         reg_submit(P, h.scope, S, true, wid);
-        reg_finish(P, h.scope);
+        lb.finish(P, h.scope, true);
       }
       __syncthreads();
       tick(PH_REGISTRY);
@@ -379,7 +378,8 @@ struct Worker {
     }
     if (P.use_components && try_split()) return false;
     tick(PH_LABEL);
-    const int v = select_max_degree(w, lo, hi);
+    // pure.py:241 select_max_degree, taken from the fixpoint's final scan
+    const int v = maxkey < 0 ? -1 : 0x7fffffff - (int)(maxkey & 0xffffffffLL);
     tick(PH_SELECT);
     if (v < 0) {
       if (threadIdx.x == 0) {
@@ -390,7 +390,7 @@ struct Worker {
       return false;
     }
     // engine.py:319 _branch_on_vertex
-    if (threadIdx.x == 0) atomicAdd(&P.reg.live[h.scope], 1);
+    if (threadIdx.x == 0) lb.inc(P, h.scope);
     // exclude child: built in the second shared-memory buffer, then stored
     {
       const long long words = payload / 16;  // [deg | inc] -> [deg2 | inc2]
@@ -416,12 +416,17 @@ struct Worker {
     }
     __syncthreads();
     tick(PH_EXCLUDE);
+    // the include child continues here: its scope best is read now and
+    // consumed after the removal (the load overlaps it)
+    int kk = 0;
+    if (threadIdx.x == 0) kk = ld_relaxed(&P.reg.key[h.scope]);
     int e2 = remove_vertex(w, v);
     if (threadIdx.x == 0) {
       h.S = S + 1;
       h.E = E - e2;
       h.depth += 1;
       if (top + 1 > max_depth) max_depth = top + 1;
+      st->best_s = kk >> 1;
     }
     __syncthreads();
     tick(PH_INCLUDE);
@@ -440,6 +445,10 @@ struct Worker {
     atomicAdd(&c->rec_in, rec_in);
     atomicAdd(&c->rec_out, rec_out);
     for (int i = 0; i < 10; ++i) atomicAdd(&c->phase[i], ph[i]);
+    for (int i = 0; i < 4; ++i) {
+      atomicAdd(&c->rcyc[i], w.bs->rcyc[i]);
+      atomicAdd(&c->rcnt[i], w.bs->rcnt[i]);
+    }
   }
 };
 
@@ -466,6 +475,9 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
     ws.tmin[i] = kInf;
     ws.flag[i] = 0;
   }
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 4; ++i) bs.rcyc[i] = bs.rcnt[i] = 0;
+  init_block_scratch(&bs);
   if (!P.record) {
     ws.inc = nullptr;
     ws.inc2 = nullptr;
@@ -499,7 +511,7 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
     if (!cont) {
       if (wk.top > 0) {
         wk.top -= 1;
-        load_node(wk.stack_slot(wk.top), &st.hdr, ws.deg, wk.payload);
+        load_node(wk.stack_slot(wk.top), &st.hdr, ws.deg, wk.payload, P.reg.key, &st.best_s);
         if (threadIdx.x == 0) ++wk.rec_in;
         __syncthreads();
       } else {
@@ -511,14 +523,17 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
         __syncthreads();
         long long pos = ((long long)st.qpos_hi << 32) | (unsigned)st.qpos_lo;
         if (pos < 0) {
-          if (threadIdx.x == 0) __nanosleep(backoff);
+          if (threadIdx.x == 0) {
+            wk.lb.flush(P);  // idle: release every held-back decrement
+            __nanosleep(backoff);
+          }
           backoff = backoff < 4096 ? backoff * 2 : 4096;
           __syncthreads();
           wk.tick(PH_IDLE);
           continue;
         }
         backoff = 32;
-        load_node(wk.queue_slot(pos), &st.hdr, ws.deg, wk.payload);
+        load_node(wk.queue_slot(pos), &st.hdr, ws.deg, wk.payload, P.reg.key, &st.best_s);
         __syncthreads();
         if (threadIdx.x == 0) {
           q_release_pop(P.q, pos);
@@ -532,6 +547,7 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
   }
   // stop: release the registry slots of abandoned work (engine.py:235-243)
   if (threadIdx.x == 0) {
+    wk.lb.flush(P);
     if (cont) reg_finish(P, st.hdr.scope);
     for (int i = wk.top - 1; i >= 0; --i) {
       const NodeHdr* hh = (const NodeHdr*)wk.stack_slot(i);

@@ -52,6 +52,7 @@ struct Ctl {
   unsigned long long deadline_ns;      // %globaltimer deadline, 0 = none
   int root_key, reg_count;             // written by the drain kernel for readback
   unsigned long long phase[10];        // SM cycles per phase, summed over blocks (thread 0)
+  unsigned long long rcyc[4], rcnt[4]; // fixpoint profile: scan, degree-one, triangle, high-degree
 };
 
 // phases of a block's time (clock64 deltas taken by thread 0)
@@ -63,6 +64,7 @@ struct Queue {
   unsigned long long* head;
   unsigned long long* tail;
   unsigned long long* count;  // records claimed by producers minus by consumers
+  int* err;                   // Ctl::error, for the spin watchdogs
   char* data;
   long long cap;
 };
@@ -91,6 +93,7 @@ struct SearchParams {
   int root_index;
   int root_in_stack;
   int record;             // record-cover mode: nodes carry inclusion bitsets
+  int batch_live;         // parallel mode: LiveBatch decrement batching
   int nw;                 // bitset words per record
   unsigned* wbits;        // witness arena [wcap][nw]
   int* wcount;
@@ -108,12 +111,12 @@ __host__ __device__ inline long long bits_bytes(int n) {
   return (nw * 4 + 15) & ~15LL;
 }
 
-// workspace bytes for one block: [deg | inc | deg2 | inc2 | flag | 7 int arrays]
+// workspace bytes for one block: [deg | inc | deg2 | inc2 | flag | 8 int arrays]
 template <typename T>
 __host__ __device__ inline long long ws_bytes(int n) {
   long long nn = n > 0 ? n : 1;
   return 2 * (deg_bytes<T>((int)nn) + bits_bytes((int)nn)) + ((nn + 15) & ~15LL) +
-         7LL * 4LL * ((nn + 3) & ~3LL);
+         8LL * 4LL * ((nn + 3) & ~3LL);
 }
 
 // bytes of the reduced CSR staged in shared memory (int32 offsets + neighbours)
@@ -145,6 +148,7 @@ __device__ inline NodeWs<T> carve_ws(char* base, int n, BlockScratch* bs, const 
   w.lst = ip + 3 * ni;
   w.ib = ip + 4 * ni;  // ib, ic and the spare that follows are contiguous:
   w.ic = ip + 5 * ni;  // component aggregates (5 ints x <= n/2 comps) use them
+  w.par = ip + 7 * ni;
   w.bs = bs;
   w.off = off;
   w.nbr = nbr;
@@ -175,7 +179,14 @@ __device__ inline long long q_reserve_push(const Queue& q, long long limit) {
   }
   long long pos = atom_add_ll(q.tail, 1);
   // the slot is free once its previous consumer has released it
-  while ((long long)ld_acquire_u64(&q.seq[pos % q.cap]) != pos) __nanosleep(32);
+  unsigned spins = 0;
+  while ((long long)ld_acquire_u64(&q.seq[pos % q.cap]) != pos) {
+    __nanosleep(32);
+    if (++spins == (1u << 26)) {
+      atomicExch(q.err, 6);  // watchdog: slot never released
+      break;
+    }
+  }
   return pos;
 }
 
@@ -194,7 +205,14 @@ __device__ inline long long q_reserve_pop(const Queue& q) {
   }
   long long pos = atom_add_ll(q.head, 1);
   // the ticket's producer is committed: wait for its publication
-  while ((long long)ld_acquire_u64(&q.seq[pos % q.cap]) != pos + 1) __nanosleep(32);
+  unsigned spins = 0;
+  while ((long long)ld_acquire_u64(&q.seq[pos % q.cap]) != pos + 1) {
+    __nanosleep(32);
+    if (++spins == (1u << 26)) {
+      atomicExch(q.err, 7);  // watchdog: ticket never published
+      break;
+    }
+  }
   return pos;
 }
 
@@ -301,15 +319,47 @@ __device__ inline void reg_finish(const SearchParams& P, int scope) {
   if (atom_dec_acq_rel(&P.reg.live[scope]) == 1) reg_cascade(P, scope);
 }
 
+// Parallel-mode batching of LiveNodes updates (thread 0 of a block).  A
+// finished node's decrement is held back and cancelled against the block's
+// next increment on the same scope; it is flushed the moment the block
+// touches another scope or idles.  While the block works in scope s, s has a
+// live node (the block's own), so holding s's decrements delays no cascade.
+// Increments are never deferred, so a counter can only read high.
+struct LiveBatch {
+  int scope = -1;
+  int pending = 0;
+  int enabled = 0;
+
+  __device__ void flush(const SearchParams& P);
+  __device__ void finish(const SearchParams& P, int s, bool submitted);
+  __device__ void inc(const SearchParams& P, int s);
+};
+
+// a pruned node submitted nothing: no release needed, only the last finisher
+// needs to acquire before cascading
+__device__ inline void reg_finish_pruned(const SearchParams& P, int scope) {
+  if (atomicSub(&P.reg.live[scope], 1) == 1) {
+    __threadfence();
+    reg_cascade(P, scope);
+  }
+}
+
 
 
 // ------------------------------------------------------------ node moves --
 
 // payload = degree array (+ inclusion bitset in record-cover mode); the
 // shared-memory layout keeps them contiguous, like the record
-__device__ inline void load_node(const char* src, NodeHdr* hdr, void* payload, long long bytes) {
+// The scope's best (engine.py:279 best_snapshot) is fetched by the thread
+// that loads the header's scope word, overlapped with the payload copy.
+__device__ inline void load_node(const char* src, NodeHdr* hdr, void* payload, long long bytes,
+                                 const int* keys, int* best_out) {
   const uint4* s = (const uint4*)src;
-  if (threadIdx.x < 2) ((uint4*)hdr)[threadIdx.x] = __ldcg(s + threadIdx.x);
+  if (threadIdx.x < 2) {
+    uint4 h = __ldcg(s + threadIdx.x);
+    ((uint4*)hdr)[threadIdx.x] = h;
+    if (threadIdx.x == 1) *best_out = ld_relaxed(&keys[(int)h.x]) >> 1;  // h.x == scope
+  }
   const long long words = bytes / 16;
   const uint4* sd = s + 2;
   uint4* dd = (uint4*)payload;
@@ -321,6 +371,42 @@ __device__ inline void store_payload(char* dst, const void* payload, long long b
   uint4* dd = (uint4*)(dst + sizeof(NodeHdr));
   const uint4* sd = (const uint4*)payload;
   for (long long i = threadIdx.x; i < words; i += blockDim.x) __stcg(dd + i, sd[i]);
+}
+
+__device__ inline void LiveBatch::flush(const SearchParams& P) {
+  if (pending > 0) {
+    const int k = pending;
+    pending = 0;
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;"
+                 : "=r"(old) : "l"(&P.reg.live[scope]), "r"(-k) : "memory");
+    if (old == k) reg_cascade(P, scope);
+  }
+  scope = -1;
+}
+
+__device__ inline void LiveBatch::finish(const SearchParams& P, int s, bool submitted) {
+  if (!enabled) {
+    if (submitted) reg_finish(P, s);
+    else reg_finish_pruned(P, s);
+    return;
+  }
+  if (s != scope) {
+    flush(P);
+    scope = s;
+  }
+  ++pending;
+}
+
+__device__ inline void LiveBatch::inc(const SearchParams& P, int s) {
+  if (enabled) {
+    if (s == scope && pending > 0) {
+      --pending;
+      return;
+    }
+    flush(P);
+  }
+  atomicAdd(&P.reg.live[s], 1);
 }
 
 }  // namespace vcg

@@ -222,7 +222,7 @@ def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
     t0 = time.perf_counter()
     bound = cfg.k if cfg.mode == "pvc" else None
     pre = root_reduce(g, enabled=cfg.use_root_reduce, crown=cfg.use_crown, bound=bound,
-                      width_override=cfg.width)
+                      width_override=cfg.width, need_greedy_original=bound is None)
     stats.phase_seconds["root_reduce"] = time.perf_counter() - t0
     for key, val in pre.rule_counts.items():
         stats.rule_counts[key] = stats.rule_counts.get(key, 0) + val
@@ -268,6 +268,9 @@ def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
     stats.phase_seconds["search"] = time.perf_counter() - t1
     result.search_ms = float(res.kernel_ms)
     result.phase_cycles = dict(zip(_lib.PHASES, (int(x) for x in res.phase_cycles)))
+    for i, nm in enumerate(("scan", "degree_one", "triangle", "high_degree")):
+        result.phase_cycles[f"fix_{nm}_cycles"] = int(res.fix_cycles[i])
+        result.phase_cycles[f"fix_{nm}_count"] = int(res.fix_count[i])
     stats.tree_nodes_visited = int(res.tree_nodes_visited)
     stats.component_branches = int(res.component_branches)
     stats.components_per_branch = hist

@@ -11,9 +11,13 @@ for label, kw in [("det-mvc", dict(deterministic=True)), ("pvc-1 w296", dict(mod
                   ("pvc-1 all", dict(mode="pvc", k=opt - 1))]:
     for th in (64, 128, 256):
         r = vc.solve(g, vc.SolverConfig(threads=th, **kw))
-        pc = r.phase_cycles
+        pc = {k: v for k, v in r.phase_cycles.items() if not k.startswith("fix_")}
+        fx = {k: v for k, v in r.phase_cycles.items() if k.startswith("fix_")}
         tot = sum(pc.values())
         nodes = r.stats.tree_nodes_visited
         busy = tot - pc["idle"]
         print(f"{label:11s} th={th:3d} kern={r.search_ms:8.2f} ms nodes={nodes} busy-cyc/node={busy/nodes:8.0f} "
               + " ".join(f"{k}={v/tot*100:4.1f}%" for k, v in pc.items()), flush=True)
+        print("   fixpoint: " + " ".join(
+            f"{nm}: {fx[f'fix_{nm}_count']/nodes:.2f}/node x {fx[f'fix_{nm}_cycles']/max(fx[f'fix_{nm}_count'],1):.0f} cyc"
+            for nm in ("scan", "degree_one", "triangle", "high_degree")), flush=True)

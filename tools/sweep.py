@@ -9,7 +9,7 @@ n, off, nbr = synth.WORKLOADS[name]()
 g = vc.StaticGraph(n, off, nbr)
 opt = vc.solve(g, vc.SolverConfig()).cover_size
 print("opt", opt, flush=True)
-for thr, threads, workers in itertools.product([0, 64, 256], [128, 256], [296, 444, 592, 0]):
+for thr, threads, workers in itertools.product([0], [32, 64, 128, 256, 512], [0, 148 * 2, 148 * 4, 148 * 8]):
     tk = []
     for k in (opt, opt - 1):
         best = None
