@@ -102,6 +102,9 @@ typedef struct {
   int record_cover;           /* nodes carry cover bitsets; witnesses are recorded */
   int32_t* cover_out;         /* record_cover: receives a cover of the reduced graph
                                  (capacity n) whose size is <= best */
+  const int32_t* root_deg;    /* NULL: search the whole graph.  Else the residual
+                                 degree array (n entries) of a subtree root, e.g. one
+                                 produced by vcg_expand; covers are counted from it */
 } vcg_search_config;
 
 typedef struct {
@@ -136,6 +139,30 @@ typedef struct {
  * receives the components-per-branch histogram indexed by component count. */
 int vcg_search(const vcg_graph* g, const vcg_search_config* cfg, vcg_search_result* res,
                int64_t* hist_out);
+
+/* Breadth-first expansion of the root's search tree on the device (one
+ * block), with the reference's node semantics (engine.py:277): reduce,
+ * prune, leaf, or branch on the max-degree vertex; a node whose residual
+ * graph is disconnected is not expanded (its subtree handles the split).
+ * Stops once `target` open subtrees exist.  Each open subtree i gets its
+ * cover-so-far sub_S[i] and residual degrees sub_deg[i*n .. i*n+n).
+ * The subtrees partition the remaining search: MVC = min(best, min_i(sub_S[i]
+ * + MVC(subtree i))) -- the unit of multi-GPU partitioning. */
+typedef struct {
+  int64_t target;
+  int64_t best_init;          /* root scope bound, as for vcg_search */
+  int use_components;
+  int use_bounds;
+} vcg_expand_config;
+
+typedef struct {
+  int64_t count;              /* open subtrees written */
+  int64_t best;               /* best cover found by leaves during the expansion */
+  int64_t nodes;              /* tree nodes processed by the expansion */
+} vcg_expand_result;
+
+int vcg_expand(const vcg_graph* g, const vcg_expand_config* cfg, vcg_expand_result* res,
+               int32_t* sub_S, int32_t* sub_deg, int64_t capacity);
 
 /* One per-node kernel on the device (parity surface of vcsolver.kernels).
  * op: 0 degree_one_pass, 1 degree_two_triangle_pass, 2 high_degree_pass,

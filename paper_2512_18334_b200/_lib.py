@@ -38,8 +38,17 @@ class SearchConfig_t(C.Structure):
         ("disable_pruning", C.c_int), ("deterministic", C.c_int), ("load_balance", C.c_int),
         ("workers", C.c_int), ("threads", C.c_int), ("worklist_threshold", I64),
         ("timeout", C.c_double), ("check_registry", C.c_int), ("record_cover", C.c_int),
-        ("cover_out", C.c_void_p),
+        ("cover_out", C.c_void_p), ("root_deg", C.c_void_p),
     ]
+
+
+class ExpandConfig_t(C.Structure):
+    _fields_ = [("target", I64), ("best_init", I64), ("use_components", C.c_int),
+                ("use_bounds", C.c_int)]
+
+
+class ExpandResult_t(C.Structure):
+    _fields_ = [("count", I64), ("best", I64), ("nodes", I64)]
 
 
 class SearchResult_t(C.Structure):
@@ -63,7 +72,7 @@ EXPORTS = (
     "vcg_graph_create", "vcg_graph_destroy", "vcg_graph_num_vertices", "vcg_graph_num_edges",
     "vcg_graph_download", "vcg_induced_subgraph", "vcg_greedy_bound", "vcg_root_reduce",
     "vcg_search", "vcg_node_op", "vcg_last_error", "vcg_device_count", "vcg_launch_count",
-    "vcg_set_device",
+    "vcg_set_device", "vcg_expand",
 )
 
 
@@ -97,6 +106,7 @@ def _load():
     lib.vcg_root_reduce.argtypes = [P, C.c_int, C.c_int, C.c_int, I64,
                                     C.POINTER(Preprocessed_t), P, P, C.POINTER(P)]
     lib.vcg_search.argtypes = [P, C.POINTER(SearchConfig_t), C.POINTER(SearchResult_t), P]
+    lib.vcg_expand.argtypes = [P, C.POINTER(ExpandConfig_t), C.POINTER(ExpandResult_t), P, P, I64]
     lib.vcg_node_op.argtypes = [C.c_int, C.c_int, I64, P, P, P, I64, I64, I64, I64, P, I64, P]
     return lib
 

@@ -633,6 +633,173 @@ extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int h
   return 0;
 }
 
+// -------------------------------------------------------------- expansion --
+// FIFO of int32-degree node records in HBM: [S, E, lo, hi, split, pad, pad, pad | deg[n]]
+
+__global__ void k_expand(int n, const int32_t* off, const int32_t* nbr, char* wsmem, char* fifo,
+                         long long rec_bytes, long long cap, long long target, int best_init,
+                         int use_components, int use_bounds, long long* out) {
+  __shared__ BlockScratch bs;
+  __shared__ int sh[8];
+  init_block_scratch(&bs);
+  NodeWs<uint32_t> w = carve_ws<uint32_t>(wsmem, n, &bs, off, nbr);
+  w.inc = w.inc2 = nullptr;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    w.tmin[i] = kInf;
+    w.flag[i] = 0;
+  }
+  __syncthreads();
+  long long head = 0, tail = 1, nodes = 0;
+  int best = best_init;
+  auto rec = [&](long long i) { return fifo + (i % cap) * rec_bytes; };
+  // splits stay open: they are moved behind the tail and never expanded
+  long long open_splits = 0;
+  while (head < tail && (tail - head) < target) {
+    int* hd = (int*)rec(head);
+    if (hd[4]) {  // an unexpanded split node: rotate it behind the tail
+      if (open_splits >= tail - head) break;  // only splits left
+      if (tail - head + 1 > cap) break;
+      int* dstr = (int*)rec(tail);
+      for (long long i = threadIdx.x; i < rec_bytes / 4; i += blockDim.x) dstr[i] = hd[i];
+      __syncthreads();
+      ++head;
+      ++tail;
+      ++open_splits;
+      continue;
+    }
+    open_splits = 0;
+    const int S0 = hd[0], E0 = hd[1], lo0 = hd[2], hi0 = hd[3];
+    uint32_t* dg = (uint32_t*)(hd + 8);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) w.deg[i] = dg[i];
+    __syncthreads();
+    ++head;
+    ++nodes;
+    long long maxkey;
+    FixRet fr = reduce_fixpoint_fast(w, lo0, hi0, best - S0 - 1, &maxkey);
+    int S = S0 + fr.forced, E = E0 - fr.edges, lo = fr.lo, hi = fr.hi;
+    if (!use_bounds && n) {
+      lo = 0;
+      hi = n - 1;
+    }
+    bool prune = S >= best;
+    if (!prune) {
+      long long rem = (long long)best - S - 1;
+      prune = (long long)E > rem * rem;
+    }
+    if (prune) continue;
+    if (E == 0) {
+      best = S;  // a leaf: the cover found so far is the new bound
+      continue;
+    }
+    int split = 0;
+    if (use_components) {
+      int nc = label_components(w, lo, hi, true);
+      split = nc > 1;
+    }
+    if (tail + 2 - head > cap) break;
+    int* c1 = (int*)rec(tail);
+    uint32_t* d1 = (uint32_t*)(c1 + 8);
+    if (split) {  // keep the node (after its reduction) as an open subtree
+      for (int i = threadIdx.x; i < n; i += blockDim.x) d1[i] = w.deg[i];
+      if (threadIdx.x == 0) {
+        c1[0] = S;
+        c1[1] = E;
+        c1[2] = lo;
+        c1[3] = hi;
+        c1[4] = 1;
+      }
+      __syncthreads();
+      ++tail;
+      continue;
+    }
+    const int v = maxkey < 0 ? -1 : 0x7fffffff - (int)(maxkey & 0xffffffffLL);
+    // exclude child (N(v) forced) first, then include child (v forced)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) w.deg2[i] = w.deg[i];
+    __syncthreads();
+    NodeWs<uint32_t> wx = w;
+    wx.deg = w.deg2;
+    int removed, edges;
+    remove_neighbors_fast(wx, v, w.lst, &removed, &edges);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) d1[i] = w.deg2[i];
+    if (threadIdx.x == 0) {
+      c1[0] = S + removed;
+      c1[1] = E - edges;
+      c1[2] = lo;
+      c1[3] = hi;
+      c1[4] = 0;
+    }
+    int e2 = remove_vertex(w, v);
+    int* c2 = (int*)rec(tail + 1);
+    uint32_t* d2 = (uint32_t*)(c2 + 8);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) d2[i] = w.deg[i];
+    if (threadIdx.x == 0) {
+      c2[0] = S + 1;
+      c2[1] = E - e2;
+      c2[2] = lo;
+      c2[3] = hi;
+      c2[4] = 0;
+    }
+    __syncthreads();
+    tail += 2;
+  }
+  if (threadIdx.x == 0) {
+    out[0] = head;
+    out[1] = tail;
+    out[2] = best;
+    out[3] = nodes;
+  }
+  (void)sh;
+}
+
+extern "C" int vcg_expand(const vcg_graph* g, const vcg_expand_config* cfg, vcg_expand_result* res,
+                          int32_t* sub_S, int32_t* sub_deg, int64_t capacity) {
+  if (int r = need_device()) return r;
+  if (!g || !cfg || !res || cfg->target < 1) return fail(VCG_EINVAL, "bad arguments");
+  const int n = (int)g->n;
+  const long long rec_bytes = 32 + 4LL * ((n + 3) & ~3);
+  const long long cap = 2 * cfg->target + 8;
+  DevBuf ws, fifo, out;
+  if (ws.ensure(ws_total<uint32_t>(n)) || fifo.ensure((size_t)(cap * rec_bytes)) || out.ensure(64))
+    return VCG_ERESOURCE;
+  std::vector<int32_t> root(rec_bytes / 4, 0);
+  int lo = -1, hi = -1;
+  for (int v = 0; v < n; ++v) {
+    int d = (int)(g->h_off[v + 1] - g->h_off[v]);
+    root[8 + v] = d;
+    if (d) {
+      if (lo < 0) lo = v;
+      hi = v;
+    }
+  }
+  root[0] = 0;
+  root[1] = (int)(g->m2 / 2);
+  root[2] = lo < 0 ? (n > 1 ? n : 1) : lo;
+  root[3] = lo < 0 ? 0 : hi;
+  CK(cudaMemcpy(fifo.p, root.data(), rec_bytes, cudaMemcpyHostToDevice));
+  COUNT_LAUNCH(1);
+  k_expand<<<1, 512>>>(n, g->d_off.as<int32_t>(), g->d_nbr.as<int32_t>(), ws.as<char>(),
+                       fifo.as<char>(), rec_bytes, cap, cfg->target, (int)cfg->best_init,
+                       cfg->use_components, cfg->use_bounds, out.as<long long>());
+  CK(cudaGetLastError());
+  long long o[4];
+  CK(cudaMemcpy(o, out.p, 32, cudaMemcpyDeviceToHost));
+  const long long head = o[0], tail = o[1];
+  memset(res, 0, sizeof(*res));
+  res->best = o[2];
+  res->nodes = o[3];
+  const long long count = tail - head;
+  if (count > capacity) return fail(VCG_ERESOURCE, "expansion capacity too small");
+  std::vector<int32_t> buf(rec_bytes / 4);
+  for (long long i = 0; i < count; ++i) {
+    CK(cudaMemcpy(buf.data(), fifo.as<char>() + ((head + i) % cap) * rec_bytes, rec_bytes,
+                  cudaMemcpyDeviceToHost));
+    sub_S[i] = buf[0];
+    memcpy(sub_deg + i * (int64_t)n, buf.data() + 8, (size_t)n * 4);
+  }
+  res->count = count;
+  return 0;
+}
+
 // ----------------------------------------------------------------- search --
 
 
@@ -759,20 +926,22 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   NodeHdr* hh = (NodeHdr*)rec.data();
   T* rdeg = (T*)(rec.data() + sizeof(NodeHdr));
   int lo = -1, hi = -1;
+  int64_t dsum = 0;
   for (int v = 0; v < n; ++v) {
-    int64_t d = g->h_off[v + 1] - g->h_off[v];
+    int64_t d = cfg->root_deg ? cfg->root_deg[v] : g->h_off[v + 1] - g->h_off[v];
     rdeg[v] = (T)d;
+    dsum += d;
     if (d) {
       if (lo < 0) lo = v;
       hi = v;
     }
   }
-  if (lo < 0 || g->m2 == 0) {
+  if (lo < 0 || dsum == 0) {
     lo = n > 1 ? n : 1;
     hi = 0;
   }
   hh->S = 0;
-  hh->E = (int)(g->m2 / 2);
+  hh->E = (int)(dsum / 2);
   hh->lo = lo;
   hh->hi = hi;
   hh->scope = 0;
@@ -916,6 +1085,11 @@ extern "C" int vcg_search(const vcg_graph* g, const vcg_search_config* cfg, vcg_
   if (int r = need_device()) return r;
   if (!g || !cfg || !res) return fail(VCG_EINVAL, "bad arguments");
   if (g->n == 0 || g->m2 == 0) return fail(VCG_EINVAL, "search needs a graph with edges");
+  if (cfg->root_deg) {
+    int64_t dsum = 0;
+    for (int64_t v = 0; v < g->n; ++v) dsum += cfg->root_deg[v];
+    if (dsum == 0) return fail(VCG_EINVAL, "subtree root has no edges");
+  }
   if (cfg->width == 8) return search_t<uint8_t>(g, cfg, res, hist_out);
   if (cfg->width == 16) return search_t<uint16_t>(g, cfg, res, hist_out);
   if (cfg->width == 32) return search_t<uint32_t>(g, cfg, res, hist_out);

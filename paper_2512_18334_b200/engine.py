@@ -141,7 +141,8 @@ class SolveResult:
 
 
 def run_search(rg: StaticGraph, cfg: SolverConfig, width: int, best_init: int,
-               achieved_init: bool, k_red: int | None, record: bool = False):
+               achieved_init: bool, k_red: int | None, record: bool = False,
+               config_hook=None):
     """One vcg_search call; returns (SearchResult_t, histogram dict, cover or None).
 
     With ``record`` the nodes carry scoped cover bitsets and the kernel
@@ -168,6 +169,8 @@ def run_search(rg: StaticGraph, cfg: SolverConfig, width: int, best_init: int,
         cover = np.zeros(max(rg.num_vertices, 1), dtype=np.int32)
         sc.record_cover = 1
         sc.cover_out = cover.ctypes.data
+    if config_hook is not None:
+        config_hook(sc)  # e.g. seed the search with a subtree root (distributed.py)
     res = _lib.SearchResult_t()
     hist = np.zeros(rg.num_vertices + 2, dtype=np.int64)
     _lib.check(_lib.lib.vcg_search(rg.device().handle, C.byref(sc), C.byref(res),
