@@ -40,6 +40,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="weak", choices=["weak", "strong"],
+                    help="weak: each rank solves its own seeded instance; strong: all ranks "
+                         "solve instance 1 together (root-subtree partition + bound exchange)")
     return ap.parse_args()
 
 
@@ -201,9 +204,12 @@ def run_b200(args):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    n, off, nbr = instance(1 + rank)
+    strong = args.mode == "strong" and world > 1
+    n, off, nbr = instance(1 if strong else 1 + rank)
     g = vc.StaticGraph(n, off, nbr)
     opt = vc.solve(g, vc.SolverConfig()).cover_size  # untimed: defines the pair
+    if strong:
+        from paper_2512_18334_b200.distributed import solve_distributed
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
     def barrier():
@@ -214,7 +220,10 @@ def run_b200(args):
     def pair(graph):
         nodes = kms = 0.0
         for k, want in ((opt, True), (opt - 1, False)):
-            r = vc.solve(graph, vc.SolverConfig(mode="pvc", k=k))
+            if strong:
+                r = solve_distributed(graph, vc.SolverConfig(mode="pvc", k=k))
+            else:
+                r = vc.solve(graph, vc.SolverConfig(mode="pvc", k=k))
             if r.found != want:
                 raise RuntimeError(f"PVC k={k}: found={r.found}, expected {want}")
             nodes += r.stats.tree_nodes_visited
@@ -284,7 +293,10 @@ def run_b200(args):
         tsum = t.clone()
         torch.distributed.all_reduce(tsum, op=torch.distributed.ReduceOp.SUM)
         total_ms, e2e_ms = float(tmax[0]), float(tmax[2])
-        nodes, e2e_nodes = float(tsum[1]), float(tsum[3])
+        if strong:  # solve_distributed already reports whole-job node counts
+            nodes, e2e_nodes = float(t[1]), float(t[3])
+        else:
+            nodes, e2e_nodes = float(tsum[1]), float(tsum[3])
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -312,12 +324,15 @@ def run_b200(args):
         "ms_per_step": total_ms / args.steps,
         "time_to_solution_s": total_ms / args.steps * 1e-3,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None,
         "dtype": "int32",
-        "data": "synthetic (seeded random geometric graph, seed 1 + rank)",
+        "data": "synthetic (seeded random geometric graph, seed 1)" if strong else
+                "synthetic (seeded random geometric graph, seed 1 + rank)",
         "config": {"workload": WORKLOAD, "opt": opt, "n": n, "m": len(nbr) // 2,
-                   "parallelism": f"dp{world} (independent instances)",
+                   "parallelism": (f"{world} GPUs on one instance (root-subtree partition, "
+                                   "NCCL MIN all-reduce of the bound)") if strong else
+                                  f"dp{world} (independent instances)",
                    "l2": "flushed between timed steps (512 MiB write)"},
         "e2e": {"value": e2e_nodes / (e2e_ms * 1e-3), "unit": "nodes/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -647,6 +647,7 @@ __global__ void k_expand(int n, const int32_t* off, const int32_t* nbr, char* ws
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     w.tmin[i] = kInf;
     w.flag[i] = 0;
+    if (i < (n + 31) / 32) w.vbits[i] = 0u;
   }
   __syncthreads();
   long long head = 0, tail = 1, nodes = 0;

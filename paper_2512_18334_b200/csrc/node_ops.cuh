@@ -255,6 +255,7 @@ struct NodeWs {
   int* lst;         // [n]
   int* id;          // [n]
   int* par;         // [n] union-find parents (component labels)
+  unsigned* vbits;  // [ceil(n/32)] candidate bitmap, all-zero between sweeps
   uint8_t* flag;    // [n], kept == 0 between operations
   unsigned* inc;    // cover-membership bitset of the node (record-cover mode), else null
   unsigned* inc2;   // bitset of the exclude child under construction
@@ -819,6 +820,67 @@ __device__ PassRet degree_one_pass_fast(const NodeWs<T>& w, int b, int e, int nc
   return PassRet{total, total, edges, 0};
 }
 
+// triangle sweep (pure.py:113) for the search: valid candidates are marked
+// in a bitmap (w.vbits, all-zero between sweeps); lane 0 walks it in index
+// order -- exactly the reference's in-order conflict resolution -- clearing
+// each word as it goes; removals use the one-barrier path.
+template <typename T>
+__device__ PassRet degree_two_triangle_pass_fast(const NodeWs<T>& w, int b, int e, int* rem) {
+  unsigned* vbits = w.vbits;
+  int nvalid = 0;
+  for (int v = b; v < e; ++v) {
+    if (w.deg[v] == 2) {
+      int u = -1, x2 = -1;
+      for (int i = w.off[v]; i < w.off[v + 1]; ++i) {
+        int x = w.nbr[i];
+        if (w.deg[x] > 0) {
+          if (u < 0) {
+            u = x;
+          } else {
+            x2 = x;
+            break;
+          }
+        }
+      }
+      if (x2 >= 0 && adjacent_static(w, u, x2)) {
+        w.ia[v] = u;
+        w.ib[v] = x2;
+        atomicOr(&vbits[v >> 5], 1u << (v & 31));
+        ++nvalid;
+      }
+    }
+  }
+  nvalid = block_sum(nvalid, w.bs);
+  if (nvalid == 0) return PassRet{0, 0, 0, 0};
+  if (threadIdx.x == 0) {
+    int p = 0, applied = 0;
+    const int w0 = b >> 5;  // thread 0's chunk starts at the window start
+    int found = 0;
+    for (int wi = w0; found < nvalid; ++wi) {
+      unsigned m = vbits[wi];
+      vbits[wi] = 0u;
+      while (m) {
+        const int v = (wi << 5) + __ffs(m) - 1;
+        m &= m - 1;
+        ++found;
+        const int u = w.ia[v], x2 = w.ib[v];
+        if (!w.flag[v] && !w.flag[u] && !w.flag[x2]) {
+          w.flag[u] = 1;
+          w.flag[x2] = 1;
+          rem[p++] = u;
+          rem[p++] = x2;
+          ++applied;
+        }
+      }
+    }
+    w.bs->bc[0] = applied;
+  }
+  __syncthreads();
+  const int applied = w.bs->bc[0];
+  int edges = remove_list_fast(w, rem, 2 * applied);
+  return PassRet{applied, 2 * applied, edges, 0};
+}
+
 // reduce_fixpoint (pure.py:188) for the search: identical forced sets and
 // counters; one fused scan decides which sweeps have candidates.
 template <typename T>
@@ -866,7 +928,7 @@ __device__ FixRet reduce_fixpoint_fast(const NodeWs<T>& w, int lo, int hi, int b
     }
     int tri = 0;
     if (st.c2 > 0) {
-      PassRet t = degree_two_triangle_pass(w, lo, hi, rem, 0);
+      PassRet t = degree_two_triangle_pass_fast(w, b, e, rem);
       rprof(w.bs, 2, &t0);
       tri = t.applied;
       r.d2t += t.applied;

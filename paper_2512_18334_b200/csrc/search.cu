@@ -473,6 +473,7 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
   }
   for (int i = threadIdx.x; i < P.n; i += blockDim.x) {
     ws.tmin[i] = kInf;
+    if (i < (P.n + 31) / 32) ws.vbits[i] = 0u;
     ws.flag[i] = 0;
   }
   if (threadIdx.x == 0)

@@ -111,12 +111,12 @@ __host__ __device__ inline long long bits_bytes(int n) {
   return (nw * 4 + 15) & ~15LL;
 }
 
-// workspace bytes for one block: [deg | inc | deg2 | inc2 | flag | 8 int arrays]
+// workspace bytes for one block: [deg | inc | deg2 | inc2 | flag | 8 int arrays | bitmap]
 template <typename T>
 __host__ __device__ inline long long ws_bytes(int n) {
   long long nn = n > 0 ? n : 1;
   return 2 * (deg_bytes<T>((int)nn) + bits_bytes((int)nn)) + ((nn + 15) & ~15LL) +
-         8LL * 4LL * ((nn + 3) & ~3LL);
+         8LL * 4LL * ((nn + 3) & ~3LL) + bits_bytes((int)nn);
 }
 
 // bytes of the reduced CSR staged in shared memory (int32 offsets + neighbours)
@@ -149,6 +149,7 @@ __device__ inline NodeWs<T> carve_ws(char* base, int n, BlockScratch* bs, const 
   w.ib = ip + 4 * ni;  // ib, ic and the spare that follows are contiguous:
   w.ic = ip + 5 * ni;  // component aggregates (5 ints x <= n/2 comps) use them
   w.par = ip + 7 * ni;
+  w.vbits = (unsigned*)(ip + 8 * ni);
   w.bs = bs;
   w.off = off;
   w.nbr = nbr;
