@@ -107,6 +107,9 @@ struct DevBuf {
 
 struct SearchCtx {
   DevBuf stacks, qseq, qdata, qctl, reg, ctl, hist, gws, wbits, wcount;
+  // root pipeline / compaction / expansion scratch, reused across calls
+  // (per-call cudaMalloc/cudaFree of tens of MB costs milliseconds, with outliers)
+  DevBuf r_flag, r_ws, r_out, r_ret, c_newid, c_cnt, c_vmap, c_tmp, x_ws, x_fifo, x_out;
 };
 
 struct vcg_graph {
@@ -241,7 +244,8 @@ static int exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t count, De
 static int compact_flagged(const vcg_graph* g, DevBuf& flag, vcg_graph** out,
                            std::vector<int64_t>* vmap_host) {
   const int n = (int)g->n;
-  DevBuf newid, cnt, noff, vmap, tmp;
+  SearchCtx& X = search_ctx();
+  DevBuf &newid = X.c_newid, &cnt = X.c_cnt, &vmap = X.c_vmap, &tmp = X.c_tmp;
   if (newid.ensure((size_t)(n + 1) * 4) || cnt.ensure((size_t)(n + 1) * 4) ||
       vmap.ensure((size_t)(n + 1) * 4))
     return VCG_ERESOURCE;
@@ -515,7 +519,8 @@ extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int h
                           : greedy_cover_host(g->n, g->h_off.data(), g->h_nbr.data(), nullptr);
   const int64_t bound0 = has_bound ? bound : info->greedy_original;
   tr.mark("greedy_original");
-  DevBuf flag;
+  SearchCtx& X = search_ctx();
+  DevBuf& flag = X.r_flag;
   if (flag.ensure((size_t)(n + 1) * 4)) return VCG_ERESOURCE;
   std::vector<int64_t> vmap;
   int64_t forced_count = 0;
@@ -524,7 +529,7 @@ extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int h
     ones[n] = 0;
     CK(cudaMemcpy(flag.p, ones.data(), (size_t)(n + 1) * 4, cudaMemcpyHostToDevice));
   } else {
-    DevBuf ws, dout, dret;
+    DevBuf &ws = X.r_ws, &dout = X.r_out, &dret = X.r_ret;
     if (ws.ensure(ws_total<uint32_t>(n)) || dout.ensure((size_t)(2 * n + 4) * 4) ||
         dret.ensure(64))
       return VCG_ERESOURCE;
@@ -574,6 +579,7 @@ extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int h
       lo = (int)ret[5];
       hi = (int)ret[6];
       info->seconds[0] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      tr.mark("  device rules round");
       if (has_bound && forced_count > bound) break;
       if (crown) {
         auto t1 = std::chrono::steady_clock::now();
@@ -603,6 +609,7 @@ extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int h
           }
         }
         info->seconds[1] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+        tr.mark("  crown round");
       }
       if (progressed == 0) break;
     }
@@ -759,7 +766,8 @@ extern "C" int vcg_expand(const vcg_graph* g, const vcg_expand_config* cfg, vcg_
   const int n = (int)g->n;
   const long long rec_bytes = 32 + 4LL * ((n + 3) & ~3);
   const long long cap = 2 * cfg->target + 8;
-  DevBuf ws, fifo, out;
+  SearchCtx& X = search_ctx();
+  DevBuf &ws = X.x_ws, &fifo = X.x_fifo, &out = X.x_out;
   if (ws.ensure(ws_total<uint32_t>(n)) || fifo.ensure((size_t)(cap * rec_bytes)) || out.ensure(64))
     return VCG_ERESOURCE;
   std::vector<int32_t> root(rec_bytes / 4, 0);

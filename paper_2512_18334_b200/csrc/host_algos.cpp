@@ -14,38 +14,50 @@ namespace vcg {
 // preprocess.py:348 greedy_bound -> pure.py:306 greedy_cover: repeatedly take
 // the lowest-index vertex of maximum residual degree.
 //
-// Degree buckets as two-level bitsets (64-bit words + a summary word per 64
-// words): the pick is "highest non-empty bucket, lowest set bit", a vertex
-// moves one bucket down per removed neighbour.  O(m + picks * n/4096) time;
+// Degree buckets as three-level bitsets (64-bit words, a summary bit per
+// word, a summary bit per summary word): the pick is "highest non-empty bucket, lowest set bit", a vertex
+// moves one bucket down per removed neighbour.  O(m + picks * n/2^18) time;
 // falls back to a lazy max-heap when buckets x n bits would exceed 256 MiB.
 namespace {
 
 struct Buckets {
-  int64_t words, sumw;
-  std::vector<uint64_t> bits, summary;  // [deg][words], [deg][sumw]
+  // per degree bucket: L0 vertex bits, L1 = non-empty L0 words, L2 = non-empty L1 words
+  int64_t w0, w1, w2;
+  std::vector<uint64_t> b0, b1, b2;
   std::vector<int64_t> count;
   Buckets(int64_t n, int64_t maxdeg)
-      : words((n + 63) / 64), sumw((words + 63) / 64),
-        bits((size_t)(maxdeg + 1) * words, 0), summary((size_t)(maxdeg + 1) * sumw, 0),
-        count(maxdeg + 1, 0) {}
+      : w0((n + 63) / 64), w1((w0 + 63) / 64), w2((w1 + 63) / 64),
+        b0((size_t)(maxdeg + 1) * w0, 0), b1((size_t)(maxdeg + 1) * w1, 0),
+        b2((size_t)(maxdeg + 1) * w2, 0), count(maxdeg + 1, 0) {}
   void set(int64_t d, int64_t v) {
-    uint64_t& w = bits[(size_t)d * words + (v >> 6)];
-    if (!w) summary[(size_t)d * sumw + ((v >> 6) >> 6)] |= 1ull << ((v >> 6) & 63);
-    w |= 1ull << (v & 63);
+    const int64_t i0 = v >> 6, i1 = i0 >> 6;
+    uint64_t& a = b0[(size_t)d * w0 + i0];
+    if (!a) {
+      uint64_t& b = b1[(size_t)d * w1 + i1];
+      if (!b) b2[(size_t)d * w2 + (i1 >> 6)] |= 1ull << (i1 & 63);
+      b |= 1ull << (i0 & 63);
+    }
+    a |= 1ull << (v & 63);
     ++count[d];
   }
   void clear(int64_t d, int64_t v) {
-    uint64_t& w = bits[(size_t)d * words + (v >> 6)];
-    w &= ~(1ull << (v & 63));
-    if (!w) summary[(size_t)d * sumw + ((v >> 6) >> 6)] &= ~(1ull << ((v >> 6) & 63));
+    const int64_t i0 = v >> 6, i1 = i0 >> 6;
+    uint64_t& a = b0[(size_t)d * w0 + i0];
+    a &= ~(1ull << (v & 63));
+    if (!a) {
+      uint64_t& b = b1[(size_t)d * w1 + i1];
+      b &= ~(1ull << (i0 & 63));
+      if (!b) b2[(size_t)d * w2 + (i1 >> 6)] &= ~(1ull << (i1 & 63));
+    }
     --count[d];
   }
   int64_t lowest(int64_t d) const {
-    const uint64_t* sm = &summary[(size_t)d * sumw];
-    for (int64_t i = 0; i < sumw; ++i)
-      if (sm[i]) {
-        int64_t wi = i * 64 + __builtin_ctzll(sm[i]);
-        return wi * 64 + __builtin_ctzll(bits[(size_t)d * words + wi]);
+    const uint64_t* l2 = &b2[(size_t)d * w2];
+    for (int64_t i = 0; i < w2; ++i)
+      if (l2[i]) {
+        const int64_t i1 = i * 64 + __builtin_ctzll(l2[i]);
+        const int64_t i0 = i1 * 64 + __builtin_ctzll(b1[(size_t)d * w1 + i1]);
+        return i0 * 64 + __builtin_ctzll(b0[(size_t)d * w0 + i0]);
       }
     return -1;
   }

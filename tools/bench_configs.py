@@ -20,6 +20,7 @@ from paper_2512_18334_b200 import synth  # noqa: E402
 
 BUDGET = float(os.environ.get("BUDGET_S", "10"))
 CPU = os.environ.get("CPU", "1") == "1"
+SKIP_CPU = set(os.environ.get("SKIP_CPU", "").split(","))
 
 
 def gpu_solve(n, off, nbr, reps=3, **kw):
@@ -71,7 +72,7 @@ for name, label in [("er200", "configs[0] MVC G(200, avg deg 4)"),
         e.update(gpu_s=tg, gpu_nodes=r.stats.tree_nodes_visited, gpu_cover=r.cover_size,
                  gpu_exact=r.exact, gpu_search_ms=r.search_ms,
                  gpu_root_s=r.stats.phase_seconds["root_reduce"])
-        if CPU:
+        if CPU and name not in SKIP_CPU:
             tc, rc = cpu_solve(n, off, nbr, deterministic=True, timeout=BUDGET if bounded else None)
             e.update(cpu_s=tc, cpu_nodes=rc["stats"]["tree_nodes_visited"], cpu_cover=rc["cover_size"],
                      cpu_exact=rc["exact"])
