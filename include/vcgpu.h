@@ -105,6 +105,10 @@ typedef struct {
   const int32_t* root_deg;    /* NULL: search the whole graph.  Else the residual
                                  degree array (n entries) of a subtree root, e.g. one
                                  produced by vcg_expand; covers are counted from it */
+  int warp_limit;             /* warp tier: subproblems with <= warp_limit (<= 64) live
+                                 vertices are solved by one warp as bitmask tasks;
+                                 0 = off.  Ignored (off) in deterministic, record-cover,
+                                 no-components and no-pruning runs. */
 } vcg_search_config;
 
 typedef struct {
@@ -133,6 +137,16 @@ typedef struct {
                                  root's best has no recorded witness */
   int64_t fix_cycles[4];      /* fixpoint profile (thread-0 cycles): scans, degree-one, */
   int64_t fix_count[4];       /* triangle and high-degree sweeps, and their counts */
+  int64_t warp_tasks;         /* warp-tier tasks solved */
+  int64_t warp_nodes;         /* tree nodes processed by the warp tier (included in
+                                 tree_nodes_visited) */
+  int64_t warp_cycles;        /* SM cycles warps spent in warp-tier tasks */
+  int warp_limit;             /* effective warp-tier size limit (0 = tier off) */
+  int64_t warp_epoch_cycles;  /* block cycles (thread 0) in warp-tier epochs */
+  int64_t warp_task_max_cycles; /* longest single warp task, SM cycles */
+  int64_t trace[8];           /* ns after the search kernel started: last node-level
+                                 step, first warp task start, last warp task end;
+                                 then tree nodes and vertices of the longest warp task */
 } vcg_search_result;
 
 /* Run the persistent search kernel.  hist_out (nullable, capacity n+2)

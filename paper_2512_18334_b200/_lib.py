@@ -38,7 +38,7 @@ class SearchConfig_t(C.Structure):
         ("disable_pruning", C.c_int), ("deterministic", C.c_int), ("load_balance", C.c_int),
         ("workers", C.c_int), ("threads", C.c_int), ("worklist_threshold", I64),
         ("timeout", C.c_double), ("check_registry", C.c_int), ("record_cover", C.c_int),
-        ("cover_out", C.c_void_p), ("root_deg", C.c_void_p),
+        ("cover_out", C.c_void_p), ("root_deg", C.c_void_p), ("warp_limit", C.c_int),
     ]
 
 
@@ -61,6 +61,8 @@ class SearchResult_t(C.Structure):
         ("records_loaded", I64), ("records_stored", I64), ("slot_bytes", I64),
         ("phase_cycles", I64 * 10), ("cover_size", I64),
         ("fix_cycles", I64 * 4), ("fix_count", I64 * 4),
+        ("warp_tasks", I64), ("warp_nodes", I64), ("warp_cycles", I64), ("warp_limit", C.c_int),
+        ("warp_epoch_cycles", I64), ("warp_task_max_cycles", I64), ("trace", I64 * 8),
     ]
 
 

@@ -15,6 +15,7 @@
 #include "../../include/vcgpu.h"
 #include "host_algos.h"
 #include "search.cuh"
+#include "warp_solve.cuh"
 
 using namespace vcg;
 
@@ -106,7 +107,7 @@ struct DevBuf {
 };
 
 struct SearchCtx {
-  DevBuf stacks, qseq, qdata, qctl, reg, ctl, hist, gws, wbits, wcount;
+  DevBuf stacks, qseq, qdata, qctl, reg, ctl, hist, gws, wbits, wcount, bseq, bdata, bctl, sg, arena;
   // root pipeline / compaction / expansion scratch, reused across calls
   // (per-call cudaMalloc/cudaFree of tens of MB costs milliseconds, with outliers)
   DevBuf r_flag, r_ws, r_out, r_ret, c_newid, c_cnt, c_vmap, c_tmp, x_ws, x_fifo, x_out;
@@ -832,11 +833,32 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   int threads = cfg->threads;
   if (threads <= 0) threads = n <= 256 ? 64 : n <= 512 ? 128 : n <= 32768 ? 256 : 512;
   const long long wsb = ws_total<T>(n);
-  const long long smem_limit = (long long)smem_optin - 2048;
+  const long long smem_limit = (long long)smem_optin - 8192;  // static smem headroom
   const int in_smem = wsb <= smem_limit;
   const long long csrb = csr_smem_bytes(n, g->m2);
   const int csr_smem = in_smem && wsb + csrb <= smem_limit && !getenv("VCG_NO_SMEM_CSR");
-  const size_t dsmem = in_smem ? (size_t)(wsb + (csr_smem ? csrb : 0)) : 0;
+  size_t dsmem = in_smem ? (size_t)(wsb + (csr_smem ? csrb : 0)) : 0;
+  // warp tier: per-warp workspaces alias the node workspace's int scratch
+  // (ia .. par, 7 arrays; the tier runs only while the block holds no node)
+  // when that is large enough, else they follow in dynamic shared memory
+  int warp_limit = std::min(std::max(cfg->warp_limit, 0), kWMax);
+  if (cfg->deterministic || cfg->record_cover || !cfg->use_components || cfg->disable_pruning ||
+      !cfg->load_balance)
+    warp_limit = 0;
+  if (threads > 512) warp_limit = 0;
+  int bws_alias = 0;
+  long long bws_off = 0;
+  if (warp_limit) {
+    const long long need = (long long)(threads / 32) * (long long)sizeof(WarpWs);
+    const long long ni = ((long long)std::max(n, 1) + 3) & ~3LL;
+    if (in_smem && 7 * ni * 4 >= need) {
+      bws_alias = 1;
+    } else {
+      bws_off = ((long long)dsmem + 15) & ~15LL;
+      if (bws_off + need <= smem_limit) dsmem = (size_t)(bws_off + need);
+      else warp_limit = 0;
+    }
+  }
   auto kern = in_smem ? search_kernel<T, true> : search_kernel<T, false>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
   int per_sm = 0;
@@ -859,6 +881,17 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   if (qcap * slot > q_budget) qcap = std::max(4096LL, q_budget / slot);
   const int reg_cap = (int)std::min<long long>(1LL << 23, std::max<long long>(1LL << 16, (long long)n * 1024));
 
+  const long long bcap = warp_limit ? std::max<long long>(65536, 64LL * blocks) : 16;
+  // component subgraph arena: order-preserving compaction of split
+  // components (not in record-cover mode, whose witnesses use reduced ids)
+  const int compact = !cfg->record_cover && !getenv("VCG_NO_COMPACT");
+  const int sg_cap = compact ? (1 << 20) : 1;
+  const long long arena_cap = compact ? std::min<long long>(
+      (1LL << 28), std::max<long long>(1LL << 22, 64LL * ((long long)n + 1 + g->m2))) : 4;
+  if (C.sg.ensure((size_t)sg_cap * 8 + 64) || C.arena.ensure((size_t)arena_cap * 4)) return VCG_ERESOURCE;
+  if (C.bseq.ensure((size_t)bcap * 8) || C.bdata.ensure((size_t)(bcap * kWSlotBytes)) ||
+      C.bctl.ensure(64))
+    return VCG_ERESOURCE;
   if (C.stacks.ensure((size_t)(stack_cap * slot * blocks)) || C.qseq.ensure((size_t)qcap * 8) ||
       C.qdata.ensure((size_t)(qcap * slot)) || C.qctl.ensure(64) ||
       C.reg.ensure((size_t)reg_cap * (4 * 13 + 8) + 64) || C.ctl.ensure(sizeof(Ctl)) ||
@@ -929,6 +962,25 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   P.k_red = (int)cfg->k_red;
   P.root_index = 0;
   P.root_in_stack = 1;
+  P.bq.seq = C.bseq.as<unsigned long long>();
+  P.bq.head = C.bctl.as<unsigned long long>();
+  P.bq.tail = C.bctl.as<unsigned long long>() + 1;
+  P.bq.count = C.bctl.as<unsigned long long>() + 2;
+  P.bq.err = &C.ctl.as<Ctl>()->error;
+  P.bq.data = C.bdata.as<char>();
+  P.bq.cap = bcap;
+  P.warp_limit = warp_limit;
+  P.bq_low = std::max(8LL, (long long)blocks * (threads / 32) / 4);
+  P.compact = compact;
+  P.sg_n = C.sg.as<int>();
+  P.sg_base = C.sg.as<int>() + sg_cap;
+  P.sg_count = C.sg.as<int>() + 2 * sg_cap;
+  P.arena_top = C.sg.as<int>() + 2 * sg_cap + 1;
+  P.sg_cap = sg_cap;
+  P.arena = C.arena.as<int>();
+  P.arena_cap = (int)arena_cap;
+  P.bws_alias = bws_alias;
+  P.bws_off = bws_off;
 
   // root scope entry + root node record (engine.py:183-188)
   std::vector<char> rec(slot, 0);
@@ -1010,6 +1062,18 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   res->records_stored = (int64_t)ctl.rec_out;
   res->slot_bytes = slot;
   for (int i = 0; i < 10; ++i) res->phase_cycles[i] = (int64_t)ctl.phase[i];
+  res->warp_tasks = (int64_t)ctl.wtasks;
+  res->warp_nodes = (int64_t)ctl.wnodes;
+  res->warp_cycles = (int64_t)ctl.wcyc;
+  res->warp_limit = warp_limit;
+  res->warp_epoch_cycles = (int64_t)ctl.wepoch;
+  res->warp_task_max_cycles = (int64_t)ctl.wmax;
+  auto rel = [&](unsigned long long t) { return t && t != ~0ull ? (int64_t)(t - ctl.t0) : -1; };
+  res->trace[0] = rel(ctl.t_node_last);
+  res->trace[1] = rel(ctl.t_task_first);
+  res->trace[2] = rel(ctl.t_task_last);
+  res->trace[3] = (int64_t)ctl.wmax_nodes;
+  res->trace[4] = (int64_t)ctl.wmax_n;
   for (int i = 0; i < 4; ++i) {
     res->fix_cycles[i] = (int64_t)ctl.rcyc[i];
     res->fix_count[i] = (int64_t)ctl.rcnt[i];

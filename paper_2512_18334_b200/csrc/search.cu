@@ -2,6 +2,7 @@
 // block at a time.  See search.cuh for the coordination structures and
 // node_ops.cuh for the exact-semantics block-parallel node operations.
 #include "search.cuh"
+#include "warp_solve.cuh"
 
 namespace vcg {
 
@@ -14,6 +15,7 @@ struct BlockState {
   int parent;
   int child_base;
   int v;
+  int emitted;   // the node went to the warp tier
 };
 
 template <typename T>
@@ -30,6 +32,12 @@ struct Worker {
   long long payload;  // bytes of a record after its header: deg (+ inclusion bitset)
   unsigned long long ph[10];
   long long last_clk;
+  unsigned long long wep;  // thread 0: cycles in warp-tier epochs that ran tasks
+  int (*gl)[kWMax];  // per-warp local -> reduced id scratch for task packing
+  int cur_graph;     // graph of the node in the workspace (0: the reduced graph)
+  int* soff;         // shared-memory CSR region (null: the CSR is read from HBM/L2)
+  int* snbr;
+  long long extra;   // record-cover bitset bytes after the degree array
 
   __device__ void tick(int phase) {
     if (threadIdx.x == 0) {
@@ -41,13 +49,160 @@ struct Worker {
 
   __device__ Worker(const SearchParams& p, NodeWs<T> ws, BlockState* s)
       : P(p), w(ws), st(s), top(0), nodes(0), comp_branches(0), pushes(0), pops(0), rec_in(0),
-        rec_out(0), max_depth(0) {
+        rec_out(0), max_depth(0), wep(0) {
     for (int i = 0; i < 6; ++i) rules[i] = 0;
     for (int i = 0; i < 10; ++i) ph[i] = 0;
     last_clk = clock64();
-    payload = deg_bytes<T>(P.n) + (P.record ? bits_bytes(P.n) : 0);
+    extra = P.record ? bits_bytes(P.n) : 0;
+    payload = deg_bytes<T>(P.n) + extra;
+    cur_graph = 0;
+    soff = snbr = nullptr;
     lb.enabled = P.batch_live;
     my_stack = P.stacks + (long long)blockIdx.x * P.stack_cap * P.slot_bytes;
+  }
+
+  // ------------------------------------------------------- warp tasks --
+  // One warp (all lanes) packs the live vertices of the current node in
+  // [lo, hi] that belong to component `root` (root < 0: all of them) --
+  // `size` of them, <= 64 -- into a warp-tier task: local ids follow the
+  // reduced graph's order (so lowest-index tie-breaks are unchanged), rows
+  // are adjacency bitmasks.  Returns false when the task ring is full.
+  __device__ bool emit_task(int root, int size, int lo, int hi, int scope, int S, int depth,
+                            int counted) {
+    const int lane = threadIdx.x & 31;
+    int* gv = gl[threadIdx.x >> 5];
+    long long pos = -1;
+    if (lane == 0) pos = q_reserve_push(P.bq, P.bq.cap);
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    if (pos < 0) return false;
+    char* slot = P.bq.data + (pos % P.bq.cap) * kWSlotBytes;
+    int base = 0;
+    for (int c0 = lo; c0 <= hi && base < size; c0 += 32) {
+      const int v = c0 + lane;
+      const bool in = v <= hi && w.deg[v] > 0 && (root < 0 || w.par[v] == root);
+      const unsigned m = __ballot_sync(0xffffffffu, in);
+      const int li = base + __popc(m & ((1u << lane) - 1u));
+      if (in && li < kWMax) {
+        w.ia[v] = li;
+        gv[li] = v;
+      }
+      base += __popc(m);
+    }
+    __syncwarp();
+    unsigned long long* adj = (unsigned long long*)(slot + kWHdrBytes);
+    for (int i = lane; i < size; i += 32) {
+      const int v = gv[i];
+      unsigned long long mk = 0;
+      for (int k = w.off[v]; k < w.off[v + 1]; ++k) {
+        const int x = w.nbr[k];
+        if (w.deg[x] > 0) mk |= 1ull << w.ia[x];
+      }
+      __stcg(adj + i, mk);
+    }
+    if (lane == 0) {
+      __stcg((int4*)slot, make_int4(S, scope, size | (counted << 16), depth));
+      __stcg((unsigned long long*)(slot + 16), size == 64 ? ~0ull : ((1ull << size) - 1));
+    }
+    __syncwarp();
+    if (lane == 0) q_publish_push(P.bq, pos);
+    return true;
+  }
+
+  // Make `graph` (gn vertices) the workspace's graph: restage its CSR in
+  // shared memory (every subgraph is smaller than the reduced graph, so it
+  // fits the region) or point at it.  All threads, block-uniform arguments.
+  __device__ void set_graph(int graph, int gn) {
+    if (graph == cur_graph) return;
+    const int* goff = P.off;
+    const int* gnbr = P.nbr;
+    long long m2 = P.m2;
+    if (graph) {
+      goff = P.arena + __ldcg(&P.sg_base[graph - 1]);
+      gnbr = goff + ((gn + 1 + 3) & ~3);
+      m2 = __ldcg(goff + gn);
+    }
+    if (soff) {
+      for (int i = threadIdx.x; i <= gn; i += blockDim.x) soff[i] = __ldcg(goff + i);
+      for (long long i = threadIdx.x; i < m2; i += blockDim.x) snbr[i] = __ldcg(gnbr + i);
+      __syncthreads();
+    } else {
+      w.off = goff;
+      w.nbr = gnbr;
+    }
+    w.n = gn;
+    cur_graph = graph;
+    payload = deg_bytes<T>(gn) + extra;
+  }
+
+  // Order-preserving compaction of component `root` of the current node
+  // (size vertices, degree sum m2c, all in [lo, hi]) into a subgraph in the
+  // arena: local ids follow the current graph's order, so every
+  // lowest-index rule and tie-break of the reference is unchanged inside the
+  // component, while the child's degree array, window and sweeps shrink
+  // from the parent's span to the component (graph.py:112 induced_subgraph,
+  // applied per component).  Writes the local degrees to dd[0, size).
+  // Returns the subgraph's graph number (id + 1), 0 when the arena is full.
+  __device__ int compact_component(int root, int size, int m2c, int lo, int hi, T* dd) {
+    const int offw = (size + 1 + 3) & ~3;
+    if (threadIdx.x == 0) {
+      int g = -1;
+      const long long words = (long long)offw + m2c;
+      const long long b = atomicAdd(P.arena_top, (int)words);
+      if (b + words <= (long long)P.arena_cap) {
+        g = atomicAdd(P.sg_count, 1);
+        if (g >= P.sg_cap) {
+          g = -1;
+        } else {
+          P.sg_base[g] = (int)b;
+          P.sg_n[g] = size;
+        }
+      }
+      st->v = g;
+      st->child_base = (int)b;
+    }
+    __syncthreads();
+    const int g = st->v;
+    if (g < 0) return 0;
+    int* goff = P.arena + st->child_base;
+    int* gnbr = goff + offw;
+    int b, e;
+    my_chunk(lo, hi, &b, &e);
+    int cnt = 0, dsum = 0;
+    for (int v = b; v < e; ++v) {
+      const int d = w.deg[v];
+      if (d > 0 && w.par[v] == root) {
+        ++cnt;
+        dsum += d;
+      }
+    }
+    int tot;
+    int li = block_exscan(cnt, w.bs, &tot);
+    int dp = block_exscan(dsum, w.bs, &tot);
+    for (int v = b; v < e; ++v) {
+      const int d = w.deg[v];
+      if (d > 0 && w.par[v] == root) {
+        w.ia[v] = li;
+        dd[li] = (T)d;
+        __stcg(goff + li, dp);
+        ++li;
+        dp += d;
+      }
+    }
+    for (int i = size + threadIdx.x; i < (int)(deg_bytes<T>(size) / sizeof(T)); i += blockDim.x)
+      dd[i] = 0;
+    if (threadIdx.x == 0) __stcg(goff + size, m2c);
+    __syncthreads();
+    for (int v = b; v < e; ++v) {
+      if (w.deg[v] > 0 && w.par[v] == root) {
+        int k = __ldcg(goff + w.ia[v]);
+        for (int j = w.off[v]; j < w.off[v + 1]; ++j) {
+          const int x = w.nbr[j];
+          if (w.deg[x] > 0) __stcg(gnbr + k++, w.ia[x]);
+        }
+      }
+    }
+    __syncthreads();
+    return g + 1;
   }
 
   __device__ char* stack_slot(int i) const { return my_stack + (long long)i * P.slot_bytes; }
@@ -279,10 +434,23 @@ struct Worker {
     __syncthreads();
     const int parent = st->parent;
     if (parent >= 0 && P.record) record_split_witness(ncomp, agg, parent);
+    if (parent >= 0 && P.warp_limit) {
+      // small general components go to the warp tier, one warp per component
+      const int nwarps = blockDim.x >> 5;
+      for (int j = threadIdx.x >> 5; j < ncomp; j += nwarps) {
+        const int c = agg[5 * j + 2];
+        if (c < 0 || agg[5 * j] > P.warp_limit) continue;
+        if (emit_task(w.lst[j], agg[5 * j], lo, hi, c, 0, h.depth + 1, 0) &&
+            (threadIdx.x & 31) == 0)
+          agg[5 * j + 1] = -1;  // taken by the warp tier
+      }
+      __syncthreads();
+    }
     if (parent >= 0) {
       for (int j = 0; j < ncomp; ++j) {
         const int c = agg[5 * j + 2];
         if (c < 0) continue;  // special: folded into the parent sum
+        if (agg[5 * j + 1] < 0) continue;  // solved by a warp
         const int root = w.lst[j];
         const int size_deg = agg[5 * j + 1];
         const int vmax = agg[5 * j + 4];
@@ -290,23 +458,32 @@ struct Worker {
         char* dst = choose_dest(&qpos);
         if (!dst) break;
         T* dd = (T*)(dst + sizeof(NodeHdr));
-        for (int v = threadIdx.x; v < P.n; v += blockDim.x) {
-          T val = 0;
-          if (v >= lo && v <= hi && w.deg[v] > 0 && w.par[v] == root) val = w.deg[v];
-          dd[v] = val;
-        }
-        if (P.record) {  // a component child starts a fresh cover scope
-          unsigned* db = (unsigned*)(dst + sizeof(NodeHdr) + deg_bytes<T>(P.n));
-          for (int i = threadIdx.x; i < P.nw; i += blockDim.x) db[i] = 0u;
-        }
         NodeHdr ch;
+        const int g = P.compact ? compact_component(root, agg[5 * j], size_deg, lo, hi, dd) : 0;
+        if (g) {
+          ch.lo = 0;
+          ch.hi = agg[5 * j] - 1;
+          ch.graph = g;
+          ch.gn = agg[5 * j];
+        } else {
+          for (int v = threadIdx.x; v < w.n; v += blockDim.x) {
+            T val = 0;
+            if (v >= lo && v <= hi && w.deg[v] > 0 && w.par[v] == root) val = w.deg[v];
+            dd[v] = val;
+          }
+          if (P.record) {  // a component child starts a fresh cover scope
+            unsigned* db = (unsigned*)(dst + sizeof(NodeHdr) + deg_bytes<T>(P.n));
+            for (int i = threadIdx.x; i < P.nw; i += blockDim.x) db[i] = 0u;
+          }
+          ch.lo = P.use_bounds ? root : 0;
+          ch.hi = P.use_bounds ? vmax : w.n - 1;
+          ch.graph = cur_graph;
+          ch.gn = w.n;
+        }
         ch.S = 0;
         ch.E = size_deg / 2;
-        ch.lo = P.use_bounds ? root : 0;
-        ch.hi = P.use_bounds ? vmax : P.n - 1;
         ch.scope = c;
         ch.depth = h.depth + 1;
-        ch.pad0 = ch.pad1 = 0;
         commit_dest(qpos, ch, dst);
         __syncthreads();
       }
@@ -341,9 +518,9 @@ struct Worker {
     int S = h.S + fr.forced;
     int E = h.E - fr.edges;
     int lo = fr.lo, hi = fr.hi;
-    if (!P.use_bounds && P.n) {
+    if (!P.use_bounds && w.n) {
       lo = 0;
-      hi = P.n - 1;
+      hi = w.n - 1;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -375,6 +552,25 @@ struct Worker {
       __syncthreads();
       tick(PH_REGISTRY);
       return false;
+    }
+    if (P.warp_limit) {
+      // small enough for one warp: hand the whole node (and its live unit
+      // on the scope) to the warp tier, which also splits it if needed
+      int b, e, cnt = 0;
+      my_chunk(lo, hi, &b, &e);
+      for (int u = b; u < e; ++u) cnt += w.deg[u] > 0;
+      cnt = block_sum(cnt, w.bs);
+      if (cnt <= P.warp_limit) {
+        if (threadIdx.x < 32) {
+          const bool ok = emit_task(-1, cnt, lo, hi, h.scope, S, h.depth, 1);
+          if (threadIdx.x == 0) st->emitted = ok;
+        }
+        __syncthreads();
+        if (st->emitted) {
+          tick(PH_SPLIT);
+          return false;
+        }
+      }
     }
     if (P.use_components && try_split()) return false;
     tick(PH_LABEL);
@@ -445,6 +641,7 @@ struct Worker {
     atomicAdd(&c->rec_in, rec_in);
     atomicAdd(&c->rec_out, rec_out);
     for (int i = 0; i < 10; ++i) atomicAdd(&c->phase[i], ph[i]);
+    atomicAdd(&c->wepoch, wep);
     for (int i = 0; i < 4; ++i) {
       atomicAdd(&c->rcyc[i], w.bs->rcyc[i]);
       atomicAdd(&c->rcnt[i], w.bs->rcnt[i]);
@@ -460,6 +657,8 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
   extern __shared__ __align__(16) unsigned char dsmem[];
   __shared__ BlockScratch bs;
   __shared__ BlockState st;
+  __shared__ int wgl[16][kWMax];
+  __shared__ int wbusy;
   char* base = kSmem ? (char*)dsmem : P.gws + (long long)blockIdx.x * P.gws_bytes;
   NodeWs<T> ws = carve_ws<T>(base, P.n, &bs, P.off, P.nbr);
   if (kSmem && P.csr_in_smem) {
@@ -470,6 +669,12 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
     for (long long i = threadIdx.x; i < P.m2; i += blockDim.x) snbr[i] = P.nbr[i];
     ws.off = soff;
     ws.nbr = snbr;
+  }
+  int* csr_soff = nullptr;
+  int* csr_snbr = nullptr;
+  if (kSmem && P.csr_in_smem) {
+    csr_soff = const_cast<int*>(ws.off);
+    csr_snbr = const_cast<int*>(ws.nbr);
   }
   for (int i = threadIdx.x; i < P.n; i += blockDim.x) {
     ws.tmin[i] = kInf;
@@ -489,7 +694,18 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
     for (long long i = threadIdx.x; i < words; i += blockDim.x) ((unsigned*)ws.deg)[i] = 0;
   }
   __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.ctl->t0 = globaltimer();
   Worker<T> wk(P, ws, &st);
+  wk.gl = wgl;
+  wk.soff = csr_soff;
+  wk.snbr = csr_snbr;
+  WarpWs* wws = nullptr;
+  if (P.warp_limit)
+    wws = (WarpWs*)((kSmem && P.bws_alias) ? (char*)ws.ia : (char*)dsmem + P.bws_off);
+  WStats wst;
+  memset(&wst, 0, sizeof(wst));
+  if (threadIdx.x == 0) wbusy = 0;
+  st.emitted = 0;
   if (blockIdx.x == 0 && P.root_in_stack) {
     wk.top = 1;
     wk.max_depth = 1;
@@ -512,9 +728,11 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
     if (!cont) {
       if (wk.top > 0) {
         wk.top -= 1;
-        load_node(wk.stack_slot(wk.top), &st.hdr, ws.deg, wk.payload, P.reg.key, &st.best_s);
+        const int gn = load_node<T>(wk.stack_slot(wk.top), &st.hdr, ws.deg, wk.extra, P.n,
+                                    P.reg.key, &st.best_s);
         if (threadIdx.x == 0) ++wk.rec_in;
         __syncthreads();
+        wk.set_graph(st.hdr.graph, gn);
       } else {
         if (threadIdx.x == 0) {
           long long pos = q_reserve_pop(P.q);
@@ -524,18 +742,33 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
         __syncthreads();
         long long pos = ((long long)st.qpos_hi << 32) | (unsigned)st.qpos_lo;
         if (pos < 0) {
-          if (threadIdx.x == 0) {
-            wk.lb.flush(P);  // idle: release every held-back decrement
-            __nanosleep(backoff);
+          if (threadIdx.x == 0) wk.lb.flush(P);  // idle: release every held-back decrement
+          if (P.warp_limit) {
+            __syncthreads();
+            wk.tick(PH_IDLE);
+            const bool ran = warp_epoch(P, wws, &wbusy, wst);
+            if (threadIdx.x == 0) {
+              const long long now = clock64();
+              if (ran) wk.wep += (unsigned long long)(now - wk.last_clk);
+              else wk.ph[PH_IDLE] += (unsigned long long)(now - wk.last_clk);
+              wk.last_clk = now;
+            }
+            if (ran) {
+              backoff = 32;
+              continue;
+            }
           }
+          if (threadIdx.x == 0) __nanosleep(backoff);
           backoff = backoff < 4096 ? backoff * 2 : 4096;
           __syncthreads();
           wk.tick(PH_IDLE);
           continue;
         }
         backoff = 32;
-        load_node(wk.queue_slot(pos), &st.hdr, ws.deg, wk.payload, P.reg.key, &st.best_s);
+        const int gn = load_node<T>(wk.queue_slot(pos), &st.hdr, ws.deg, wk.extra, P.n,
+                                    P.reg.key, &st.best_s);
         __syncthreads();
+        wk.set_graph(st.hdr.graph, gn);
         if (threadIdx.x == 0) {
           q_release_pop(P.q, pos);
           ++wk.pops;
@@ -545,6 +778,7 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
     }
     wk.tick(PH_LOAD);
     cont = wk.process();
+    if (threadIdx.x == 0) atomicMax(&P.ctl->t_node_last, globaltimer());
   }
   // stop: release the registry slots of abandoned work (engine.py:235-243)
   if (threadIdx.x == 0) {
@@ -564,8 +798,10 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
       q_release_pop(P.q, pos);
       reg_finish(P, scope);
     }
+    warp_ring_drain(P);
   }
   wk.flush_stats();
+  warp_flush_stats(P, wst);
 }
 
 // single-thread drain of records pushed after the in-kernel drain
@@ -580,6 +816,7 @@ __global__ void drain_kernel(SearchParams P) {
     q_release_pop(P.q, pos);
     reg_finish(P, scope);
   }
+  warp_ring_drain(P);
   __threadfence();
   P.ctl->root_key = ld_relaxed(&P.reg.key[P.root_index]);
   P.ctl->reg_count = ld_relaxed(P.reg.count);
@@ -591,6 +828,7 @@ __global__ void search_init_kernel(SearchParams P, int root_key, unsigned long l
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long nth = (long long)gridDim.x * blockDim.x;
   for (long long i = tid; i < P.q.cap; i += nth) P.q.seq[i] = (unsigned long long)i;
+  for (long long i = tid; i < P.bq.cap; i += nth) P.bq.seq[i] = (unsigned long long)i;
   for (long long i = tid; i < P.n + 2; i += nth) P.hist[i] = 0ull;
   if (tid == 0) {
     const Registry& R = P.reg;
@@ -609,10 +847,16 @@ __global__ void search_init_kernel(SearchParams P, int root_key, unsigned long l
     *P.q.head = 0ull;
     *P.q.tail = 0ull;
     *P.q.count = 0ull;
+    *P.bq.head = 0ull;
+    *P.bq.tail = 0ull;
+    *P.bq.count = 0ull;
+    *P.sg_count = 0;
+    *P.arena_top = 0;
     Ctl* c = P.ctl;
     unsigned long long* cw = (unsigned long long*)c;
     for (size_t i = 0; i < sizeof(Ctl) / 8; ++i) cw[i] = 0ull;
     c->deadline_ns = timeout_ns ? globaltimer() + timeout_ns : 0ull;
+    c->t_task_first = ~0ull;
   }
 }
 

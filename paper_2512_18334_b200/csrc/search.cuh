@@ -19,9 +19,11 @@
 
 namespace vcg {
 
-// node record header, 32 bytes, followed by deg[n] (padded to 16 B)
+// node record header, 32 bytes, followed by deg[gn] (padded to 16 B).
+// graph 0: the reduced graph (gn = n); graph g + 1: compacted component
+// subgraph g (gn vertices, local ids in reduced-graph order).
 struct NodeHdr {
-  int S, E, lo, hi, scope, depth, pad0, pad1;
+  int S, E, lo, hi, scope, depth, graph, gn;
 };
 
 struct Registry {
@@ -53,6 +55,13 @@ struct Ctl {
   int root_key, reg_count;             // written by the drain kernel for readback
   unsigned long long phase[10];        // SM cycles per phase, summed over blocks (thread 0)
   unsigned long long rcyc[4], rcnt[4]; // fixpoint profile: scan, degree-one, triangle, high-degree
+  unsigned long long wtasks, wnodes, wcyc;  // warp tier: tasks, tree nodes, warp cycles in tasks
+  unsigned long long wepoch;           // block cycles (thread 0) spent in warp-tier epochs
+  unsigned long long wmax;             // longest warp task (cycles)
+  unsigned long long wmax_nodes, wmax_n;  // its tree nodes and vertex count
+  // %globaltimer trace (ns): search start, last node-level step, first warp
+  // task start, last warp task end
+  unsigned long long t0, t_node_last, t_task_first, t_task_last;
 };
 
 // phases of a block's time (clock64 deltas taken by thread 0)
@@ -98,6 +107,23 @@ struct SearchParams {
   unsigned* wbits;        // witness arena [wcap][nw]
   int* wcount;
   int wcap;
+  // warp tier (warp_solve.cuh): ring of bitmask tasks, per-warp workspaces
+  Queue bq;
+  int warp_limit;         // 0 = off
+  long long bq_low;       // a long warp task sheds work while the ring holds fewer
+  // component subgraphs (order-preserving compaction of split components):
+  // subgraph g = CSR at arena[sg_base[g]]: offsets [sg_n[g] + 1] (padded to 4),
+  // then neighbours
+  int compact;            // compact general components larger than warp_limit
+  int* sg_n;
+  int* sg_base;
+  int* sg_count;
+  int sg_cap;
+  int* arena;
+  int* arena_top;
+  int arena_cap;
+  int bws_alias;          // warp workspaces alias the node workspace's int scratch
+  long long bws_off;      // else: their offset in dynamic shared memory
 };
 
 template <typename T>
@@ -349,22 +375,29 @@ __device__ inline void reg_finish_pruned(const SearchParams& P, int scope) {
 
 // ------------------------------------------------------------ node moves --
 
-// payload = degree array (+ inclusion bitset in record-cover mode); the
-// shared-memory layout keeps them contiguous, like the record
-// The scope's best (engine.py:279 best_snapshot) is fetched by the thread
-// that loads the header's scope word, overlapped with the payload copy.
-__device__ inline void load_node(const char* src, NodeHdr* hdr, void* payload, long long bytes,
-                                 const int* keys, int* best_out) {
+// payload = degree array of the node's graph (+ inclusion bitset in
+// record-cover mode, which never compacts: extra = its bytes); the
+// shared-memory layout keeps them contiguous, like the record.  Every thread
+// reads the header's second half (one broadcast request per warp) to size
+// the copy; the scope's best (engine.py:279 best_snapshot) is fetched by
+// thread 1, overlapped with the payload copy.  Returns the graph's vertex
+// count.
+template <typename T>
+__device__ inline int load_node(const char* src, NodeHdr* hdr, void* payload, long long extra,
+                                int n_root, const int* keys, int* best_out) {
   const uint4* s = (const uint4*)src;
-  if (threadIdx.x < 2) {
-    uint4 h = __ldcg(s + threadIdx.x);
-    ((uint4*)hdr)[threadIdx.x] = h;
-    if (threadIdx.x == 1) *best_out = ld_relaxed(&keys[(int)h.x]) >> 1;  // h.x == scope
+  const uint4 h1 = __ldcg(s + 1);  // scope, depth, graph, gn
+  const int gn = h1.z ? (int)h1.w : n_root;
+  if (threadIdx.x == 0) ((uint4*)hdr)[0] = __ldcg(s);
+  if (threadIdx.x == 1) {
+    ((uint4*)hdr)[1] = h1;
+    *best_out = ld_relaxed(&keys[(int)h1.x]) >> 1;
   }
-  const long long words = bytes / 16;
+  const long long words = (deg_bytes<T>(gn) + extra) / 16;
   const uint4* sd = s + 2;
   uint4* dd = (uint4*)payload;
   for (long long i = threadIdx.x; i < words; i += blockDim.x) dd[i] = __ldcg(sd + i);
+  return gn;
 }
 
 __device__ inline void store_payload(char* dst, const void* payload, long long bytes) {

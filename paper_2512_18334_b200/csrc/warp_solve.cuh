@@ -1,0 +1,521 @@
+// Warp tier of the search: a subproblem with at most 64 live vertices is
+// solved by ONE warp as bitmask branch-and-reduce.
+//
+// Why: on the component-splitting workloads (configs[1], the RGG) the search
+// nodes hold ~13 live vertices on average while their degree-array window
+// spans ~540 vertices of the reduced graph (87% of the nodes have <= 32 live
+// vertices, 97.6% <= 64).  A whole thread block sweeping a 1 KB degree
+// record per node is the wrong granularity for them.  Here a task is the
+// induced subgraph itself -- 64 adjacency bitmasks (512 B) held in
+// registers, two rows per lane -- and a search node is a 64-bit live mask
+// plus a cover count, so a node costs a few hundred warp instructions and no
+// block barrier, HBM record or registry atomic.
+//
+// Semantics (reference engine.py:277 _process_node, kernels/pure.py rules,
+// engine.py:334 _try_component_split) are preserved as sets, not as
+// schedules: the same rules are applied to a fixpoint (in a different but
+// sound order), the same stopping rule prunes, the same max-degree vertex
+// (lowest index on ties, the task keeps the reduced graph's vertex order) is
+// branched on, include child first.  A node that splits is handled
+// component-aware inside the warp: clique / chordless-cycle components are
+// folded in closed form (reductions.py:160), the general ones are solved one
+// after another as nested frames whose bounds account for the components
+// already solved -- the sequential restatement of the registry's parent /
+// child entries, with the cover total submitted to the enclosing scope.
+// Parity: answers (cover size, PVC yes/no) equal the reference's; tree-node
+// counts differ, as in every parallel schedule.  Deterministic mode and
+// record-cover mode do not use this tier.
+#pragma once
+
+#include "search.cuh"
+
+namespace vcg {
+
+constexpr int kWMax = 64;      // vertices per warp task
+constexpr int kWStack = 72;    // DFS stack entries per warp (depth <= 64)
+constexpr int kWFrames = 24;   // nested component frames (each >= 6 vertices)
+constexpr int kWPend = 32;     // pending component masks over all frames
+
+// warp-task record: 32 B header + adjacency rows (n used of 64)
+struct WTaskHdr {
+  int S;      // cover size of the task's root within its registry scope
+  int scope;  // registry entry the task reports to (it holds one live unit)
+  int n;      // vertices | (root already counted as a tree node) << 16
+  int depth;
+  unsigned long long live;  // live vertices of the task's root node
+  unsigned long long pad;
+};
+constexpr long long kWHdrBytes = 32;
+constexpr long long kWSlotBytes = kWHdrBytes + 8 * kWMax;
+constexpr int kWExportAfter = 64;  // nodes a task runs before it may shed work
+
+struct WFrame {
+  int best;     // looking for covers of this frame's graph smaller than best
+  int ach;      // best is the size of a known cover
+  int running;  // frames > 0: cover of the enclosing node so far
+  int base;     // DFS stack height when the current component started
+  int pend_b, pend_e;  // its pending general components: pend[pend_b, pend_e)
+  int pad0, pad1;
+};
+
+struct WarpWs {
+  unsigned long long adj[kWMax];
+  unsigned long long stL[kWStack];
+  unsigned long long pend[kWPend];
+  int stS[kWStack];
+  WFrame fr[kWFrames];
+};
+
+struct WStats {
+  unsigned long long tasks, nodes, splits, cyc, maxcyc, max_nodes, max_n;
+  unsigned long long rules[6];
+};
+
+__device__ __forceinline__ unsigned long long wor64(unsigned long long x) {
+  const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)x);
+  const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(x >> 32));
+  return ((unsigned long long)hi << 32) | lo;
+}
+
+__device__ __forceinline__ unsigned long long ballot64(bool a, bool b) {
+  return (unsigned long long)__ballot_sync(0xffffffffu, a) |
+         ((unsigned long long)__ballot_sync(0xffffffffu, b) << 32);
+}
+
+// Per-lane view of the task graph: this lane owns vertices lane and lane+32.
+struct WLane {
+  unsigned long long a0, a1;  // adjacency rows of the two vertices
+  int v0, v1;
+};
+
+// Connected component of the live mask L containing r (frontier BFS, one
+// OR-reduction per level).
+__device__ __forceinline__ unsigned long long w_component(const WLane& q, unsigned long long L,
+                                                          int r) {
+  unsigned long long comp = 1ull << r, fr = comp;
+  while (fr) {
+    unsigned long long c = 0;
+    if ((fr >> q.v0) & 1) c |= q.a0;
+    if ((fr >> q.v1) & 1) c |= q.a1;
+    fr = wor64(c) & L & ~comp;
+    comp |= fr;
+  }
+  return comp;
+}
+
+// Rules to a joint fixpoint on (L, S) under the bound `best` (pure.py:188
+// reduce_fixpoint: degree-one, degree-two triangle, high degree).  Leaves d0
+// / d1 = current degrees of the lane's vertices.  Returns the edge count,
+// or -1 when S reached the bound (prune).
+__device__ __forceinline__ int w_fixpoint(const WarpWs& ws, const WLane& q, unsigned long long& L,
+                                          int& S, int best, int& d0, int& d1, WStats& st) {
+  while (true) {
+    d0 = ((L >> q.v0) & 1) ? __popcll(q.a0 & L) : 0;
+    d1 = ((L >> q.v1) & 1) ? __popcll(q.a1 & L) : 0;
+    L = ballot64(d0 > 0, d1 > 0);  // isolated vertices leave the graph
+    const int k = best - S - 1;    // vertices an improving cover may still take
+    if (k < 0) return -1;
+    // degree one (pure.py:82): the neighbour of a pendant vertex is forced;
+    // of an isolated edge only the higher end (the in-order sweep's choice)
+    const unsigned long long p1 = ballot64(d0 == 1, d1 == 1);
+    if (p1) {
+      unsigned long long c = 0;
+      if (d0 == 1) {
+        const int u = __ffsll((long long)(q.a0 & L)) - 1;
+        if (!(((p1 >> u) & 1) && u < q.v0)) c |= 1ull << u;
+      }
+      if (d1 == 1) {
+        const int u = __ffsll((long long)(q.a1 & L)) - 1;
+        if (!(((p1 >> u) & 1) && u < q.v1)) c |= 1ull << u;
+      }
+      const unsigned long long F = wor64(c);
+      L &= ~F;
+      S += __popcll(F);
+      st.rules[0] += __popcll(F);
+      continue;
+    }
+    // degree-two triangle (pure.py:113): in index order with revalidation
+    unsigned long long p2 = ballot64(d0 == 2, d1 == 2);
+    bool changed = false;
+    while (p2) {
+      const int v = __ffsll((long long)p2) - 1;
+      p2 &= p2 - 1;
+      if (!((L >> v) & 1)) continue;
+      const unsigned long long nv = ws.adj[v] & L;
+      if (__popcll(nv) != 2) continue;
+      const int a = __ffsll((long long)nv) - 1;
+      const int b = 63 - __clzll((long long)nv);
+      if ((ws.adj[a] >> b) & 1) {
+        L &= ~(nv | (1ull << v));
+        S += 2;
+        st.rules[1] += 1;
+        changed = true;
+      }
+    }
+    if (changed) continue;
+    // high degree (pure.py:158): a vertex of degree > k is in every cover
+    // that still improves the bound
+    const unsigned long long H = ballot64(d0 > k, d1 > k);
+    if (H) {
+      L &= ~H;
+      S += __popcll(H);
+      st.rules[2] += __popcll(H);
+      continue;
+    }
+    break;
+  }
+  return __reduce_add_sync(0xffffffffu, d0 + d1) >> 1;
+}
+
+// Push (adjacency of this task, live mask L) as a new task on the same
+// scope with cover offset th.S + Sl.  false: ring full.
+__device__ inline bool warp_export(const SearchParams& P, const WarpWs& ws, const WTaskHdr& th,
+                                   int n, unsigned long long L, int Sl) {
+  const int lane = threadIdx.x & 31;
+  long long pos = -1;
+  if (lane == 0) pos = q_reserve_push(P.bq, P.bq.cap);
+  pos = __shfl_sync(0xffffffffu, pos, 0);
+  if (pos < 0) return false;
+  char* slot = P.bq.data + (pos % P.bq.cap) * kWSlotBytes;
+  unsigned long long* dst = (unsigned long long*)(slot + kWHdrBytes);
+  for (int i = lane; i < n; i += 32) __stcg(dst + i, ws.adj[i]);
+  if (lane == 0) {
+    __stcg((int4*)slot, make_int4(th.S + Sl, th.scope, n, th.depth + 1));
+    __stcg((unsigned long long*)(slot + 16), L);
+    atomicAdd(&P.reg.live[th.scope], 1);  // before the task can finish it
+  }
+  __syncwarp();
+  if (lane == 0) q_publish_push(P.bq, pos);
+  return true;
+}
+
+// Solve one task to completion (or until the stop flag).  All 32 lanes run
+// it with warp-uniform state; returns false when abandoned on stop.
+__device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const WTaskHdr th,
+                                WStats& st) {
+  const int lane = threadIdx.x & 31;
+  const int n = th.n & 0xffff;
+  WLane q;
+  q.v0 = lane;
+  q.v1 = lane + 32;
+  q.a0 = q.v0 < n ? ws.adj[q.v0] : 0ull;
+  q.a1 = q.v1 < n ? ws.adj[q.v1] : 0ull;
+  bool skip_count = (th.n >> 16) & 1;
+
+  int sb = 0;
+  if (lane == 0) sb = ld_relaxed(&P.reg.key[th.scope]) >> 1;
+  sb = __shfl_sync(0xffffffffu, sb, 0);
+  ws.fr[0].best = sb - th.S;
+  ws.fr[0].ach = 0;
+  ws.fr[0].base = 0;
+  ws.fr[0].pend_b = ws.fr[0].pend_e = 0;
+  int nf = 1, sp = 0;
+  unsigned long long L = th.live;
+  int S = 0;
+  bool have = ws.fr[0].best > 0;
+  unsigned tick = 0;
+
+  while (true) {
+    if (!have) {
+      const int f = nf - 1;
+      if (sp > ws.fr[f].base) {
+        --sp;
+        L = ws.stL[sp];
+        S = ws.stS[sp];
+        have = true;
+      } else if (f == 0) {
+        break;  // task exhausted
+      } else {
+        // the current component of frame f is exhausted
+        WFrame& F = ws.fr[f];
+        if (!F.ach) {
+          --nf;  // nothing below its bound: the enclosing node cannot improve
+          continue;
+        }
+        F.running += F.best;
+        if (F.pend_e > F.pend_b) {
+          const unsigned long long c = ws.pend[--F.pend_e];
+          const int bound = ws.fr[f - 1].best - F.running - (F.pend_e - F.pend_b);
+          const int size = __popcll(c);
+          if (bound <= 0) {
+            --nf;
+            continue;
+          }
+          if (size - 1 < bound) {
+            F.best = size - 1;
+            F.ach = 1;
+          } else {
+            F.best = bound;
+            F.ach = 0;
+          }
+          F.base = sp;
+          L = c;
+          S = 0;
+          have = true;
+        } else {
+          const int total = F.running;
+          --nf;
+          WFrame& G = ws.fr[f - 1];
+          if (total < G.best) {  // leaf of the enclosing frame
+            G.best = total;
+            G.ach = 1;
+            if (f - 1 == 0 && lane == 0) reg_submit(P, th.scope, th.S + total, true, kNoWitness);
+          }
+        }
+        continue;
+      }
+    }
+    // ------------------------------------------------------------ node --
+    const int f = nf - 1;
+    if ((++tick & 15) == 0) {
+      int stop = 0, shed = 0;
+      if (lane == 0) {
+        stop = ld_relaxed(&P.ctl->stop);
+        if (!stop && P.ctl->deadline_ns && globaltimer() > P.ctl->deadline_ns) {
+          atomicExch(&P.ctl->timed_out, 1);
+          atomicExch(&P.ctl->stop, 1);
+          stop = 1;
+        }
+        if (!stop) {  // the scope may be shared (exports, MVC root): follow its bound
+          const int b = (ld_relaxed(&P.reg.key[th.scope]) >> 1) - th.S;
+          if (b < ws.fr[0].best) ws.fr[0].best = b;
+          shed = tick >= kWExportAfter &&
+                 (long long)ld_relaxed_u64(P.bq.count) < P.bq_low;
+        }
+      }
+      __syncwarp();
+      if (__shfl_sync(0xffffffffu, stop, 0)) return false;
+      // Long task and a short ring: shed the shallowest pending node of
+      // frame 0 (the largest open subtree) as a task of its own on the same
+      // scope, which takes a live unit there (engine.py:413's offload, for
+      // the warp tier).
+      const int top0 = nf > 1 ? ws.fr[1].base : sp;
+      if (__shfl_sync(0xffffffffu, shed, 0) && top0 > ws.fr[0].base) {
+        const int b = ws.fr[0].base;
+        if (warp_export(P, ws, th, n, ws.stL[b], ws.stS[b])) ws.fr[0].base = b + 1;
+      }
+    }
+    if (skip_count) skip_count = false;
+    else ++st.nodes;
+    WFrame& F = ws.fr[f];
+    int d0, d1;
+    const int E = w_fixpoint(ws, q, L, S, F.best, d0, d1, st);
+    have = false;
+    if (E < 0) continue;
+    {
+      const long long rem = (long long)F.best - S - 1;
+      if ((long long)E > rem * rem) continue;  // stopping rule (engine.py:296)
+    }
+    if (E == 0) {
+      if (S < F.best) {
+        F.best = S;
+        F.ach = 1;
+        if (f == 0 && lane == 0) reg_submit(P, th.scope, th.S + S, true, kNoWitness);
+      }
+      continue;
+    }
+    // --------------------------------------------------- components --
+    unsigned long long comp = w_component(q, L, __ffsll((long long)L) - 1);
+    if (comp != L) {
+      ++st.splits;
+      int special = 0, ng = 0, ncomp = 0;
+      // pend[] is a stack: frames <= f own everything below F.pend_e; the
+      // general components are staged at pend[pbase ..] in discovery order
+      const int pbase = F.pend_e;
+      unsigned long long rest = L;
+      bool overflow = false;
+      while (true) {
+        ++ncomp;
+        const int size = __popcll(comp);
+        const bool in0 = (comp >> q.v0) & 1, in1 = (comp >> q.v1) & 1;
+        if (!ballot64(in0 && d0 != size - 1, in1 && d1 != size - 1)) {
+          special += size - 1;  // clique: all but one vertex
+          st.rules[4] += 1;
+        } else if (size >= 3 && !ballot64(in0 && d0 != 2, in1 && d1 != 2)) {
+          special += (size + 1) / 2;  // chordless cycle
+          st.rules[5] += 1;
+        } else {
+          if (pbase + ng < kWPend) ws.pend[pbase + ng] = comp;
+          else overflow = true;
+          ++ng;
+        }
+        rest &= ~comp;
+        if (!rest) break;
+        comp = w_component(q, rest, __ffsll((long long)rest) - 1);
+      }
+      if (lane == 0) atomicAdd(&P.hist[ncomp < P.n + 1 ? ncomp : P.n + 1], 1ull);
+      const int base_S = S + special;
+      if (ng == 0) {
+        if (base_S < F.best) {
+          F.best = base_S;
+          F.ach = 1;
+          if (f == 0 && lane == 0) reg_submit(P, th.scope, th.S + base_S, true, kNoWitness);
+        }
+        continue;
+      }
+      if (base_S + ng >= F.best) continue;  // every general component needs >= 1
+      if (ng == 1) {
+        L = ws.pend[pbase];
+        S = base_S;
+        have = true;
+        continue;
+      }
+      if (overflow || nf >= kWFrames) {
+        if (lane == 0) {
+          atomicExch(&P.ctl->error, 8);
+          atomicExch(&P.ctl->stop, 1);
+        }
+        return false;
+      }
+      // new frame: solve pend[pbase] now, the rest afterwards (popped from
+      // the end, so store them reversed to keep discovery order)
+      const unsigned long long first = ws.pend[pbase];
+      for (int i = 1, j = ng - 1; i < j; ++i, --j) {
+        const unsigned long long t = ws.pend[pbase + i];
+        ws.pend[pbase + i] = ws.pend[pbase + j];
+        ws.pend[pbase + j] = t;
+      }
+      WFrame& G = ws.fr[nf++];
+      G.running = base_S;
+      G.pend_b = pbase + 1;
+      G.pend_e = pbase + ng;
+      const int bound = F.best - base_S - (ng - 1);
+      const int size = __popcll(first);
+      if (size - 1 < bound) {
+        G.best = size - 1;
+        G.ach = 1;
+      } else {
+        G.best = bound;
+        G.ach = 0;
+      }
+      G.base = sp;
+      L = first;
+      S = 0;
+      have = true;
+      continue;
+    }
+    // ------------------------------------------------------- branch --
+    // pure.py:241 select_max_degree (lowest index on ties)
+    unsigned k0 = d0 > 0 ? ((unsigned)d0 << 7) | (127u - q.v0) : 0u;
+    unsigned k1 = d1 > 0 ? ((unsigned)d1 << 7) | (127u - q.v1) : 0u;
+    const unsigned key = __reduce_max_sync(0xffffffffu, k0 > k1 ? k0 : k1);
+    const int v = 127 - (int)(key & 127u);
+    const unsigned long long nv = ws.adj[v] & L;
+    // engine.py:319: exclude child (v out, N(v) in) to the stack, include
+    // child (v in) continues here
+    const int Sx = S + __popcll(nv);
+    if (Sx < F.best) {
+      if (sp >= kWStack) {
+        if (lane == 0) {
+          atomicExch(&P.ctl->error, 8);
+          atomicExch(&P.ctl->stop, 1);
+        }
+        return false;
+      }
+      ws.stL[sp] = L & ~(nv | (1ull << v));
+      ws.stS[sp] = Sx;
+      ++sp;
+    }
+    L &= ~(1ull << v);
+    S += 1;
+    have = true;
+  }
+  return true;
+}
+
+// One warp-tier epoch of a block (all threads call it, block-uniformly).
+// Every warp takes tasks from the ring and solves them; a warp leaves once
+// the ring is empty and no warp of its block is still busy (new tasks can
+// only come from busy blocks), or as soon as node-level work is queued (the
+// block is needed there), or on stop.  Returns whether the block ran a task.
+__device__ inline bool warp_epoch(const SearchParams& P, WarpWs* wws, int* busy, WStats& st) {
+  const int lane = threadIdx.x & 31;
+  WarpWs& ws = wws[threadIdx.x >> 5];
+  bool any = false;
+  unsigned backoff = 64;
+  while (true) {
+    long long pos = -1;
+    int stop = 0, node_work = 0;
+    if (lane == 0) {
+      stop = ld_relaxed(&P.ctl->stop);
+      node_work = (long long)ld_relaxed_u64(P.q.count) > 0;
+      if (!stop && !node_work) {
+        pos = q_reserve_pop(P.bq);
+        if (pos >= 0) atomicAdd(busy, 1);
+      }
+    }
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    stop = __shfl_sync(0xffffffffu, stop, 0);
+    node_work = __shfl_sync(0xffffffffu, node_work, 0);
+    if (stop) break;
+    if (pos < 0) {
+      int b = 0;
+      if (lane == 0) b = *(volatile int*)busy;
+      b = __shfl_sync(0xffffffffu, b, 0);
+      if (node_work || b == 0) break;
+      if (lane == 0) __nanosleep(backoff);
+      backoff = backoff < 2048 ? backoff * 2 : 2048;
+      __syncwarp();
+      continue;
+    }
+    backoff = 64;
+    any = true;
+    const char* slot = P.bq.data + (pos % P.bq.cap) * kWSlotBytes;
+    const int4 h = __ldcg((const int4*)slot);
+    const WTaskHdr th{h.x, h.y, h.z, h.w, __ldcg((const unsigned long long*)(slot + 16)), 0ull};
+    const int n = th.n & 0xffff;
+    const unsigned long long* src = (const unsigned long long*)(slot + kWHdrBytes);
+    for (int i = lane; i < n; i += 32) ws.adj[i] = __ldcg(src + i);
+    __syncwarp();
+    if (lane == 0) q_release_pop(P.bq, pos);
+    const long long t0 = clock64();
+    const unsigned long long nodes0 = st.nodes;
+    if (lane == 0) atomicMin(&P.ctl->t_task_first, globaltimer());
+    warp_solve_task(P, ws, th, st);
+    __syncwarp();
+    if (lane == 0) {
+      reg_finish(P, th.scope);  // the task's live unit on its scope
+      atomicSub(busy, 1);
+    }
+    const unsigned long long dt = (unsigned long long)(clock64() - t0);
+    st.tasks += 1;
+    st.cyc += dt;
+    if (dt > st.maxcyc) {
+      st.maxcyc = dt;
+      st.max_nodes = st.nodes - nodes0;
+      st.max_n = n;
+    }
+    if (lane == 0) atomicMax(&P.ctl->t_task_last, globaltimer());
+  }
+  return __syncthreads_or(any);
+}
+
+// end of the kernel: lane 0 of every warp adds its counters
+__device__ inline void warp_flush_stats(const SearchParams& P, const WStats& st) {
+  if ((threadIdx.x & 31) != 0 || !P.warp_limit) return;
+  Ctl* c = P.ctl;
+  atomicAdd(&c->nodes, st.nodes);
+  atomicAdd(&c->comp_branches, st.splits);
+  for (int i = 0; i < 6; ++i)
+    if (st.rules[i]) atomicAdd(&c->rules[i], st.rules[i]);
+  atomicAdd(&c->wtasks, st.tasks);
+  atomicAdd(&c->wnodes, st.nodes);
+  atomicAdd(&c->wcyc, st.cyc);
+  if (atomicMax(&c->wmax, st.maxcyc) < st.maxcyc) {
+    c->wmax_nodes = st.max_nodes;
+    c->wmax_n = st.max_n;
+  }
+}
+
+// release the live units of tasks still queued after a stop
+__device__ inline void warp_ring_drain(const SearchParams& P) {
+  while (true) {
+    const long long pos = q_reserve_pop(P.bq);
+    if (pos < 0) break;
+    const int scope = __ldcg((const int*)(P.bq.data + (pos % P.bq.cap) * kWSlotBytes) + 1);
+    q_release_pop(P.bq, pos);
+    reg_finish(P, scope);
+  }
+}
+
+}  // namespace vcg

@@ -55,6 +55,10 @@ class SolverConfig:
     worklist_threshold: int | None = None
     threads: int = 0  # block size; 0 = chosen from the reduced graph size
     check_registry: bool = False
+    # warp tier: subproblems with <= warp_limit live vertices (max 64) are
+    # solved by one warp each as bitmask tasks; 0 = off.  Parallel mode only
+    # (deterministic / record_cover runs keep the reference's node schedule).
+    warp_limit: int = 64
     _disable_pruning: bool = False
 
     def validate(self) -> None:
@@ -69,6 +73,8 @@ class SolverConfig:
             raise ValueError("timeout must be positive")
         if self.worklist_threshold is not None and self.worklist_threshold < 1:
             raise ValueError("worklist threshold must be >= 1")
+        if not 0 <= self.warp_limit <= 64:
+            raise ValueError("warp_limit must be in [0, 64]")
 
 
 @dataclass
@@ -136,6 +142,8 @@ class SolveResult:
     registry: RegistrySummary | None = None
     root_index: int | None = None
     forced: list[int] = field(default_factory=list)
+    warp_tasks: int = 0     # warp-tier tasks solved
+    warp_nodes: int = 0     # tree nodes processed by the warp tier
     search_ms: float = 0.0  # device time of the search kernel
     phase_cycles: dict = field(default_factory=dict)  # block time by phase (SM cycles)
 
@@ -164,6 +172,7 @@ def run_search(rg: StaticGraph, cfg: SolverConfig, width: int, best_init: int,
     sc.worklist_threshold = int(cfg.worklist_threshold or 0)
     sc.timeout = float(cfg.timeout or 0.0)
     sc.check_registry = int(cfg.check_registry)
+    sc.warp_limit = int(cfg.warp_limit)
     cover = None
     if record:
         cover = np.zeros(max(rg.num_vertices, 1), dtype=np.int32)
@@ -271,6 +280,14 @@ def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
     stats.phase_seconds["search"] = time.perf_counter() - t1
     result.search_ms = float(res.kernel_ms)
     result.phase_cycles = dict(zip(_lib.PHASES, (int(x) for x in res.phase_cycles)))
+    result.phase_cycles["warp_task_cycles"] = int(res.warp_cycles)
+    result.phase_cycles["warp_epoch_cycles"] = int(res.warp_epoch_cycles)
+    result.phase_cycles["warp_task_max_cycles"] = int(res.warp_task_max_cycles)
+    for i, nm in enumerate(("t_node_last_ns", "t_task_first_ns", "t_task_last_ns",
+                            "warp_task_max_nodes", "warp_task_max_n")):
+        result.phase_cycles[nm] = int(res.trace[i])
+    result.warp_tasks = int(res.warp_tasks)
+    result.warp_nodes = int(res.warp_nodes)
     for i, nm in enumerate(("scan", "degree_one", "triangle", "high_degree")):
         result.phase_cycles[f"fix_{nm}_cycles"] = int(res.fix_cycles[i])
         result.phase_cycles[f"fix_{nm}_count"] = int(res.fix_count[i])

@@ -45,3 +45,13 @@ def test_product_never_imports_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text, f
                 assert "liboracle" not in text, f
+
+
+def test_warp_limit_validation():
+    import paper_2512_18334_b200 as vc
+
+    vc.SolverConfig(warp_limit=0).validate()
+    vc.SolverConfig(warp_limit=64).validate()
+    for bad in (-1, 65):
+        with pytest.raises(ValueError):
+            vc.SolverConfig(warp_limit=bad).validate()

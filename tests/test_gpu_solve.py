@@ -5,7 +5,11 @@ vcsolver itself, see tests/golden/make_golden.py).
 * deterministic mode (one block) replays the reference's single-worker
   schedule: answers AND every statistic must be identical;
 * parallel mode (every resident block): answers identical, registry
-  quiescent and conserved."""
+  quiescent and conserved.
+
+The one-block parallel configurations ("w1") replay the reference's
+single-worker statistics too, so they run with the warp tier off (the tier
+changes the schedule, not the answers: tests/test_gpu_warp_tier.py)."""
 
 from __future__ import annotations
 
@@ -17,12 +21,12 @@ pytestmark = pytest.mark.gpu
 
 _CFG = {
     "det": dict(deterministic=True),
-    "w1": dict(workers=1),
+    "w1": dict(workers=1, warp_limit=0),
     "det_nocomp": dict(deterministic=True, use_components=False),
     "det_noroot": dict(deterministic=True, use_root_reduce=False),
     "det_nobounds": dict(deterministic=True, use_bounds=False),
     "det_nocrown": dict(deterministic=True, use_crown=False),
-    "w1_nolb": dict(workers=1, load_balance=False),
+    "w1_nolb": dict(workers=1, load_balance=False, warp_limit=0),
 }
 
 
