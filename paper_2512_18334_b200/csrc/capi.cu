@@ -9,7 +9,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
+#include <thread>
+#include <unistd.h>
 #include <vector>
 
 #include "../../include/vcgpu.h"
@@ -834,7 +837,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   if (threads <= 0) threads = n <= 256 ? 64 : n <= 512 ? 128 : n <= 32768 ? 256 : 512;
   const long long wsb = ws_total<T>(n);
   const long long smem_limit = (long long)smem_optin - 8192;  // static smem headroom
-  const int in_smem = wsb <= smem_limit;
+  const int in_smem = wsb <= smem_limit && !getenv("VCG_WS_GLOBAL");
   const long long csrb = csr_smem_bytes(n, g->m2);
   const int csr_smem = in_smem && wsb + csrb <= smem_limit && !getenv("VCG_NO_SMEM_CSR");
   size_t dsmem = in_smem ? (size_t)(wsb + (csr_smem ? csrb : 0)) : 0;
@@ -1026,12 +1029,54 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
   }
+  // debug heartbeat: per-warp progress codes in host-mapped memory, dumped
+  // (and the process ended) when the search kernel overruns VCG_HEARTBEAT s
+  static int* hb_host = nullptr;
+  static long long hb_cap = 0;
+  const char* hb_env = getenv("VCG_HEARTBEAT");
+  P.hb = nullptr;
+  if (hb_env) {
+    const long long need = (long long)blocks * kMaxWarps;
+    if (need > hb_cap) {
+      if (hb_host) cudaFreeHost(hb_host);
+      CK(cudaHostAlloc((void**)&hb_host, (size_t)need * 4, cudaHostAllocMapped));
+      hb_cap = need;
+    }
+    memset(hb_host, 0, (size_t)need * 4);
+    CK(cudaHostGetDevicePointer((void**)&P.hb, hb_host, 0));
+  }
   cudaEventRecord(e0);
   COUNT_LAUNCH(2);  // search + drain
   kern<<<blocks, threads, dsmem>>>(P);
   cudaEventRecord(e1);
   cudaError_t le = cudaGetLastError();
   if (le != cudaSuccess) return fail(VCG_ECUDA, std::string("search launch: ") + cudaGetErrorString(le));
+  if (hb_env) {
+    const double lim = atof(hb_env);
+    auto t0 = std::chrono::steady_clock::now();
+    while (cudaEventQuery(e1) == cudaErrorNotReady) {
+      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > lim) {
+        std::map<std::string, int> hist;
+        const int nw = threads / 32;
+        for (int b = 0; b < blocks; ++b) {
+          std::string key;
+          for (int w = 0; w < nw; ++w) key += std::to_string(((volatile int*)hb_host)[b * kMaxWarps + w]) + " ";
+          hist[key] += 1;
+        }
+        fprintf(stderr, "[vcg heartbeat] search kernel still running after %.1f s (%d blocks x %d warps); per-warp codes -> blocks:\n", lim, blocks, nw);
+        for (auto& kv : hist) fprintf(stderr, "  %5d x [ %s]\n", kv.second, kv.first.c_str());
+        for (int b = 0; b < blocks; ++b) {
+          const volatile int* r = hb_host + (long long)b * kMaxWarps;
+          if (r[0] == 99) continue;
+          fprintf(stderr, "  block %d: d1 ncand=%d applied=%d no-live-nbr=%d | graph=%d lo=%d hi=%d gn=%d cur_graph=%d ws.n=%d\n",
+                  b, r[20], r[21], r[22], r[23], r[24], r[25], r[26], r[27], r[28]);
+        }
+        fflush(stderr);
+        _exit(3);
+      }
+      std::this_thread::sleep_for(std::chrono::milliseconds(50));
+    }
+  }
   tr.mark("search_kernel");
   drain_kernel<<<1, 32>>>(P);
   CK(cudaDeviceSynchronize());

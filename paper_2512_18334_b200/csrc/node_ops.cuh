@@ -115,7 +115,25 @@ struct BlockScratch {
   // time every warp has read it); the parity is per warp, so no cross-warp race
   int red[2][8][kMaxWarps];
   int wpar[kMaxWarps];
+  // debug heartbeat (VCG_HEARTBEAT): this block's row of per-warp codes in
+  // host-mapped memory, null when off
+  int* hb;
 };
+
+#ifdef VCG_DBG_FENCE
+#define VCG_FENCE() __threadfence()
+#else
+#define VCG_FENCE() \
+  do {              \
+  } while (0)
+#endif
+
+// lane 0 of the calling warp records `code` in the heartbeat row
+#define VCG_HB(bs, code)                                                  \
+  do {                                                                    \
+    if ((bs)->hb && (threadIdx.x & 31) == 0)                              \
+      ((volatile int*)(bs)->hb)[threadIdx.x >> 5] = (code);               \
+  } while (0)
 
 __device__ __forceinline__ void rprof(BlockScratch* bs, int i, long long* t) {
   if (threadIdx.x == 0) {
@@ -268,6 +286,7 @@ struct NodeWs {
 // every kernel that uses the block collectives calls this first
 __device__ __forceinline__ void init_block_scratch(BlockScratch* bs) {
   if (threadIdx.x < kMaxWarps) bs->wpar[threadIdx.x] = 0;
+  if (threadIdx.x == 0) bs->hb = nullptr;
   __syncthreads();
 }
 
@@ -316,6 +335,7 @@ template <typename T>
 __device__ __forceinline__ int remove_list(const NodeWs<T>& w, const int* list, int cnt) {
   int edges = 0;
   for (int k = threadIdx.x; k < cnt; k += blockDim.x) edges += remove_marked_edges(w, list[k], 1);
+  VCG_FENCE();
   edges = block_sum(edges, w.bs);  // also a barrier
   for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
     int u = list[k];
@@ -356,6 +376,7 @@ __device__ PassRet degree_one_pass(const NodeWs<T>& w, int lo, int hi, int* out,
       atomicMin(&w.tmin[u], v);
     }
   }
+  VCG_FENCE();
   __syncthreads();
   // decide, in candidate order (chunks of the candidate list)
   int cb, ce;
@@ -443,6 +464,7 @@ __device__ PassRet degree_two_triangle_pass(const NodeWs<T>& w, int lo, int hi, 
 template <typename T>
 __device__ PassRet high_degree_pass(const NodeWs<T>& w, int lo, int hi, int budget, int* out,
                                     int pos) {
+  VCG_HB(w.bs, 104);
   int b, e;
   my_chunk(lo, hi, &b, &e);
   int cnt = 0;
@@ -470,6 +492,7 @@ __device__ PassRet high_degree_pass(const NodeWs<T>& w, int lo, int hi, int budg
           int x = w.nbr[j];
           if (ldv(w.deg, x) > 0) deg_dec(w.deg, x);
         }
+        VCG_FENCE();
         __syncwarp();
         if (lane == 0) {
           w.deg[c] = 0;
@@ -634,6 +657,7 @@ __device__ int remove_vertex(const NodeWs<T>& w, int v) {
     int x = w.nbr[j];
     if (ldv(w.deg, x) > 0) deg_dec(w.deg, x);
   }
+  VCG_FENCE();
   __syncthreads();
   if (threadIdx.x == 0) {
     w.deg[v] = 0;
@@ -764,6 +788,7 @@ __device__ __forceinline__ void deg_zero(T* deg, int x) {
 // block_sum, before any later reader (every later reader is behind a barrier).
 template <typename T>
 __device__ __forceinline__ int remove_list_fast(const NodeWs<T>& w, const int* list, int cnt) {
+  VCG_HB(w.bs, 105);
   int edges = 0;
   for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
     const int u = list[k];
@@ -780,6 +805,7 @@ __device__ __forceinline__ int remove_list_fast(const NodeWs<T>& w, const int* l
     deg_zero(w.deg, u);
     mark_inc(w.inc, u);
   }
+  VCG_FENCE();
   edges = block_sum(edges, w.bs);
   for (int k = threadIdx.x; k < cnt; k += blockDim.x) w.flag[list[k]] = 0;
   return edges;
@@ -788,6 +814,7 @@ __device__ __forceinline__ int remove_list_fast(const NodeWs<T>& w, const int* l
 // degree-one sweep with the candidate count/offsets already known
 template <typename T>
 __device__ PassRet degree_one_pass_fast(const NodeWs<T>& w, int b, int e, int ncand, int* rem) {
+  VCG_HB(w.bs, 102);
   // candidates in any order: the decision below depends only on tmin
   for (int v = b; v < e; ++v) {
     if (w.deg[v] == 1) {
@@ -799,12 +826,19 @@ __device__ PassRet degree_one_pass_fast(const NodeWs<T>& w, int b, int e, int nc
           break;
         }
       }
+      if (u < 0) {  // inconsistent degree array: report instead of looping
+        if (w.bs->hb) atomicAdd(&w.bs->hb[22], 1);
+        w.bs->bc[10] = 1;
+        continue;
+      }
       w.ia[v] = u;
       w.lst[atomicAdd(&w.bs->bc[8], 1)] = v;
       atomicMin(&w.tmin[u], v);
     }
   }
+  VCG_FENCE();
   __syncthreads();
+  ncand = w.bs->bc[8];
   for (int k = threadIdx.x; k < ncand; k += blockDim.x) {
     int v = w.lst[k];
     int u = w.ia[v];
@@ -815,6 +849,10 @@ __device__ PassRet degree_one_pass_fast(const NodeWs<T>& w, int b, int e, int nc
   }
   __syncthreads();
   const int total = w.bs->bc[9];
+  if (threadIdx.x == 0 && w.bs->hb) {
+    ((volatile int*)w.bs->hb)[20] = ncand;
+    ((volatile int*)w.bs->hb)[21] = total;
+  }
   int edges = remove_list_fast(w, rem, total);
   for (int k = threadIdx.x; k < ncand; k += blockDim.x) w.tmin[w.ia[w.lst[k]]] = kInf;
   return PassRet{total, total, edges, 0};
@@ -826,6 +864,7 @@ __device__ PassRet degree_one_pass_fast(const NodeWs<T>& w, int b, int e, int nc
 // each word as it goes; removals use the one-barrier path.
 template <typename T>
 __device__ PassRet degree_two_triangle_pass_fast(const NodeWs<T>& w, int b, int e, int* rem) {
+  VCG_HB(w.bs, 103);
   unsigned* vbits = w.vbits;
   int nvalid = 0;
   for (int v = b; v < e; ++v) {
@@ -850,6 +889,7 @@ __device__ PassRet degree_two_triangle_pass_fast(const NodeWs<T>& w, int b, int 
       }
     }
   }
+  VCG_FENCE();
   nvalid = block_sum(nvalid, w.bs);
   if (nvalid == 0) return PassRet{0, 0, 0, 0};
   if (threadIdx.x == 0) {
@@ -895,6 +935,7 @@ __device__ FixRet reduce_fixpoint_fast(const NodeWs<T>& w, int lo, int hi, int b
   while (true) {
     int cycle = 0;
     while (true) {
+      VCG_HB(w.bs, 101);
       const int bud = budget - r.forced;
       int t1 = 0, t2 = 0, th = 0, mn = kInf, mx = -1, dm = 0, dv = kInf;
       for (int v = b; v < e; ++v) {
@@ -915,12 +956,18 @@ __device__ FixRet reduce_fixpoint_fast(const NodeWs<T>& w, int lo, int hi, int b
       if (threadIdx.x == 0) {  // list cursors of the sweep that follows
         w.bs->bc[8] = 0;
         w.bs->bc[9] = 0;
+        w.bs->bc[10] = 0;
       }
       st = block_scan_stats(t1, t2, th, mn, mx, dm, dv, w.bs);
       rprof(w.bs, 0, &t0);
       if (st.c1 == 0) break;
       PassRet a = degree_one_pass_fast(w, b, e, st.c1, rem);
       rprof(w.bs, 1, &t0);
+      if (((volatile int*)w.bs->bc)[10]) {  // corrupted node state: give up on it
+        r.pos = -1;
+        *maxkey = -1;
+        return r;
+      }
       r.d1 += a.applied;
       r.forced += a.forced;
       r.edges += a.edges;
@@ -963,6 +1010,7 @@ template <typename T>
 __device__ void remove_neighbors_fast(const NodeWs<T>& w, int v, int* rem, int* removed,
                                       int* edges) {
   if (threadIdx.x == 0) w.bs->bc[8] = 0;
+  VCG_HB(w.bs, 106);
   __syncthreads();
   for (int j = w.off[v] + threadIdx.x; j < w.off[v + 1]; j += blockDim.x) {
     int x = w.nbr[j];
@@ -1014,6 +1062,7 @@ __device__ __forceinline__ void uf_union(int* par, int a, int b) {
 // `inited`: par[v] == v already holds on [lo, hi] (the fixpoint's scan sets it).
 template <typename T>
 __device__ int label_components(const NodeWs<T>& w, int lo, int hi, bool inited = false) {
+  VCG_HB(w.bs, 110);
   int* par = w.par;
   if (!inited) {
     for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x) par[v] = v;
@@ -1027,7 +1076,9 @@ __device__ int label_components(const NodeWs<T>& w, int lo, int hi, bool inited 
       }
     }
   }
+  VCG_HB(w.bs, 111);
   __syncthreads();
+  VCG_HB(w.bs, 112);
   int roots = 0;
   for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x)
     if (w.deg[v] > 0 && ((volatile int*)par)[v] == v) ++roots;
@@ -1037,6 +1088,7 @@ __device__ int label_components(const NodeWs<T>& w, int lo, int hi, bool inited 
 // full path compression: par[v] = component minimum for every live v
 template <typename T>
 __device__ void compress_labels(const NodeWs<T>& w, int lo, int hi) {
+  VCG_HB(w.bs, 113);
   for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x)
     if (w.deg[v] > 0) w.par[v] = uf_find(w.par, v);
   __syncthreads();
@@ -1054,6 +1106,7 @@ struct CompInfo {
 // Aggregates are written to agg[5*ncomp] (caller-provided int scratch).
 template <typename T>
 __device__ void component_aggregates(const NodeWs<T>& w, int lo, int hi, int ncomp, int* agg) {
+  VCG_HB(w.bs, 114);
   int b, e;
   my_chunk(lo, hi, &b, &e);
   int cnt = 0;

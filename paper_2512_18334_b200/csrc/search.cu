@@ -40,6 +40,7 @@ struct Worker {
   long long extra;   // record-cover bitset bytes after the degree array
 
   __device__ void tick(int phase) {
+    VCG_HB(w.bs, phase);
     if (threadIdx.x == 0) {
       long long now = clock64();
       ph[phase] += (unsigned long long)(now - last_clk);
@@ -213,6 +214,7 @@ struct Worker {
   // engine.py:413 _offload_or_push: pick where the next child record goes.
   // Returns the destination; *qpos >= 0 means a reserved worklist slot.
   __device__ char* choose_dest(long long* qpos) {
+    VCG_HB(w.bs, 30);
     if (threadIdx.x == 0) {
       long long pos = -1;
       if (P.share) pos = q_reserve_push(P.q, P.threshold);
@@ -231,7 +233,9 @@ struct Worker {
       st->qpos_lo = (int)(pos & 0xffffffffLL);
       st->qpos_hi = (int)(pos >> 32);
     }
+    VCG_HB(w.bs, 31);
     __syncthreads();
+    VCG_HB(w.bs, 32);
     long long pos = ((long long)st->qpos_hi << 32) | (unsigned)st->qpos_lo;
     *qpos = pos;
     if (pos >= 0) return queue_slot(pos);
@@ -510,6 +514,15 @@ struct Worker {
     long long maxkey;
     FixRet fr = reduce_fixpoint_fast(w, h.lo, h.hi, budget, &maxkey);
     tick(PH_REDUCE);
+    if (fr.pos < 0) {  // inconsistent degree array (a protocol bug): fail loudly
+      if (threadIdx.x == 0) {
+        atomicExch(&P.ctl->error, 8);
+        atomicExch(&P.ctl->stop, 1);
+        lb.finish(P, h.scope, false);
+      }
+      __syncthreads();
+      return false;
+    }
     if (threadIdx.x == 0) {
       rules[0] += fr.d1;
       rules[1] += fr.d2t;
@@ -684,6 +697,7 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
   if (threadIdx.x == 0)
     for (int i = 0; i < 4; ++i) bs.rcyc[i] = bs.rcnt[i] = 0;
   init_block_scratch(&bs);
+  if (threadIdx.x == 0 && P.hb) bs.hb = P.hb + (long long)blockIdx.x * kMaxWarps;
   if (!P.record) {
     ws.inc = nullptr;
     ws.inc2 = nullptr;
@@ -713,6 +727,7 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
   bool cont = false;
   unsigned backoff = 32;
   while (true) {
+    VCG_HB(&bs, 50);
     if (threadIdx.x == 0) {
       int stop = ld_relaxed(&P.ctl->stop);
       if (!stop && P.ctl->deadline_ns && globaltimer() > P.ctl->deadline_ns) {
@@ -746,7 +761,9 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
           if (P.warp_limit) {
             __syncthreads();
             wk.tick(PH_IDLE);
+            VCG_HB(&bs, 60);
             const bool ran = warp_epoch(P, wws, &wbusy, wst);
+            VCG_HB(&bs, 61);
             if (threadIdx.x == 0) {
               const long long now = clock64();
               if (ran) wk.wep += (unsigned long long)(now - wk.last_clk);
@@ -777,10 +794,19 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
       }
     }
     wk.tick(PH_LOAD);
+    if (threadIdx.x == 0 && bs.hb) {
+      ((volatile int*)bs.hb)[23] = st.hdr.graph;
+      ((volatile int*)bs.hb)[24] = st.hdr.lo;
+      ((volatile int*)bs.hb)[25] = st.hdr.hi;
+      ((volatile int*)bs.hb)[26] = st.hdr.gn;
+      ((volatile int*)bs.hb)[27] = wk.cur_graph;
+      ((volatile int*)bs.hb)[28] = wk.w.n;
+    }
     cont = wk.process();
     if (threadIdx.x == 0) atomicMax(&P.ctl->t_node_last, globaltimer());
   }
   // stop: release the registry slots of abandoned work (engine.py:235-243)
+  VCG_HB(&bs, 70);
   if (threadIdx.x == 0) {
     wk.lb.flush(P);
     if (cont) reg_finish(P, st.hdr.scope);
@@ -802,6 +828,7 @@ __global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
   }
   wk.flush_stats();
   warp_flush_stats(P, wst);
+  VCG_HB(&bs, 99);
 }
 
 // single-thread drain of records pushed after the in-kernel drain

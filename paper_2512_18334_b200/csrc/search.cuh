@@ -124,6 +124,7 @@ struct SearchParams {
   int arena_cap;
   int bws_alias;          // warp workspaces alias the node workspace's int scratch
   long long bws_off;      // else: their offset in dynamic shared memory
+  int* hb;                // debug heartbeat rows [gridDim.x][kMaxWarps] (host-mapped), or null
 };
 
 template <typename T>
