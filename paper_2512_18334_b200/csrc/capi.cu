@@ -833,39 +833,80 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
     cached_dev = dev;
   }
 
+  const bool auto_threads = cfg->threads <= 0;
   int threads = cfg->threads;
-  if (threads <= 0) threads = n <= 256 ? 64 : n <= 512 ? 128 : n <= 32768 ? 256 : 512;
+  if (auto_threads) threads = n <= 256 ? 64 : n <= 512 ? 128 : n <= 32768 ? 256 : 512;
   const long long wsb = ws_total<T>(n);
   const long long smem_limit = (long long)smem_optin - 8192;  // static smem headroom
   const int in_smem = wsb <= smem_limit && !getenv("VCG_WS_GLOBAL");
   const long long csrb = csr_smem_bytes(n, g->m2);
-  const int csr_smem = in_smem && wsb + csrb <= smem_limit && !getenv("VCG_NO_SMEM_CSR");
-  size_t dsmem = in_smem ? (size_t)(wsb + (csr_smem ? csrb : 0)) : 0;
-  // warp tier: per-warp workspaces alias the node workspace's int scratch
-  // (ia .. par, 7 arrays; the tier runs only while the block holds no node)
-  // when that is large enough, else they follow in dynamic shared memory
-  int warp_limit = std::min(std::max(cfg->warp_limit, 0), kWMax);
+  int warp_limit0 = std::min(std::max(cfg->warp_limit, 0), kWMax);
   if (cfg->deterministic || cfg->record_cover || !cfg->use_components || cfg->disable_pruning ||
       !cfg->load_balance)
-    warp_limit = 0;
-  if (threads > 512) warp_limit = 0;
-  int bws_alias = 0;
-  long long bws_off = 0;
-  if (warp_limit) {
-    const long long need = (long long)(threads / 32) * (long long)sizeof(WarpWs);
-    const long long ni = ((long long)std::max(n, 1) + 3) & ~3LL;
-    if (in_smem && 7 * ni * 4 >= need) {
-      bws_alias = 1;
-    } else {
-      bws_off = ((long long)dsmem + 15) & ~15LL;
-      if (bws_off + need <= smem_limit) dsmem = (size_t)(bws_off + need);
-      else warp_limit = 0;
+    warp_limit0 = 0;
+  auto kern = in_smem ? search_kernel<T, true> : search_kernel<T, false>;
+  // launch plan for a block size and CSR placement: dynamic shared memory,
+  // warp-tier workspace placement and resident blocks per SM
+  struct Plan {
+    int threads, csr_smem, warp_limit, bws_alias, per_sm;
+    long long bws_off;
+    size_t dsmem;
+  };
+  auto plan = [&](int th, int csr, Plan* pl) -> int {
+    pl->threads = th;
+    pl->csr_smem = csr;
+    pl->dsmem = in_smem ? (size_t)(wsb + (csr ? csrb : 0)) : 0;
+    // warp tier: per-warp workspaces alias the node workspace's int scratch
+    // (ia .. par, 7 arrays; the tier runs only while the block holds no node)
+    // when that is large enough, else they follow in dynamic shared memory
+    pl->warp_limit = th > 512 ? 0 : warp_limit0;
+    pl->bws_alias = 0;
+    pl->bws_off = 0;
+    if (pl->warp_limit) {
+      const long long need = (long long)(th / 32) * (long long)sizeof(WarpWs);
+      const long long ni = ((long long)std::max(n, 1) + 3) & ~3LL;
+      if (in_smem && 7 * ni * 4 >= need) {
+        pl->bws_alias = 1;
+      } else {
+        pl->bws_off = ((long long)pl->dsmem + 15) & ~15LL;
+        if (pl->bws_off + need <= smem_limit) pl->dsmem = (size_t)(pl->bws_off + need);
+        else pl->warp_limit = 0;
+      }
+    }
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->dsmem));
+    pl->per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->per_sm, kern, th, pl->dsmem));
+    return 0;
+  };
+  Plan pl;
+  const int csr_fits = in_smem && wsb + csrb <= smem_limit && !getenv("VCG_NO_SMEM_CSR");
+  if (int r = plan(threads, csr_fits, &pl)) return r;
+  if (!cfg->deterministic && cfg->workers <= 0 && auto_threads) {
+    // a staged CSR that dominates the block's shared memory (dense reduced
+    // graphs, e.g. G(400, 0.1)) is dropped when that at least doubles the
+    // resident blocks: more concurrent nodes beat on-chip adjacency there
+    if (pl.csr_smem && csrb > 2 * wsb) {
+      Plan alt;
+      if (int r = plan(threads, 0, &alt)) return r;
+      if (alt.per_sm >= 2 * pl.per_sm) pl = alt;
+    }
+    // one resident block per SM (large workspaces, e.g. the 60x60 torus):
+    // use the widest block so the SM still has 16 warps in flight
+    if (pl.per_sm == 1 && pl.threads < 512) {
+      Plan alt;
+      if (int r = plan(512, pl.csr_smem, &alt)) return r;
+      if (alt.per_sm >= 1) pl = alt;
     }
   }
-  auto kern = in_smem ? search_kernel<T, true> : search_kernel<T, false>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, dsmem));
+  // the chosen plan is the kernel's final attribute setting
+  if (int r = plan(pl.threads, pl.csr_smem, &pl)) return r;
+  threads = pl.threads;
+  const int csr_smem = pl.csr_smem;
+  const int warp_limit = pl.warp_limit;
+  const int bws_alias = pl.bws_alias;
+  const long long bws_off = pl.bws_off;
+  const size_t dsmem = pl.dsmem;
+  const int per_sm = pl.per_sm;
   if (per_sm < 1) return fail(VCG_ERESOURCE, "search kernel does not fit on an SM");
   const int resident = per_sm * sm_count;
   int blocks = cfg->deterministic ? 1 : (cfg->workers > 0 ? cfg->workers : resident);

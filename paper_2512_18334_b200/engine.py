@@ -145,6 +145,8 @@ class SolveResult:
     warp_tasks: int = 0     # warp-tier tasks solved
     warp_nodes: int = 0     # tree nodes processed by the warp tier
     search_ms: float = 0.0  # device time of the search kernel
+    blocks: int = 0         # search-kernel launch: resident blocks (workers)
+    threads: int = 0        # and threads per block
     phase_cycles: dict = field(default_factory=dict)  # block time by phase (SM cycles)
 
 
@@ -279,6 +281,8 @@ def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
                                      record=cfg.record_cover)
     stats.phase_seconds["search"] = time.perf_counter() - t1
     result.search_ms = float(res.kernel_ms)
+    result.blocks = int(res.workers)
+    result.threads = int(res.threads)
     result.phase_cycles = dict(zip(_lib.PHASES, (int(x) for x in res.phase_cycles)))
     result.phase_cycles["warp_task_cycles"] = int(res.warp_cycles)
     result.phase_cycles["warp_epoch_cycles"] = int(res.warp_epoch_cycles)
