@@ -838,24 +838,26 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   if (auto_threads) threads = n <= 256 ? 64 : n <= 512 ? 128 : n <= 32768 ? 256 : 512;
   const long long wsb = ws_total<T>(n);
   const long long smem_limit = (long long)smem_optin - 8192;  // static smem headroom
-  const int in_smem = wsb <= smem_limit && !getenv("VCG_WS_GLOBAL");
+  const int smem_fits = wsb <= smem_limit && !getenv("VCG_WS_GLOBAL");
   const long long csrb = csr_smem_bytes(n, g->m2);
   int warp_limit0 = std::min(std::max(cfg->warp_limit, 0), kWMax);
   if (cfg->deterministic || cfg->record_cover || !cfg->use_components || cfg->disable_pruning ||
       !cfg->load_balance)
     warp_limit0 = 0;
-  auto kern = in_smem ? search_kernel<T, true> : search_kernel<T, false>;
-  // launch plan for a block size and CSR placement: dynamic shared memory,
+  // launch plan for a block size, workspace placement (shared memory or a
+  // per-block slice of HBM) and CSR placement: dynamic shared memory,
   // warp-tier workspace placement and resident blocks per SM
   struct Plan {
-    int threads, csr_smem, warp_limit, bws_alias, per_sm;
+    int threads, in_smem, csr_smem, warp_limit, bws_alias, per_sm;
     long long bws_off;
     size_t dsmem;
   };
-  auto plan = [&](int th, int csr, Plan* pl) -> int {
+  auto plan = [&](int th, int ws_smem, int csr, Plan* pl) -> int {
+    auto kern = ws_smem ? search_kernel<T, true> : search_kernel<T, false>;
     pl->threads = th;
-    pl->csr_smem = csr;
-    pl->dsmem = in_smem ? (size_t)(wsb + (csr ? csrb : 0)) : 0;
+    pl->in_smem = ws_smem;
+    pl->csr_smem = ws_smem && csr;
+    pl->dsmem = ws_smem ? (size_t)(wsb + (pl->csr_smem ? csrb : 0)) : 0;
     // warp tier: per-warp workspaces alias the node workspace's int scratch
     // (ia .. par, 7 arrays; the tier runs only while the block holds no node)
     // when that is large enough, else they follow in dynamic shared memory
@@ -865,7 +867,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
     if (pl->warp_limit) {
       const long long need = (long long)(th / 32) * (long long)sizeof(WarpWs);
       const long long ni = ((long long)std::max(n, 1) + 3) & ~3LL;
-      if (in_smem && 7 * ni * 4 >= need) {
+      if (ws_smem && 7 * ni * 4 >= need) {
         pl->bws_alias = 1;
       } else {
         pl->bws_off = ((long long)pl->dsmem + 15) & ~15LL;
@@ -879,27 +881,31 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
     return 0;
   };
   Plan pl;
-  const int csr_fits = in_smem && wsb + csrb <= smem_limit && !getenv("VCG_NO_SMEM_CSR");
-  if (int r = plan(threads, csr_fits, &pl)) return r;
+  const int csr_fits = smem_fits && wsb + csrb <= smem_limit && !getenv("VCG_NO_SMEM_CSR");
+  if (int r = plan(threads, smem_fits, csr_fits, &pl)) return r;
   if (!cfg->deterministic && cfg->workers <= 0 && auto_threads) {
     // a staged CSR that dominates the block's shared memory (dense reduced
     // graphs, e.g. G(400, 0.1)) is dropped when that at least doubles the
     // resident blocks: more concurrent nodes beat on-chip adjacency there
     if (pl.csr_smem && csrb > 2 * wsb) {
       Plan alt;
-      if (int r = plan(threads, 0, &alt)) return r;
+      if (int r = plan(threads, 1, 0, &alt)) return r;
       if (alt.per_sm >= 2 * pl.per_sm) pl = alt;
     }
     // one resident block per SM (large workspaces, e.g. the 60x60 torus):
-    // use the widest block so the SM still has 16 warps in flight
-    if (pl.per_sm == 1 && pl.threads < 512) {
+    // 128-thread blocks with their workspaces in HBM (L1/L2-resident) keep
+    // 8x the nodes in flight, which beats on-chip workspaces there
+    // (torus60: 5.4 vs 2.7 M nodes/s)
+    if (pl.in_smem && pl.per_sm == 1) {
       Plan alt;
-      if (int r = plan(512, pl.csr_smem, &alt)) return r;
-      if (alt.per_sm >= 1) pl = alt;
+      if (int r = plan(128, 0, 0, &alt)) return r;
+      if (alt.per_sm >= 4) pl = alt;
     }
   }
   // the chosen plan is the kernel's final attribute setting
-  if (int r = plan(pl.threads, pl.csr_smem, &pl)) return r;
+  if (int r = plan(pl.threads, pl.in_smem, pl.csr_smem, &pl)) return r;
+  auto kern = pl.in_smem ? search_kernel<T, true> : search_kernel<T, false>;
+  const int in_smem = pl.in_smem;
   threads = pl.threads;
   const int csr_smem = pl.csr_smem;
   const int warp_limit = pl.warp_limit;

@@ -1085,12 +1085,22 @@ __device__ int label_components(const NodeWs<T>& w, int lo, int hi, bool inited 
   return block_sum(roots, w.bs);
 }
 
-// full path compression: par[v] = component minimum for every live v
+// full path compression: par[v] = component minimum for every live v.
+// Two phases: finds (with path halving, which only ever shortcuts to an
+// ancestor, so every find still returns the root) into w.ia, a barrier,
+// then the writes.  Writing par[v] = root in the same phase races: a
+// concurrent find's halving store (par[x] = grandparent) can land after x's
+// owner wrote the root and leave par[x] at a non-root ancestor, mislabelling
+// x (observed as lost degrees in component children with the workspace in
+// HBM, where the window is wide).
 template <typename T>
 __device__ void compress_labels(const NodeWs<T>& w, int lo, int hi) {
   VCG_HB(w.bs, 113);
   for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x)
-    if (w.deg[v] > 0) w.par[v] = uf_find(w.par, v);
+    if (w.deg[v] > 0) w.ia[v] = uf_find(w.par, v);
+  __syncthreads();
+  for (int v = lo + threadIdx.x; v <= hi; v += blockDim.x)
+    if (w.deg[v] > 0) w.par[v] = w.ia[v];
   __syncthreads();
 }
 

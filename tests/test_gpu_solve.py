@@ -151,3 +151,42 @@ def test_record_cover_on_workloads(name):
     r = vc.solve(g, vc.SolverConfig(mode="pvc", k=exp["mvc"], record_cover=True))
     assert r.found and len(r.cover) <= exp["mvc"]
     assert_valid_cover(n, off, nbr, r.cover)
+
+
+@pytest.mark.parametrize("threads", [128, 256, 512])
+def test_hbm_workspace_split_heavy(monkeypatch, threads):
+    """Workspaces in HBM (the launch plan for large reduced graphs, forced
+    here with VCG_WS_GLOBAL) on the split-heavy rgg2000 workload with every
+    resident block: answers identical, registry quiescent.  Regression test
+    for the in-place label compression race (node_ops.cuh compress_labels),
+    which lost degrees in component children and livelocked the degree-one
+    sweep at >= 128-thread blocks."""
+    import paper_2512_18334_b200 as vc
+    from paper_2512_18334_b200 import synth
+
+    monkeypatch.setenv("VCG_WS_GLOBAL", "1")
+    exp = golden("workloads.json")["rgg2000"]
+    n, off, nbr = synth.WORKLOADS["rgg2000"]()
+    g = vc.StaticGraph(n, off, nbr)
+    for _ in range(3):
+        r = vc.solve(g, vc.SolverConfig(threads=threads, check_registry=True))
+        assert r.cover_size == exp["mvc"]
+        assert r.registry.quiescence_violations() == []
+    for k, e in exp["pvc"].items():
+        r = vc.solve(g, vc.SolverConfig(mode="pvc", k=int(k), threads=threads))
+        assert r.found == e["found"], k
+
+
+def test_torus_time_budget_consistent():
+    """torus60 (configs[4]) under a short time budget on the default launch
+    plan (128-thread blocks, HBM workspaces): stops on time with a valid
+    bound (the bipartite torus has a perfect matching: MVC = 1800)."""
+    import paper_2512_18334_b200 as vc
+    from paper_2512_18334_b200 import synth
+
+    n, off, nbr = synth.WORKLOADS["torus60"]()
+    g = vc.StaticGraph(n, off, nbr)
+    r = vc.solve(g, vc.SolverConfig(timeout=0.5))
+    assert r.cover_size >= 1800
+    assert not r.exact
+    assert r.stats.tree_nodes_visited > 0

@@ -11,5 +11,6 @@ t = time.time()
 r = vc.solve(g, vc.SolverConfig(threads=th, timeout=float(os.environ.get("BUDGET", "0.5")),
                                 workers=int(os.environ.get("WORKERS", "0")),
                                 warp_limit=int(os.environ.get("WARP", "64")),
+                                use_components=os.environ.get("COMP", "1") == "1",
                                 width=int(os.environ["WIDTH"]) if "WIDTH" in os.environ else None))
 print(name, th, r.stats.tree_nodes_visited, r.cover_size, f"{time.time()-t:.2f}s", flush=True)
