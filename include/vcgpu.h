@@ -71,12 +71,20 @@ typedef struct {
   double seconds[3];      /* device reduction, crown, compaction */
 } vcg_preprocessed;
 
+/* `enabled` flags of vcg_root_reduce: bit 0 applies the rules; with
+ * VCG_ROOT_ANY_ORDER the forced ids may come back in index order instead of
+ * forcing order (same set and rule counts), which lets the device run the
+ * fused order-free sweeps on an on-chip workspace (the solve path). */
+#define VCG_ROOT_RULES 1
+#define VCG_ROOT_ANY_ORDER 2
+
 /* Root reduction (lightweight rules on the device to a joint fixpoint with
  * the crown rule) and device compaction of the survivors.
  * has_bound: 0 = no bound (MVC: the greedy cover of g is the bound),
  * 1 = `bound` given (PVC; greedy_original is not computed, reported as -1),
  * 2 = `bound` given and greedy_original computed as well.
- * forced_out: capacity n, original ids in forcing order.
+ * forced_out: capacity n, original ids in forcing order (index order under
+ * VCG_ROOT_ANY_ORDER).
  * vertex_map_out: capacity n, reduced id -> original id.
  * reduced_out: new graph handle (the input handle itself is never aliased). */
 int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int has_bound, int64_t bound,

@@ -503,6 +503,60 @@ __global__ void k_root_fixpoint(int n, const int32_t* off, const int32_t* nbr, c
   }
 }
 
+// The same fixpoint with the order-free sweeps of the search (identical
+// forced set and rule counts, node_ops.cuh reduce_fixpoint_fast) on a
+// workspace in shared memory; the forced vertices are collected from the
+// workspace's inclusion bitset (index order).  gdeg: int32 degrees in HBM,
+// read (unless init) and written back.
+// ret: forced, d1, d2t, hd, edges, lo, hi, ids written, error
+__global__ void __launch_bounds__(1024, 1)
+    k_root_fixpoint_fast(int n, const int32_t* off, const int32_t* nbr, uint32_t* gdeg, int lo,
+                         int hi, int budget, int32_t* out, long long* ret, int init) {
+  extern __shared__ __align__(16) unsigned char rsm[];
+  __shared__ BlockScratch bs;
+  init_block_scratch(&bs);
+  NodeWs<uint32_t> w = carve_ws<uint32_t>((char*)rsm, n, &bs, off, nbr);
+  const int nwords = (n + 31) / 32;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    w.deg[i] = init ? (uint32_t)(off[i + 1] - off[i]) : gdeg[i];
+    w.tmin[i] = kInf;
+    w.flag[i] = 0;
+  }
+  for (int i = threadIdx.x; i < nwords; i += blockDim.x) {
+    w.vbits[i] = 0u;
+    w.inc[i] = 0u;
+  }
+  __syncthreads();
+  long long maxkey;
+  FixRet f = reduce_fixpoint_fast(w, lo, hi, budget, &maxkey);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) gdeg[i] = w.deg[i];
+  // forced ids in index order: contiguous word chunks, one block scan
+  int wb, we;
+  my_chunk(0, nwords - 1, &wb, &we);
+  int cnt = 0;
+  for (int i = wb; i < we; ++i) cnt += __popc(w.inc[i]);
+  int tot;
+  int at = block_exscan(cnt, w.bs, &tot);
+  for (int i = wb; i < we; ++i) {
+    unsigned m = w.inc[i];
+    while (m) {
+      out[at++] = i * 32 + __ffs(m) - 1;
+      m &= m - 1;
+    }
+  }
+  if (threadIdx.x == 0) {
+    ret[0] = f.forced;
+    ret[1] = f.d1;
+    ret[2] = f.d2t;
+    ret[3] = f.hd;
+    ret[4] = f.edges;
+    ret[5] = f.lo;
+    ret[6] = f.hi;
+    ret[7] = tot;
+    ret[8] = f.pos < 0 ? 1 : 0;
+  }
+}
+
 __global__ void k_flags_from_deg(const uint32_t* deg, int n, int32_t* flag) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -517,6 +571,7 @@ extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int h
   memset(info, 0, sizeof(*info));
   Tracer tr("root");
   const int n = (int)g->n;
+  const int rules_on = enabled & 1;
   // PVC (has_bound) never needs the greedy cover of the original graph; the
   // public root_reduce() asks for it (has_bound == 2) to mirror the reference
   info->greedy_original = has_bound == 1 ? -1
@@ -528,14 +583,14 @@ extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int h
   if (flag.ensure((size_t)(n + 1) * 4)) return VCG_ERESOURCE;
   std::vector<int64_t> vmap;
   int64_t forced_count = 0;
-  if (!enabled) {
+  if (!rules_on) {
     std::vector<int32_t> ones(n + 1, 1);
     ones[n] = 0;
     CK(cudaMemcpy(flag.p, ones.data(), (size_t)(n + 1) * 4, cudaMemcpyHostToDevice));
   } else {
     DevBuf &ws = X.r_ws, &dout = X.r_out, &dret = X.r_ret;
     if (ws.ensure(ws_total<uint32_t>(n)) || dout.ensure((size_t)(2 * n + 4) * 4) ||
-        dret.ensure(64))
+        dret.ensure(128))
       return VCG_ERESOURCE;
     NodeWs<uint32_t> layout = {};
     (void)layout;
@@ -559,16 +614,38 @@ extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int h
     int first = 1;
     int pos = 0;
     std::vector<int32_t> forced;
+    // any-order callers (the solve path) get the order-free sweeps on an
+    // on-chip workspace when it fits; the degrees then live at ws.p as int32
+    static int smem_optin = 0;
+    if (!smem_optin)
+      CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0));
+    const long long fast_smem = ws_bytes<uint32_t>(n);
+    const bool fast = (enabled & VCG_ROOT_ANY_ORDER) && fast_smem + 8192 <= smem_optin &&
+                      !getenv("VCG_ROOT_ORDERED");
+    if (fast)
+      CK(cudaFuncSetAttribute(k_root_fixpoint_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)fast_smem));
+    int crown_applied_last = 1;
     while (true) {
       int64_t progressed = 0;
       auto t0 = std::chrono::steady_clock::now();
-      long long ret[8];
+      long long ret[9];
+      // a round after a crown that applied nothing finds the fixpoint
+      // unchanged and the crown again empty: skip it (same counts)
+      if (!first && !crown_applied_last) break;
       COUNT_LAUNCH(1);
-      k_root_fixpoint<<<1, 1024>>>(n, g->d_off.as<int32_t>(), g->d_nbr.as<int32_t>(),
-                                   ws.as<char>(), lo, hi, (int)(bound0 - forced_count),
-                                   dout.as<int32_t>(), 0, dret.as<long long>(), first);
+      if (fast) {
+        k_root_fixpoint_fast<<<1, 1024, fast_smem>>>(
+            n, g->d_off.as<int32_t>(), g->d_nbr.as<int32_t>(), ws.as<uint32_t>(), lo, hi,
+            (int)(bound0 - forced_count), dout.as<int32_t>(), dret.as<long long>(), first);
+      } else {
+        k_root_fixpoint<<<1, 1024>>>(n, g->d_off.as<int32_t>(), g->d_nbr.as<int32_t>(),
+                                     ws.as<char>(), lo, hi, (int)(bound0 - forced_count),
+                                     dout.as<int32_t>(), 0, dret.as<long long>(), first);
+      }
       CK(cudaGetLastError());
-      CK(cudaMemcpy(ret, dret.p, 64, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(ret, dret.p, fast ? 72 : 64, cudaMemcpyDeviceToHost));
+      if (fast && ret[8]) return fail(VCG_ECUDA, "root fixpoint: inconsistent degree array");
       first = 0;
       if (ret[7] > 0) {
         size_t old = forced.size();
@@ -592,6 +669,7 @@ extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int h
         int64_t er = 0;
         int64_t nh = crown_reduce_host(n, g->h_off.data(), g->h_nbr.data(), hdeg.data(), lo, hi,
                                        &heads, &er);
+        crown_applied_last = nh > 0;
         if (nh > 0) {
           info->rule_counts[3] += 1;
           forced.insert(forced.end(), heads.begin(), heads.end());

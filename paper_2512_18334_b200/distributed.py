@@ -49,7 +49,8 @@ class GpuBackend:
 
         bound = cfg.k if cfg.mode == "pvc" else None
         return root_reduce(g, enabled=cfg.use_root_reduce, crown=cfg.use_crown, bound=bound,
-                           width_override=cfg.width, need_greedy_original=bound is None)
+                           width_override=cfg.width, need_greedy_original=bound is None,
+                      ordered=False)
 
     def expand(self, rg, cfg, best_init, target) -> Subtrees:
         from . import _lib

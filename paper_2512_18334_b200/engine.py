@@ -236,7 +236,8 @@ def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
     t0 = time.perf_counter()
     bound = cfg.k if cfg.mode == "pvc" else None
     pre = root_reduce(g, enabled=cfg.use_root_reduce, crown=cfg.use_crown, bound=bound,
-                      width_override=cfg.width, need_greedy_original=bound is None)
+                      width_override=cfg.width, need_greedy_original=bound is None,
+                      ordered=False)
     stats.phase_seconds["root_reduce"] = time.perf_counter() - t0
     for key, val in pre.rule_counts.items():
         stats.rule_counts[key] = stats.rule_counts.get(key, 0) + val
