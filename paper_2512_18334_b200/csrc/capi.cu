@@ -500,6 +500,7 @@ __global__ void k_root_fixpoint(int n, const int32_t* off, const int32_t* nbr, c
     ret[5] = f.lo;
     ret[6] = f.hi;
     ret[7] = f.pos;
+    ret[8] = bs.spec_m;
   }
 }
 
@@ -554,6 +555,7 @@ __global__ void __launch_bounds__(1024, 1)
     ret[6] = f.hi;
     ret[7] = tot;
     ret[8] = f.pos < 0 ? 1 : 0;
+    ret[9] = bs.spec_m;
   }
 }
 
@@ -563,20 +565,39 @@ __global__ void k_flags_from_deg(const uint32_t* deg, int n, int32_t* flag) {
     flag[i] = (i < n) ? (deg[i] > 0) : 0;
 }
 
-extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int has_bound,
-                               int64_t bound, vcg_preprocessed* info, int32_t* forced_out,
-                               int64_t* vertex_map_out, vcg_graph** reduced_out) {
-  if (int r = need_device()) return r;
-  if (!g || !info || !reduced_out) return fail(VCG_EINVAL, "bad arguments");
+static constexpr int kSpecFailed = 1000;  // internal: speculation refuted, rerun
+
+static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_bound,
+                            int64_t bound, vcg_preprocessed* info, int32_t* forced_out,
+                            int64_t* vertex_map_out, vcg_graph** reduced_out, int spec_ok) {
   memset(info, 0, sizeof(*info));
   Tracer tr("root");
   const int n = (int)g->n;
   const int rules_on = enabled & 1;
-  // PVC (has_bound) never needs the greedy cover of the original graph; the
-  // public root_reduce() asks for it (has_bound == 2) to mirror the reference
-  info->greedy_original = has_bound == 1 ? -1
-                          : greedy_cover_host(g->n, g->h_off.data(), g->h_nbr.data(), nullptr);
-  const int64_t bound0 = has_bound ? bound : info->greedy_original;
+  // PVC (has_bound == 1) never needs the greedy cover of the original graph;
+  // the public root_reduce() asks for it (has_bound == 2) to mirror the
+  // reference.  It runs on a host thread, overlapped with the device rules:
+  // for MVC (has_bound == 0) it is also the rules' bound, so the rules run
+  // with a speculative budget under which the high-degree rule cannot fire,
+  // recording per round the largest (live degree + forced so far); once the
+  // greedy value is known the host checks that the real budget would not
+  // have fired it either (else the pipeline reruns with the real bound).
+  int64_t greedy_orig = -1;
+  std::thread greedy_thr;
+  if (has_bound != 1)
+    greedy_thr = std::thread([&]() {
+      greedy_orig = greedy_cover_host(g->n, g->h_off.data(), g->h_nbr.data(), nullptr);
+    });
+  struct JoinGuard {
+    std::thread& t;
+    ~JoinGuard() {
+      if (t.joinable()) t.join();
+    }
+  } join_guard{greedy_thr};
+  const bool spec = spec_ok && has_bound == 0 && rules_on && !getenv("VCG_NO_SPEC");
+  if (has_bound == 0 && !spec) greedy_thr.join();
+  const int64_t bound0 = has_bound ? bound : greedy_orig;  // unused while speculating
+  std::vector<std::pair<int64_t, int64_t>> spec_rounds;   // (spec_m, forced before the round)
   tr.mark("greedy_original");
   SearchCtx& X = search_ctx();
   DevBuf& flag = X.r_flag;
@@ -629,23 +650,25 @@ extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int h
     while (true) {
       int64_t progressed = 0;
       auto t0 = std::chrono::steady_clock::now();
-      long long ret[9];
+      long long ret[10];
       // a round after a crown that applied nothing finds the fixpoint
       // unchanged and the crown again empty: skip it (same counts)
       if (!first && !crown_applied_last) break;
       COUNT_LAUNCH(1);
+      const int budget = spec ? kSpecBudget : (int)(bound0 - forced_count);
       if (fast) {
         k_root_fixpoint_fast<<<1, 1024, fast_smem>>>(
             n, g->d_off.as<int32_t>(), g->d_nbr.as<int32_t>(), ws.as<uint32_t>(), lo, hi,
-            (int)(bound0 - forced_count), dout.as<int32_t>(), dret.as<long long>(), first);
+            budget, dout.as<int32_t>(), dret.as<long long>(), first);
       } else {
         k_root_fixpoint<<<1, 1024>>>(n, g->d_off.as<int32_t>(), g->d_nbr.as<int32_t>(),
-                                     ws.as<char>(), lo, hi, (int)(bound0 - forced_count),
+                                     ws.as<char>(), lo, hi, budget,
                                      dout.as<int32_t>(), 0, dret.as<long long>(), first);
       }
       CK(cudaGetLastError());
-      CK(cudaMemcpy(ret, dret.p, fast ? 72 : 64, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(ret, dret.p, 80, cudaMemcpyDeviceToHost));
       if (fast && ret[8]) return fail(VCG_ECUDA, "root fixpoint: inconsistent degree array");
+      if (spec) spec_rounds.emplace_back(fast ? ret[9] : ret[8], forced_count);
       first = 0;
       if (ret[7] > 0) {
         size_t old = forced.size();
@@ -716,10 +739,31 @@ extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int h
   tr.mark("compaction");
   info->greedy_reduced = greedy_cover_host(red->n, red->h_off.data(), red->h_nbr.data(), nullptr);
   tr.mark("greedy_reduced");
+  if (greedy_thr.joinable()) greedy_thr.join();
+  tr.mark("greedy_original joined");
+  info->greedy_original = greedy_orig;
+  for (const auto& sr : spec_rounds)
+    if (sr.first > greedy_orig - sr.second) {  // the real budget would have fired
+      vcg_graph_destroy(red);
+      return kSpecFailed;
+    }
   if (vertex_map_out)
     for (size_t i = 0; i < vmap.size(); ++i) vertex_map_out[i] = vmap[i];
   *reduced_out = red;
   return 0;
+}
+
+extern "C" int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int has_bound,
+                               int64_t bound, vcg_preprocessed* info, int32_t* forced_out,
+                               int64_t* vertex_map_out, vcg_graph** reduced_out) {
+  if (int r = need_device()) return r;
+  if (!g || !info || !reduced_out) return fail(VCG_EINVAL, "bad arguments");
+  int r = root_reduce_impl(g, enabled, crown, has_bound, bound, info, forced_out, vertex_map_out,
+                           reduced_out, 1);
+  if (r == kSpecFailed)
+    r = root_reduce_impl(g, enabled, crown, has_bound, bound, info, forced_out, vertex_map_out,
+                         reduced_out, 0);
+  return r;
 }
 
 // -------------------------------------------------------------- expansion --
@@ -1099,6 +1143,12 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   P.bq.cap = bcap;
   P.warp_limit = warp_limit;
   P.bq_low = std::max(8LL, (long long)blocks * (threads / 32) / 4);
+  {
+    const char* e1 = getenv("VCG_WCHECK");
+    const char* e2 = getenv("VCG_WEXPORT");
+    P.w_check_mask = e1 ? atoi(e1) : 3;
+    P.w_export_after = e2 ? atoi(e2) : 4;
+  }
   P.compact = compact;
   P.sg_n = C.sg.as<int>();
   P.sg_base = C.sg.as<int>() + sg_cap;
@@ -1244,6 +1294,9 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   res->trace[2] = rel(ctl.t_task_last);
   res->trace[3] = (int64_t)ctl.wmax_nodes;
   res->trace[4] = (int64_t)ctl.wmax_n;
+  res->trace[5] = (int64_t)ctl.wc_fix;
+  res->trace[6] = (int64_t)ctl.wc_comp;
+  res->trace[7] = (int64_t)ctl.wc_split;
   for (int i = 0; i < 4; ++i) {
     res->fix_cycles[i] = (int64_t)ctl.rcyc[i];
     res->fix_count[i] = (int64_t)ctl.rcnt[i];

@@ -6,7 +6,8 @@
 #include "host_algos.h"
 
 #include <algorithm>
-#include <queue>
+#include <climits>
+#include <cstdint>
 #include <vector>
 
 namespace vcg {
@@ -14,111 +15,64 @@ namespace vcg {
 // preprocess.py:348 greedy_bound -> pure.py:306 greedy_cover: repeatedly take
 // the lowest-index vertex of maximum residual degree.
 //
-// Degree buckets as three-level bitsets (64-bit words, a summary bit per
-// word, a summary bit per summary word): the pick is "highest non-empty bucket, lowest set bit", a vertex
-// moves one bucket down per removed neighbour.  O(m + picks * n/2^18) time;
-// falls back to a lazy max-heap when buckets x n bits would exceed 256 MiB.
-namespace {
-
-struct Buckets {
-  // per degree bucket: L0 vertex bits, L1 = non-empty L0 words, L2 = non-empty L1 words
-  int64_t w0, w1, w2;
-  std::vector<uint64_t> b0, b1, b2;
-  std::vector<int64_t> count;
-  Buckets(int64_t n, int64_t maxdeg)
-      : w0((n + 63) / 64), w1((w0 + 63) / 64), w2((w1 + 63) / 64),
-        b0((size_t)(maxdeg + 1) * w0, 0), b1((size_t)(maxdeg + 1) * w1, 0),
-        b2((size_t)(maxdeg + 1) * w2, 0), count(maxdeg + 1, 0) {}
-  void set(int64_t d, int64_t v) {
-    const int64_t i0 = v >> 6, i1 = i0 >> 6;
-    uint64_t& a = b0[(size_t)d * w0 + i0];
-    if (!a) {
-      uint64_t& b = b1[(size_t)d * w1 + i1];
-      if (!b) b2[(size_t)d * w2 + (i1 >> 6)] |= 1ull << (i1 & 63);
-      b |= 1ull << (i0 & 63);
-    }
-    a |= 1ull << (v & 63);
-    ++count[d];
-  }
-  void clear(int64_t d, int64_t v) {
-    const int64_t i0 = v >> 6, i1 = i0 >> 6;
-    uint64_t& a = b0[(size_t)d * w0 + i0];
-    a &= ~(1ull << (v & 63));
-    if (!a) {
-      uint64_t& b = b1[(size_t)d * w1 + i1];
-      b &= ~(1ull << (i0 & 63));
-      if (!b) b2[(size_t)d * w2 + (i1 >> 6)] &= ~(1ull << (i1 & 63));
-    }
-    --count[d];
-  }
-  int64_t lowest(int64_t d) const {
-    const uint64_t* l2 = &b2[(size_t)d * w2];
-    for (int64_t i = 0; i < w2; ++i)
-      if (l2[i]) {
-        const int64_t i1 = i * 64 + __builtin_ctzll(l2[i]);
-        const int64_t i0 = i1 * 64 + __builtin_ctzll(b1[(size_t)d * w1 + i1]);
-        return i0 * 64 + __builtin_ctzll(b0[(size_t)d * w0 + i0]);
-      }
-    return -1;
-  }
-};
-
-}  // namespace
-
+// Level form of the same pick sequence: with D the current maximum degree,
+// degrees only fall, so the picks at level D are exactly the vertices of
+// degree D visited in ascending index order that still have degree D when
+// visited (a pick demotes its degree-D neighbours, nothing enters level D).
+// Each level's candidates come from an append-only list (a vertex enters
+// list[d] once, when its degree reaches d) and are visited through a
+// bitmap over their index span.  O(n + m + sum over levels of span/64)
+// time, sequential memory traffic apart from the degree updates.
 int64_t greedy_cover_host(int64_t n, const int64_t* off, const int32_t* nbr, int32_t* members) {
   if (n <= 0) return 0;
-  std::vector<uint32_t> deg(n);
+  std::vector<int32_t> deg(n);
   int64_t m2 = 0, maxdeg = 0;
   for (int64_t v = 0; v < n; ++v) {
-    deg[v] = (uint32_t)(off[v + 1] - off[v]);
+    deg[v] = (int32_t)(off[v + 1] - off[v]);
     m2 += deg[v];
     maxdeg = std::max<int64_t>(maxdeg, deg[v]);
   }
   if (m2 == 0) return 0;
-  int64_t size = 0;
-  if ((maxdeg + 1) * ((n + 63) / 64) * 8 <= (256LL << 20)) {
-    Buckets b(n, maxdeg);
+  std::vector<std::vector<int32_t>> level(maxdeg + 1);
+  {
+    std::vector<int64_t> cnt(maxdeg + 1, 0);
+    for (int64_t v = 0; v < n; ++v) ++cnt[deg[v]];
+    for (int64_t d = 1; d <= maxdeg; ++d) level[d].reserve((size_t)cnt[d]);
     for (int64_t v = 0; v < n; ++v)
-      if (deg[v]) b.set(deg[v], v);
-    int64_t top = maxdeg;
-    while (true) {
-      while (top > 0 && b.count[top] == 0) --top;
-      if (top == 0) break;
-      const int64_t v = b.lowest(top);
-      b.clear(top, v);
-      for (int64_t i = off[v]; i < off[v + 1]; ++i) {
-        const int32_t u = nbr[i];
-        if (deg[u] > 0) {
-          b.clear(deg[u], u);
-          --deg[u];
-          if (deg[u]) b.set(deg[u], u);
-        }
-      }
-      deg[v] = 0;
-      if (members) members[size] = (int32_t)v;
-      ++size;
-    }
-    return size;
+      if (deg[v]) level[deg[v]].push_back((int32_t)v);
   }
-  using Key = std::pair<uint32_t, int64_t>;  // (degree, -index)
-  std::priority_queue<Key> heap;
-  for (int64_t v = 0; v < n; ++v)
-    if (deg[v]) heap.push(Key(deg[v], -v));
-  while (!heap.empty()) {
-    Key k = heap.top();
-    heap.pop();
-    int64_t v = -k.second;
-    if (deg[v] == 0 || deg[v] != k.first) continue;
-    for (int64_t i = off[v]; i < off[v + 1]; ++i) {
-      int32_t u = nbr[i];
-      if (deg[u] > 0) {
-        --deg[u];
-        if (deg[u]) heap.push(Key(deg[u], -(int64_t)u));
+  std::vector<uint64_t> mark((size_t)((n + 63) / 64), 0);
+  int64_t size = 0;
+  for (int64_t d = maxdeg; d >= 1; --d) {
+    std::vector<int32_t>& cand = level[d];
+    if (cand.empty()) continue;
+    int64_t wlo = INT64_MAX, whi = -1;
+    for (int32_t v : cand)
+      if (deg[v] == d) {
+        mark[v >> 6] |= 1ull << (v & 63);
+        wlo = std::min<int64_t>(wlo, v >> 6);
+        whi = std::max<int64_t>(whi, v >> 6);
+      }
+    std::vector<int32_t>().swap(cand);
+    for (int64_t w = wlo; w <= whi; ++w) {
+      uint64_t bits = mark[w];
+      mark[w] = 0;
+      while (bits) {
+        const int64_t v = w * 64 + __builtin_ctzll(bits);
+        bits &= bits - 1;
+        if (deg[v] != d) continue;  // demoted by an earlier pick of this level
+        for (int64_t i = off[v]; i < off[v + 1]; ++i) {
+          const int32_t u = nbr[i];
+          if (deg[u] > 0) {
+            const int32_t du = --deg[u];
+            if (du) level[du].push_back(u);
+          }
+        }
+        deg[v] = 0;
+        if (members) members[size] = (int32_t)v;
+        ++size;
       }
     }
-    deg[v] = 0;
-    if (members) members[size] = (int32_t)v;
-    ++size;
   }
   return size;
 }

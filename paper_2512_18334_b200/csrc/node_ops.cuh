@@ -35,6 +35,12 @@
 namespace vcg {
 
 constexpr int kInf = 0x7fffffff;
+// Speculative root budget: the root rules run with this budget while the
+// host computes the greedy bound; the high-degree rule cannot fire, and the
+// sweeps record in BlockScratch::spec_m the largest (max live degree +
+// vertices forced so far) they saw, so the host can verify afterwards that
+// the real budget would not have fired it either (capi.cu vcg_root_reduce).
+constexpr int kSpecBudget = 1 << 30;
 constexpr int kMaxWarps = 32;
 
 // ---------------------------------------------------------------------------
@@ -118,6 +124,7 @@ struct BlockScratch {
   // debug heartbeat (VCG_HEARTBEAT): this block's row of per-warp codes in
   // host-mapped memory, null when off
   int* hb;
+  int spec_m;  // speculative root budget: max(live degree + forced so far)
 };
 
 #ifdef VCG_DBG_FENCE
@@ -286,7 +293,10 @@ struct NodeWs {
 // every kernel that uses the block collectives calls this first
 __device__ __forceinline__ void init_block_scratch(BlockScratch* bs) {
   if (threadIdx.x < kMaxWarps) bs->wpar[threadIdx.x] = 0;
-  if (threadIdx.x == 0) bs->hb = nullptr;
+  if (threadIdx.x == 0) {
+    bs->hb = nullptr;
+    bs->spec_m = -1;
+  }
   __syncthreads();
 }
 
@@ -467,10 +477,16 @@ __device__ PassRet high_degree_pass(const NodeWs<T>& w, int lo, int hi, int budg
   VCG_HB(w.bs, 104);
   int b, e;
   my_chunk(lo, hi, &b, &e);
-  int cnt = 0;
+  int cnt = 0, dmax = 0;
   for (int v = b; v < e; ++v) {
     int d = w.deg[v];
     cnt += (d > 0 && d > budget);
+    dmax = d > dmax ? d : dmax;
+  }
+  if (budget > kSpecBudget / 2) {  // speculative: forced so far = kSpecBudget - budget
+    dmax = block_max(dmax, w.bs);
+    if (threadIdx.x == 0 && dmax + (kSpecBudget - budget) > w.bs->spec_m)
+      w.bs->spec_m = dmax + (kSpecBudget - budget);
   }
   int ncand;
   int at = block_exscan(cnt, w.bs, &ncand);
@@ -960,6 +976,10 @@ __device__ FixRet reduce_fixpoint_fast(const NodeWs<T>& w, int lo, int hi, int b
       }
       st = block_scan_stats(t1, t2, th, mn, mx, dm, dv, w.bs);
       rprof(w.bs, 0, &t0);
+      if (bud > kSpecBudget / 2 && threadIdx.x == 0 && st.key >= 0) {
+        const int m = (int)(st.key >> 32) + (kSpecBudget - bud);
+        if (m > w.bs->spec_m) w.bs->spec_m = m;
+      }
       if (st.c1 == 0) break;
       PassRet a = degree_one_pass_fast(w, b, e, st.c1, rem);
       rprof(w.bs, 1, &t0);

@@ -62,6 +62,7 @@ struct Ctl {
   // %globaltimer trace (ns): search start, last node-level step, first warp
   // task start, last warp task end
   unsigned long long t0, t_node_last, t_task_first, t_task_last;
+  unsigned long long wc_fix, wc_comp, wc_split;  // warp-task cycles: fixpoint, component test, splits
 };
 
 // phases of a block's time (clock64 deltas taken by thread 0)
@@ -111,6 +112,8 @@ struct SearchParams {
   Queue bq;
   int warp_limit;         // 0 = off
   long long bq_low;       // a long warp task sheds work while the ring holds fewer
+  int w_check_mask;       // a warp task polls stop / bound / ring every (mask + 1) nodes
+  int w_export_after;     // and may shed work once it has run this many nodes
   // component subgraphs (order-preserving compaction of split components):
   // subgraph g = CSR at arena[sg_base[g]]: offsets [sg_n[g] + 1] (padded to 4),
   // then neighbours

@@ -47,7 +47,8 @@ struct WTaskHdr {
 };
 constexpr long long kWHdrBytes = 32;
 constexpr long long kWSlotBytes = kWHdrBytes + 8 * kWMax;
-constexpr int kWExportAfter = 64;  // nodes a task runs before it may shed work
+// a task polls every 4 nodes and may shed work after 4 (capi.cu; VCG_WCHECK /
+// VCG_WEXPORT override): on rgg2000 PVC(opt-1) 1.40 -> 1.28 ms vs every 16 / after 64
 
 struct WFrame {
   int best;     // looking for covers of this frame's graph smaller than best
@@ -68,6 +69,7 @@ struct WarpWs {
 
 struct WStats {
   unsigned long long tasks, nodes, splits, cyc, maxcyc, max_nodes, max_n;
+  unsigned long long c_fix, c_comp, c_split;  // cycles in the node phases
   unsigned long long rules[6];
 };
 
@@ -267,7 +269,7 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
     }
     // ------------------------------------------------------------ node --
     const int f = nf - 1;
-    if ((++tick & 15) == 0) {
+    if ((++tick & (unsigned)P.w_check_mask) == 0) {
       int stop = 0, shed = 0;
       if (lane == 0) {
         stop = ld_relaxed(&P.ctl->stop);
@@ -279,7 +281,7 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
         if (!stop) {  // the scope may be shared (exports, MVC root): follow its bound
           const int b = (ld_relaxed(&P.reg.key[th.scope]) >> 1) - th.S;
           if (b < ws.fr[0].best) ws.fr[0].best = b;
-          shed = tick >= kWExportAfter &&
+          shed = tick >= (unsigned)P.w_export_after &&
                  (long long)ld_relaxed_u64(P.bq.count) < P.bq_low;
         }
       }
@@ -299,7 +301,10 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
     else ++st.nodes;
     WFrame& F = ws.fr[f];
     int d0, d1;
+    long long c0 = clock64();
     const int E = w_fixpoint(ws, q, L, S, F.best, d0, d1, st);
+    long long c1 = clock64();
+    st.c_fix += (unsigned long long)(c1 - c0);
     have = false;
     if (E < 0) continue;
     {
@@ -316,6 +321,8 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
     }
     // --------------------------------------------------- components --
     unsigned long long comp = w_component(q, L, __ffsll((long long)L) - 1);
+    c0 = clock64();
+    st.c_comp += (unsigned long long)(c0 - c1);
     if (comp != L) {
       ++st.splits;
       int special = 0, ng = 0, ncomp = 0;
@@ -344,6 +351,7 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
         comp = w_component(q, rest, __ffsll((long long)rest) - 1);
       }
       if (lane == 0) atomicAdd(&P.hist[ncomp < P.n + 1 ? ncomp : P.n + 1], 1ull);
+      st.c_split += (unsigned long long)(clock64() - c0);
       const int base_S = S + special;
       if (ng == 0) {
         if (base_S < F.best) {
@@ -501,6 +509,9 @@ __device__ inline void warp_flush_stats(const SearchParams& P, const WStats& st)
   atomicAdd(&c->wtasks, st.tasks);
   atomicAdd(&c->wnodes, st.nodes);
   atomicAdd(&c->wcyc, st.cyc);
+  atomicAdd(&c->wc_fix, st.c_fix);
+  atomicAdd(&c->wc_comp, st.c_comp);
+  atomicAdd(&c->wc_split, st.c_split);
   if (atomicMax(&c->wmax, st.maxcyc) < st.maxcyc) {
     c->wmax_nodes = st.max_nodes;
     c->wmax_n = st.max_n;

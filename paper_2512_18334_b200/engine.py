@@ -289,7 +289,8 @@ def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
     result.phase_cycles["warp_epoch_cycles"] = int(res.warp_epoch_cycles)
     result.phase_cycles["warp_task_max_cycles"] = int(res.warp_task_max_cycles)
     for i, nm in enumerate(("t_node_last_ns", "t_task_first_ns", "t_task_last_ns",
-                            "warp_task_max_nodes", "warp_task_max_n")):
+                            "warp_task_max_nodes", "warp_task_max_n", "warp_fix_cycles",
+                            "warp_comp_cycles", "warp_split_cycles")):
         result.phase_cycles[nm] = int(res.trace[i])
     result.warp_tasks = int(res.warp_tasks)
     result.warp_nodes = int(res.warp_nodes)
