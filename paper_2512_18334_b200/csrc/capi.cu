@@ -647,6 +647,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
       CK(cudaFuncSetAttribute(k_root_fixpoint_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)fast_smem));
     int crown_applied_last = 1;
+    static const int root_threads = getenv("VCG_ROOT_THREADS") ? atoi(getenv("VCG_ROOT_THREADS")) : 1024;
     while (true) {
       int64_t progressed = 0;
       auto t0 = std::chrono::steady_clock::now();
@@ -657,7 +658,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
       COUNT_LAUNCH(1);
       const int budget = spec ? kSpecBudget : (int)(bound0 - forced_count);
       if (fast) {
-        k_root_fixpoint_fast<<<1, 1024, fast_smem>>>(
+        k_root_fixpoint_fast<<<1, root_threads, fast_smem>>>(
             n, g->d_off.as<int32_t>(), g->d_nbr.as<int32_t>(), ws.as<uint32_t>(), lo, hi,
             budget, dout.as<int32_t>(), dret.as<long long>(), first);
       } else {
@@ -1297,6 +1298,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   res->trace[5] = (int64_t)ctl.wc_fix;
   res->trace[6] = (int64_t)ctl.wc_comp;
   res->trace[7] = (int64_t)ctl.wc_split;
+
   for (int i = 0; i < 4; ++i) {
     res->fix_cycles[i] = (int64_t)ctl.rcyc[i];
     res->fix_count[i] = (int64_t)ctl.rcnt[i];

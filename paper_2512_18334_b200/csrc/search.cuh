@@ -63,6 +63,7 @@ struct Ctl {
   // task start, last warp task end
   unsigned long long t0, t_node_last, t_task_first, t_task_last;
   unsigned long long wc_fix, wc_comp, wc_split;  // warp-task cycles: fixpoint, component test, splits
+  unsigned long long wc_iter;                    // warp fixpoint loop iterations
 };
 
 // phases of a block's time (clock64 deltas taken by thread 0)

@@ -70,6 +70,7 @@ struct WarpWs {
 struct WStats {
   unsigned long long tasks, nodes, splits, cyc, maxcyc, max_nodes, max_n;
   unsigned long long c_fix, c_comp, c_split;  // cycles in the node phases
+  unsigned long long c_iter;                   // fixpoint loop iterations
   unsigned long long rules[6];
 };
 
@@ -112,6 +113,7 @@ __device__ __forceinline__ unsigned long long w_component(const WLane& q, unsign
 __device__ __forceinline__ int w_fixpoint(const WarpWs& ws, const WLane& q, unsigned long long& L,
                                           int& S, int best, int& d0, int& d1, WStats& st) {
   while (true) {
+    ++st.c_iter;
     d0 = ((L >> q.v0) & 1) ? __popcll(q.a0 & L) : 0;
     d1 = ((L >> q.v1) & 1) ? __popcll(q.a1 & L) : 0;
     L = ballot64(d0 > 0, d1 > 0);  // isolated vertices leave the graph
@@ -136,25 +138,58 @@ __device__ __forceinline__ int w_fixpoint(const WarpWs& ws, const WLane& q, unsi
       st.rules[0] += __popcll(F);
       continue;
     }
-    // degree-two triangle (pure.py:113): in index order with revalidation
-    unsigned long long p2 = ballot64(d0 == 2, d1 == 2);
-    bool changed = false;
-    while (p2) {
-      const int v = __ffsll((long long)p2) - 1;
-      p2 &= p2 - 1;
-      if (!((L >> v) & 1)) continue;
-      const unsigned long long nv = ws.adj[v] & L;
-      if (__popcll(nv) != 2) continue;
-      const int a = __ffsll((long long)nv) - 1;
-      const int b = 63 - __clzll((long long)nv);
-      if ((ws.adj[a] >> b) & 1) {
-        L &= ~(nv | (1ull << v));
-        S += 2;
-        st.rules[1] += 1;
-        changed = true;
+    // degree-two triangle (pure.py:113): in index order with revalidation.
+    // Validity (the two neighbours adjacent) is decided by every lane for
+    // its own vertices, fetching the neighbour's row from its owner lane;
+    // the in-order walk then only visits valid candidates, and a later
+    // candidate stays applicable iff it and its two neighbours are still
+    // live (a removal only deletes vertices, so its degree cannot stay 2
+    // otherwise).
+    {
+      int ab0 = -1, ab1 = -1;
+      bool t0 = false, t1 = false;
+      {
+        const unsigned long long n0 = q.a0 & L, n1 = q.a1 & L;
+        const int a0 = __ffsll((long long)n0) - 1, b0 = 63 - __clzll((long long)n0);
+        const int a1 = __ffsll((long long)n1) - 1, b1 = 63 - __clzll((long long)n1);
+        // row of a0 / a1 from their owner lanes (all lanes shuffle)
+        const unsigned long long r0lo = __shfl_sync(0xffffffffu, q.a0, a0 & 31);
+        const unsigned long long r0hi = __shfl_sync(0xffffffffu, q.a1, a0 & 31);
+        const unsigned long long r1lo = __shfl_sync(0xffffffffu, q.a0, a1 & 31);
+        const unsigned long long r1hi = __shfl_sync(0xffffffffu, q.a1, a1 & 31);
+        if (d0 == 2) {
+          const unsigned long long ra = a0 < 32 ? r0lo : r0hi;
+          t0 = (ra >> b0) & 1;
+          ab0 = a0 | (b0 << 8);
+        }
+        if (d1 == 2) {
+          const unsigned long long ra = a1 < 32 ? r1lo : r1hi;
+          t1 = (ra >> b1) & 1;
+          ab1 = a1 | (b1 << 8);
+        }
+      }
+      unsigned long long T = ballot64(t0, t1);
+      if (T) {
+        unsigned long long R = 0;  // vertices removed by this sweep
+        int applied = 0;
+        while (T) {
+          const int v = __ffsll((long long)T) - 1;
+          T &= T - 1;
+          const int ab = __shfl_sync(0xffffffffu, v < 32 ? ab0 : ab1, v & 31);
+          const unsigned long long tri = (1ull << v) | (1ull << (ab & 255)) | (1ull << (ab >> 8));
+          if (tri & R) continue;
+          R |= tri & ~(1ull << v);
+          R |= 1ull << v;  // v leaves too (isolated once its neighbours are in)
+          ++applied;
+        }
+        const unsigned long long nb = R;  // includes the candidates themselves
+        // cover gains exactly the two neighbours per applied triangle
+        L &= ~nb;
+        S += 2 * applied;
+        st.rules[1] += applied;
+        continue;
       }
     }
-    if (changed) continue;
     // high degree (pure.py:158): a vertex of degree > k is in every cover
     // that still improves the bound
     const unsigned long long H = ballot64(d0 > k, d1 > k);
@@ -512,6 +547,7 @@ __device__ inline void warp_flush_stats(const SearchParams& P, const WStats& st)
   atomicAdd(&c->wc_fix, st.c_fix);
   atomicAdd(&c->wc_comp, st.c_comp);
   atomicAdd(&c->wc_split, st.c_split);
+  atomicAdd(&c->wc_iter, st.c_iter);
   if (atomicMax(&c->wmax, st.maxcyc) < st.maxcyc) {
     c->wmax_nodes = st.max_nodes;
     c->wmax_n = st.max_n;
