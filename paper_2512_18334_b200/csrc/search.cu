@@ -69,11 +69,18 @@ struct Worker {
   // reduced graph's order (so lowest-index tie-breaks are unchanged), rows
   // are adjacency bitmasks.  Returns false when the task ring is full.
   __device__ bool emit_task(int root, int size, int lo, int hi, int scope, int S, int depth,
-                            int counted) {
+                            int counted, long long ticket = -1) {
     const int lane = threadIdx.x & 31;
     int* gv = gl[threadIdx.x >> 5];
     long long pos = -1;
-    if (lane == 0) pos = q_reserve_push(P.bq, P.bq.cap);
+    if (lane == 0) {
+      if (ticket >= 0) {
+        q_wait_free(P.bq, ticket);
+        pos = ticket;
+      } else {
+        pos = q_reserve_push(P.bq, P.bq.cap);
+      }
+    }
     pos = __shfl_sync(0xffffffffu, pos, 0);
     if (pos < 0) return false;
     char* slot = P.bq.data + (pos % P.bq.cap) * kWSlotBytes;
@@ -439,12 +446,29 @@ struct Worker {
     const int parent = st->parent;
     if (parent >= 0 && P.record) record_split_witness(ncomp, agg, parent);
     if (parent >= 0 && P.warp_limit) {
-      // small general components go to the warp tier, one warp per component
+      // small general components go to the warp tier, one warp per
+      // component: thread 0 numbers them and claims all their ring tickets
+      // with one reservation; each task packs only its component's index
+      // span [root, vmax]
+      if (threadIdx.x == 0) {
+        int k = 0;
+        for (int j = 0; j < ncomp; ++j) {
+          const bool small = agg[5 * j + 2] >= 0 && agg[5 * j] <= P.warp_limit;
+          agg[5 * j + 3] = small ? k++ : -1;
+        }
+        const long long t0 = k ? q_reserve_push_n(P.bq, k, P.bq.cap) : -1;
+        st->qpos_lo = (int)(t0 & 0xffffffffLL);
+        st->qpos_hi = (int)(t0 >> 32);
+      }
+      __syncthreads();
+      const long long t0 = ((long long)st->qpos_hi << 32) | (unsigned)st->qpos_lo;
       const int nwarps = blockDim.x >> 5;
       for (int j = threadIdx.x >> 5; j < ncomp; j += nwarps) {
         const int c = agg[5 * j + 2];
-        if (c < 0 || agg[5 * j] > P.warp_limit) continue;
-        if (emit_task(w.lst[j], agg[5 * j], lo, hi, c, 0, h.depth + 1, 0) &&
+        const int ord = agg[5 * j + 3];
+        if (ord < 0) continue;
+        if (emit_task(w.lst[j], agg[5 * j], w.lst[j], agg[5 * j + 4], c, 0, h.depth + 1, 0,
+                      t0 >= 0 ? t0 + ord : -1) &&
             (threadIdx.x & 31) == 0)
           agg[5 * j + 1] = -1;  // taken by the warp tier
       }

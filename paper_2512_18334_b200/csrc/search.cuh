@@ -222,6 +222,31 @@ __device__ inline long long q_reserve_push(const Queue& q, long long limit) {
   return pos;
 }
 
+// Claim k consecutive tickets at once (a split's warp tasks); the caller
+// waits for each slot with q_wait_free before writing it.  -1: no room.
+__device__ inline long long q_reserve_push_n(const Queue& q, long long k, long long limit) {
+  if (limit > q.cap) limit = q.cap;
+  if ((long long)ld_relaxed_u64(q.count) + k > limit) return -1;
+  long long c = atom_add_ll(q.count, k);
+  if (c + k > limit) {
+    atom_add_ll(q.count, -k);
+    return -1;
+  }
+  return atom_add_ll(q.tail, k);
+}
+
+// the slot of ticket pos is free once its previous consumer released it
+__device__ inline void q_wait_free(const Queue& q, long long pos) {
+  unsigned spins = 0;
+  while ((long long)ld_acquire_u64(&q.seq[pos % q.cap]) != pos) {
+    __nanosleep(32);
+    if (++spins == (1u << 26)) {
+      atomicExch(q.err, 6);
+      break;
+    }
+  }
+}
+
 __device__ inline void q_publish_push(const Queue& q, long long pos) {
   __threadfence();
   st_release_u64(&q.seq[pos % q.cap], (unsigned long long)pos + 1);
