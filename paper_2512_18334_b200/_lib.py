@@ -12,7 +12,7 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_build", "libvcgpu.so")
+LIB_PATH = os.environ.get("VCG_LIB") or os.path.join(_HERE, "_build", "libvcgpu.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 I64 = C.c_int64

@@ -4,6 +4,13 @@
 #include "search.cuh"
 #include "warp_solve.cuh"
 
+#ifndef VCG_SEARCH_MAXT
+#define VCG_SEARCH_MAXT 512
+#endif
+#ifndef VCG_SEARCH_MINB
+#define VCG_SEARCH_MINB 2
+#endif
+
 namespace vcg {
 
 struct BlockState {
@@ -690,7 +697,7 @@ struct Worker {
 // a compile-time choice so every workspace access is an LDS/STS/ATOMS rather
 // than a generic-address access.
 template <typename T, bool kSmem>
-__global__ void __launch_bounds__(512, 2) search_kernel(SearchParams P) {
+__global__ void __launch_bounds__(VCG_SEARCH_MAXT, VCG_SEARCH_MINB) search_kernel(SearchParams P) {
   extern __shared__ __align__(16) unsigned char dsmem[];
   __shared__ BlockScratch bs;
   __shared__ BlockState st;

@@ -307,17 +307,20 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
     if ((++tick & (unsigned)P.w_check_mask) == 0) {
       int stop = 0, shed = 0;
       if (lane == 0) {
+        // four independent L2 reads issued together: one round trip
         stop = ld_relaxed(&P.ctl->stop);
-        if (!stop && P.ctl->deadline_ns && globaltimer() > P.ctl->deadline_ns) {
+        const unsigned long long dl = __ldcg(&P.ctl->deadline_ns);
+        const int key = ld_relaxed(&P.reg.key[th.scope]);
+        const long long ring = (long long)ld_relaxed_u64(P.bq.count);
+        if (!stop && dl && globaltimer() > dl) {
           atomicExch(&P.ctl->timed_out, 1);
           atomicExch(&P.ctl->stop, 1);
           stop = 1;
         }
         if (!stop) {  // the scope may be shared (exports, MVC root): follow its bound
-          const int b = (ld_relaxed(&P.reg.key[th.scope]) >> 1) - th.S;
+          const int b = (key >> 1) - th.S;
           if (b < ws.fr[0].best) ws.fr[0].best = b;
-          shed = tick >= (unsigned)P.w_export_after &&
-                 (long long)ld_relaxed_u64(P.bq.count) < P.bq_low;
+          shed = tick >= (unsigned)P.w_export_after && ring < P.bq_low;
         }
       }
       __syncwarp();
