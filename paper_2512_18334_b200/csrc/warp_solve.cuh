@@ -85,22 +85,50 @@ __device__ __forceinline__ unsigned long long ballot64(bool a, bool b) {
          ((unsigned long long)__ballot_sync(0xffffffffu, b) << 32);
 }
 
+// Mask helpers for both task widths: tasks of <= 32 vertices run on 32-bit
+// masks (one vertex per lane: one ballot / reduction per collective, no
+// 64-bit emulation), larger ones on 64-bit masks (two vertices per lane).
+__device__ __forceinline__ unsigned wor(unsigned x) { return __reduce_or_sync(0xffffffffu, x); }
+__device__ __forceinline__ unsigned long long wor(unsigned long long x) { return wor64(x); }
+__device__ __forceinline__ int wpopc(unsigned x) { return __popc(x); }
+__device__ __forceinline__ int wpopc(unsigned long long x) { return __popcll(x); }
+__device__ __forceinline__ int wlsb(unsigned x) { return __ffs((int)x) - 1; }
+__device__ __forceinline__ int wlsb(unsigned long long x) { return __ffsll((long long)x) - 1; }
+__device__ __forceinline__ int wmsb(unsigned x) { return 31 - __clz((int)x); }
+__device__ __forceinline__ int wmsb(unsigned long long x) { return 63 - __clzll((long long)x); }
+template <typename M>
+__device__ __forceinline__ M wbit(int i) { return (M)1 << i; }
+// vertex v live in L (v >= the mask width: never)
+__device__ __forceinline__ bool whas(unsigned L, int v) { return v < 32 && ((L >> v) & 1u); }
+__device__ __forceinline__ bool whas(unsigned long long L, int v) { return (L >> v) & 1ull; }
+template <typename M>
+__device__ __forceinline__ M wballot(bool a, bool b);
+template <>
+__device__ __forceinline__ unsigned wballot<unsigned>(bool a, bool) {
+  return __ballot_sync(0xffffffffu, a);
+}
+template <>
+__device__ __forceinline__ unsigned long long wballot<unsigned long long>(bool a, bool b) {
+  return ballot64(a, b);
+}
+
 // Per-lane view of the task graph: this lane owns vertices lane and lane+32.
+template <typename M>
 struct WLane {
-  unsigned long long a0, a1;  // adjacency rows of the two vertices
+  M a0, a1;  // adjacency rows of the two vertices (32-bit tasks: a1 = 0, v1 = 64)
   int v0, v1;
 };
 
 // Connected component of the live mask L containing r (frontier BFS, one
 // OR-reduction per level).
-__device__ __forceinline__ unsigned long long w_component(const WLane& q, unsigned long long L,
-                                                          int r) {
-  unsigned long long comp = 1ull << r, fr = comp;
+template <typename M>
+__device__ __forceinline__ M w_component(const WLane<M>& q, M L, int r) {
+  M comp = wbit<M>(r), fr = comp;
   while (fr) {
-    unsigned long long c = 0;
-    if ((fr >> q.v0) & 1) c |= q.a0;
-    if ((fr >> q.v1) & 1) c |= q.a1;
-    fr = wor64(c) & L & ~comp;
+    M c = 0;
+    if (whas(fr, q.v0)) c |= q.a0;
+    if (whas(fr, q.v1)) c |= q.a1;
+    fr = wor(c) & L & ~comp;
     comp |= fr;
   }
   return comp;
@@ -110,32 +138,33 @@ __device__ __forceinline__ unsigned long long w_component(const WLane& q, unsign
 // reduce_fixpoint: degree-one, degree-two triangle, high degree).  Leaves d0
 // / d1 = current degrees of the lane's vertices.  Returns the edge count,
 // or -1 when S reached the bound (prune).
-__device__ __forceinline__ int w_fixpoint(const WarpWs& ws, const WLane& q, unsigned long long& L,
-                                          int& S, int best, int& d0, int& d1, WStats& st) {
+template <typename M>
+__device__ __forceinline__ int w_fixpoint(const WarpWs& ws, const WLane<M>& q, M& L, int& S,
+                                          int best, int& d0, int& d1, WStats& st) {
   while (true) {
     ++st.c_iter;
-    d0 = ((L >> q.v0) & 1) ? __popcll(q.a0 & L) : 0;
-    d1 = ((L >> q.v1) & 1) ? __popcll(q.a1 & L) : 0;
-    L = ballot64(d0 > 0, d1 > 0);  // isolated vertices leave the graph
+    d0 = whas(L, q.v0) ? wpopc(q.a0 & L) : 0;
+    d1 = whas(L, q.v1) ? wpopc(q.a1 & L) : 0;
+    L = wballot<M>(d0 > 0, d1 > 0);  // isolated vertices leave the graph
     const int k = best - S - 1;    // vertices an improving cover may still take
     if (k < 0) return -1;
     // degree one (pure.py:82): the neighbour of a pendant vertex is forced;
     // of an isolated edge only the higher end (the in-order sweep's choice)
-    const unsigned long long p1 = ballot64(d0 == 1, d1 == 1);
+    const M p1 = wballot<M>(d0 == 1, d1 == 1);
     if (p1) {
-      unsigned long long c = 0;
+      M c = 0;
       if (d0 == 1) {
-        const int u = __ffsll((long long)(q.a0 & L)) - 1;
-        if (!(((p1 >> u) & 1) && u < q.v0)) c |= 1ull << u;
+        const int u = wlsb(q.a0 & L);
+        if (!(((p1 >> u) & 1) && u < q.v0)) c |= wbit<M>(u);
       }
       if (d1 == 1) {
-        const int u = __ffsll((long long)(q.a1 & L)) - 1;
-        if (!(((p1 >> u) & 1) && u < q.v1)) c |= 1ull << u;
+        const int u = wlsb(q.a1 & L);
+        if (!(((p1 >> u) & 1) && u < q.v1)) c |= wbit<M>(u);
       }
-      const unsigned long long F = wor64(c);
+      const M F = wor(c);
       L &= ~F;
-      S += __popcll(F);
-      st.rules[0] += __popcll(F);
+      S += wpopc(F);
+      st.rules[0] += wpopc(F);
       continue;
     }
     // degree-two triangle (pure.py:113): in index order with revalidation.
@@ -149,40 +178,40 @@ __device__ __forceinline__ int w_fixpoint(const WarpWs& ws, const WLane& q, unsi
       int ab0 = -1, ab1 = -1;
       bool t0 = false, t1 = false;
       {
-        const unsigned long long n0 = q.a0 & L, n1 = q.a1 & L;
-        const int a0 = __ffsll((long long)n0) - 1, b0 = 63 - __clzll((long long)n0);
-        const int a1 = __ffsll((long long)n1) - 1, b1 = 63 - __clzll((long long)n1);
+        const M n0 = q.a0 & L, n1 = q.a1 & L;
+        const int a0 = wlsb(n0), b0 = wmsb(n0);
+        const int a1 = wlsb(n1), b1 = wmsb(n1);
         // row of a0 / a1 from their owner lanes (all lanes shuffle)
-        const unsigned long long r0lo = __shfl_sync(0xffffffffu, q.a0, a0 & 31);
-        const unsigned long long r0hi = __shfl_sync(0xffffffffu, q.a1, a0 & 31);
-        const unsigned long long r1lo = __shfl_sync(0xffffffffu, q.a0, a1 & 31);
-        const unsigned long long r1hi = __shfl_sync(0xffffffffu, q.a1, a1 & 31);
+        const M r0lo = __shfl_sync(0xffffffffu, q.a0, a0 & 31);
+        const M r0hi = __shfl_sync(0xffffffffu, q.a1, a0 & 31);
+        const M r1lo = __shfl_sync(0xffffffffu, q.a0, a1 & 31);
+        const M r1hi = __shfl_sync(0xffffffffu, q.a1, a1 & 31);
         if (d0 == 2) {
-          const unsigned long long ra = a0 < 32 ? r0lo : r0hi;
+          const M ra = a0 < 32 ? r0lo : r0hi;
           t0 = (ra >> b0) & 1;
           ab0 = a0 | (b0 << 8);
         }
         if (d1 == 2) {
-          const unsigned long long ra = a1 < 32 ? r1lo : r1hi;
+          const M ra = a1 < 32 ? r1lo : r1hi;
           t1 = (ra >> b1) & 1;
           ab1 = a1 | (b1 << 8);
         }
       }
-      unsigned long long T = ballot64(t0, t1);
+      M T = wballot<M>(t0, t1);
       if (T) {
-        unsigned long long R = 0;  // vertices removed by this sweep
+        M R = 0;  // vertices removed by this sweep
         int applied = 0;
         while (T) {
-          const int v = __ffsll((long long)T) - 1;
+          const int v = wlsb(T);
           T &= T - 1;
           const int ab = __shfl_sync(0xffffffffu, v < 32 ? ab0 : ab1, v & 31);
-          const unsigned long long tri = (1ull << v) | (1ull << (ab & 255)) | (1ull << (ab >> 8));
+          const M tri = wbit<M>(v) | wbit<M>(ab & 255) | wbit<M>(ab >> 8);
           if (tri & R) continue;
-          R |= tri & ~(1ull << v);
-          R |= 1ull << v;  // v leaves too (isolated once its neighbours are in)
+          R |= tri & ~wbit<M>(v);
+          R |= wbit<M>(v);  // v leaves too (isolated once its neighbours are in)
           ++applied;
         }
-        const unsigned long long nb = R;  // includes the candidates themselves
+        const M nb = R;  // includes the candidates themselves
         // cover gains exactly the two neighbours per applied triangle
         L &= ~nb;
         S += 2 * applied;
@@ -192,11 +221,11 @@ __device__ __forceinline__ int w_fixpoint(const WarpWs& ws, const WLane& q, unsi
     }
     // high degree (pure.py:158): a vertex of degree > k is in every cover
     // that still improves the bound
-    const unsigned long long H = ballot64(d0 > k, d1 > k);
+    const M H = wballot<M>(d0 > k, d1 > k);
     if (H) {
       L &= ~H;
-      S += __popcll(H);
-      st.rules[2] += __popcll(H);
+      S += wpopc(H);
+      st.rules[2] += wpopc(H);
       continue;
     }
     break;
@@ -228,15 +257,17 @@ __device__ inline bool warp_export(const SearchParams& P, const WarpWs& ws, cons
 
 // Solve one task to completion (or until the stop flag).  All 32 lanes run
 // it with warp-uniform state; returns false when abandoned on stop.
+template <typename M>
 __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const WTaskHdr th,
-                                WStats& st) {
+                                       WStats& st) {
   const int lane = threadIdx.x & 31;
   const int n = th.n & 0xffff;
-  WLane q;
+  constexpr bool kTwo = sizeof(M) == 8;
+  WLane<M> q;
   q.v0 = lane;
-  q.v1 = lane + 32;
-  q.a0 = q.v0 < n ? ws.adj[q.v0] : 0ull;
-  q.a1 = q.v1 < n ? ws.adj[q.v1] : 0ull;
+  q.v1 = kTwo ? lane + 32 : 64;  // 64: never live (whas)
+  q.a0 = q.v0 < n ? (M)ws.adj[q.v0] : (M)0;
+  q.a1 = kTwo && q.v1 < n ? (M)ws.adj[q.v1] : (M)0;
   bool skip_count = (th.n >> 16) & 1;
 
   int sb = 0;
@@ -247,7 +278,7 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
   ws.fr[0].base = 0;
   ws.fr[0].pend_b = ws.fr[0].pend_e = 0;
   int nf = 1, sp = 0;
-  unsigned long long L = th.live;
+  M L = (M)th.live;
   int S = 0;
   bool have = ws.fr[0].best > 0;
   unsigned tick = 0;
@@ -257,7 +288,7 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
       const int f = nf - 1;
       if (sp > ws.fr[f].base) {
         --sp;
-        L = ws.stL[sp];
+        L = (M)ws.stL[sp];
         S = ws.stS[sp];
         have = true;
       } else if (f == 0) {
@@ -271,9 +302,9 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
         }
         F.running += F.best;
         if (F.pend_e > F.pend_b) {
-          const unsigned long long c = ws.pend[--F.pend_e];
+          const M c = (M)ws.pend[--F.pend_e];
           const int bound = ws.fr[f - 1].best - F.running - (F.pend_e - F.pend_b);
-          const int size = __popcll(c);
+          const int size = wpopc(c);
           if (bound <= 0) {
             --nf;
             continue;
@@ -309,7 +340,7 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
       if (lane == 0) {
         // four independent L2 reads issued together: one round trip
         stop = ld_relaxed(&P.ctl->stop);
-        const unsigned long long dl = __ldcg(&P.ctl->deadline_ns);
+        const M dl = __ldcg(&P.ctl->deadline_ns);
         const int key = ld_relaxed(&P.reg.key[th.scope]);
         const long long ring = (long long)ld_relaxed_u64(P.bq.count);
         if (!stop && dl && globaltimer() > dl) {
@@ -342,7 +373,7 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
     long long c0 = clock64();
     const int E = w_fixpoint(ws, q, L, S, F.best, d0, d1, st);
     long long c1 = clock64();
-    st.c_fix += (unsigned long long)(c1 - c0);
+    st.c_fix += (M)(c1 - c0);
     have = false;
     if (E < 0) continue;
     {
@@ -358,25 +389,25 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
       continue;
     }
     // --------------------------------------------------- components --
-    unsigned long long comp = w_component(q, L, __ffsll((long long)L) - 1);
+    M comp = w_component(q, L, wlsb(L));
     c0 = clock64();
-    st.c_comp += (unsigned long long)(c0 - c1);
+    st.c_comp += (M)(c0 - c1);
     if (comp != L) {
       ++st.splits;
       int special = 0, ng = 0, ncomp = 0;
       // pend[] is a stack: frames <= f own everything below F.pend_e; the
       // general components are staged at pend[pbase ..] in discovery order
       const int pbase = F.pend_e;
-      unsigned long long rest = L;
+      M rest = L;
       bool overflow = false;
       while (true) {
         ++ncomp;
-        const int size = __popcll(comp);
-        const bool in0 = (comp >> q.v0) & 1, in1 = (comp >> q.v1) & 1;
-        if (!ballot64(in0 && d0 != size - 1, in1 && d1 != size - 1)) {
+        const int size = wpopc(comp);
+        const bool in0 = whas(comp, q.v0), in1 = whas(comp, q.v1);
+        if (!wballot<M>(in0 && d0 != size - 1, in1 && d1 != size - 1)) {
           special += size - 1;  // clique: all but one vertex
           st.rules[4] += 1;
-        } else if (size >= 3 && !ballot64(in0 && d0 != 2, in1 && d1 != 2)) {
+        } else if (size >= 3 && !wballot<M>(in0 && d0 != 2, in1 && d1 != 2)) {
           special += (size + 1) / 2;  // chordless cycle
           st.rules[5] += 1;
         } else {
@@ -386,10 +417,10 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
         }
         rest &= ~comp;
         if (!rest) break;
-        comp = w_component(q, rest, __ffsll((long long)rest) - 1);
+        comp = w_component(q, rest, wlsb(rest));
       }
       if (lane == 0) atomicAdd(&P.hist[ncomp < P.n + 1 ? ncomp : P.n + 1], 1ull);
-      st.c_split += (unsigned long long)(clock64() - c0);
+      st.c_split += (M)(clock64() - c0);
       const int base_S = S + special;
       if (ng == 0) {
         if (base_S < F.best) {
@@ -401,7 +432,7 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
       }
       if (base_S + ng >= F.best) continue;  // every general component needs >= 1
       if (ng == 1) {
-        L = ws.pend[pbase];
+        L = (M)ws.pend[pbase];
         S = base_S;
         have = true;
         continue;
@@ -415,7 +446,7 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
       }
       // new frame: solve pend[pbase] now, the rest afterwards (popped from
       // the end, so store them reversed to keep discovery order)
-      const unsigned long long first = ws.pend[pbase];
+      const M first = (M)ws.pend[pbase];
       for (int i = 1, j = ng - 1; i < j; ++i, --j) {
         const unsigned long long t = ws.pend[pbase + i];
         ws.pend[pbase + i] = ws.pend[pbase + j];
@@ -426,7 +457,7 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
       G.pend_b = pbase + 1;
       G.pend_e = pbase + ng;
       const int bound = F.best - base_S - (ng - 1);
-      const int size = __popcll(first);
+      const int size = wpopc(first);
       if (size - 1 < bound) {
         G.best = size - 1;
         G.ach = 1;
@@ -446,10 +477,10 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
     unsigned k1 = d1 > 0 ? ((unsigned)d1 << 7) | (127u - q.v1) : 0u;
     const unsigned key = __reduce_max_sync(0xffffffffu, k0 > k1 ? k0 : k1);
     const int v = 127 - (int)(key & 127u);
-    const unsigned long long nv = ws.adj[v] & L;
+    const M nv = (M)ws.adj[v] & L;
     // engine.py:319: exclude child (v out, N(v) in) to the stack, include
     // child (v in) continues here
-    const int Sx = S + __popcll(nv);
+    const int Sx = S + wpopc(nv);
     if (Sx < F.best) {
       if (sp >= kWStack) {
         if (lane == 0) {
@@ -458,11 +489,11 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
         }
         return false;
       }
-      ws.stL[sp] = L & ~(nv | (1ull << v));
+      ws.stL[sp] = L & ~(nv | wbit<M>(v));
       ws.stS[sp] = Sx;
       ++sp;
     }
-    L &= ~(1ull << v);
+    L &= ~wbit<M>(v);
     S += 1;
     have = true;
   }
@@ -517,7 +548,8 @@ __device__ inline bool warp_epoch(const SearchParams& P, WarpWs* wws, int* busy,
     const long long t0 = clock64();
     const unsigned long long nodes0 = st.nodes;
     if (lane == 0) atomicMin(&P.ctl->t_task_first, globaltimer());
-    warp_solve_task(P, ws, th, st);
+    if (n <= 32) warp_solve_task<unsigned>(P, ws, th, st);
+    else warp_solve_task<unsigned long long>(P, ws, th, st);
     __syncwarp();
     if (lane == 0) {
       reg_finish(P, th.scope);  // the task's live unit on its scope
