@@ -229,6 +229,15 @@ struct Worker {
   // Returns the destination; *qpos >= 0 means a reserved worklist slot.
   __device__ char* choose_dest(long long* qpos) {
     VCG_HB(w.bs, 30);
+    reserve_dest();
+    return resolve_dest(qpos);
+  }
+
+  // choose_dest in two halves: thread 0 claims the worklist ticket (L2
+  // atomics) without a barrier, so the claim overlaps the block's work up
+  // to the next barrier; resolve_dest (all threads, after that barrier or
+  // its own) reads the outcome.
+  __device__ void reserve_dest() {
     if (threadIdx.x == 0) {
       long long pos = -1;
       if (P.share) pos = q_reserve_push(P.q, P.threshold);
@@ -247,6 +256,9 @@ struct Worker {
       st->qpos_lo = (int)(pos & 0xffffffffLL);
       st->qpos_hi = (int)(pos >> 32);
     }
+  }
+
+  __device__ char* resolve_dest(long long* qpos) {
     VCG_HB(w.bs, 31);
     __syncthreads();
     VCG_HB(w.bs, 32);
@@ -631,7 +643,9 @@ struct Worker {
     }
     // engine.py:319 _branch_on_vertex
     if (threadIdx.x == 0) lb.inc(P, h.scope);
-    // exclude child: built in the second shared-memory buffer, then stored
+    // exclude child: built in the second shared-memory buffer, then stored;
+    // its destination is claimed first so the claim overlaps the build
+    reserve_dest();
     {
       const long long words = payload / 16;  // [deg | inc] -> [deg2 | inc2]
       const uint4* a = (const uint4*)w.deg;
@@ -645,7 +659,7 @@ struct Worker {
     int removed, edges;
     remove_neighbors_fast(wx, v, w.lst, &removed, &edges);
     long long qpos;
-    char* dst = choose_dest(&qpos);
+    char* dst = resolve_dest(&qpos);
     if (dst) {
       store_payload(dst, w.deg2, payload);
       NodeHdr ex = h;

@@ -31,6 +31,15 @@
 
 namespace vcg {
 
+// per-phase cycle counters of warp tasks (SolveResult.phase_cycles
+// warp_*_cycles): build with -DVCG_WARP_PROFILE; off by default, the
+// counters live in local memory on the hot path
+#ifdef VCG_WARP_PROFILE
+#define WPROF(...) __VA_ARGS__
+#else
+#define WPROF(...)
+#endif
+
 constexpr int kWMax = 64;      // vertices per warp task
 constexpr int kWStack = 72;    // DFS stack entries per warp (depth <= 64)
 constexpr int kWFrames = 24;   // nested component frames (each >= 6 vertices)
@@ -142,7 +151,7 @@ template <typename M>
 __device__ __forceinline__ int w_fixpoint(const WarpWs& ws, const WLane<M>& q, M& L, int& S,
                                           int best, int& d0, int& d1, WStats& st) {
   while (true) {
-    ++st.c_iter;
+    WPROF(++st.c_iter);
     d0 = whas(L, q.v0) ? wpopc(q.a0 & L) : 0;
     d1 = whas(L, q.v1) ? wpopc(q.a1 & L) : 0;
     L = wballot<M>(d0 > 0, d1 > 0);  // isolated vertices leave the graph
@@ -340,7 +349,7 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
       if (lane == 0) {
         // four independent L2 reads issued together: one round trip
         stop = ld_relaxed(&P.ctl->stop);
-        const M dl = __ldcg(&P.ctl->deadline_ns);
+        const unsigned long long dl = __ldcg(&P.ctl->deadline_ns);
         const int key = ld_relaxed(&P.reg.key[th.scope]);
         const long long ring = (long long)ld_relaxed_u64(P.bq.count);
         if (!stop && dl && globaltimer() > dl) {
@@ -370,10 +379,9 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
     else ++st.nodes;
     WFrame& F = ws.fr[f];
     int d0, d1;
-    long long c0 = clock64();
+    WPROF(long long c0 = clock64());
     const int E = w_fixpoint(ws, q, L, S, F.best, d0, d1, st);
-    long long c1 = clock64();
-    st.c_fix += (M)(c1 - c0);
+    WPROF(long long c1 = clock64(); st.c_fix += (unsigned long long)(c1 - c0));
     have = false;
     if (E < 0) continue;
     {
@@ -390,8 +398,7 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
     }
     // --------------------------------------------------- components --
     M comp = w_component(q, L, wlsb(L));
-    c0 = clock64();
-    st.c_comp += (M)(c0 - c1);
+    WPROF(c0 = clock64(); st.c_comp += (unsigned long long)(c0 - c1));
     if (comp != L) {
       ++st.splits;
       int special = 0, ng = 0, ncomp = 0;
@@ -420,7 +427,7 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
         comp = w_component(q, rest, wlsb(rest));
       }
       if (lane == 0) atomicAdd(&P.hist[ncomp < P.n + 1 ? ncomp : P.n + 1], 1ull);
-      st.c_split += (M)(clock64() - c0);
+      WPROF(st.c_split += (unsigned long long)(clock64() - c0));
       const int base_S = S + special;
       if (ng == 0) {
         if (base_S < F.best) {
