@@ -190,3 +190,20 @@ def test_torus_time_budget_consistent():
     assert r.cover_size >= 1800
     assert not r.exact
     assert r.stats.tree_nodes_visited > 0
+
+
+def test_deadline_far_in_future_is_exact():
+    """A generous time limit arms the device deadline checks (block loop and
+    warp-task poll) without ever firing them: answers stay exact.  Regression
+    test for a narrowed deadline read in 32-bit warp tasks."""
+    import paper_2512_18334_b200 as vc
+    from paper_2512_18334_b200 import synth
+
+    for case in golden("solve.json")[::5]:
+        g = _graph(case)
+        r = vc.solve(g, vc.SolverConfig(timeout=120.0))
+        assert r.exact and r.cover_size == case["runs"]["det"]["cover_size"], case["name"]
+    exp = golden("workloads.json")["rgg2000"]
+    n, off, nbr = synth.WORKLOADS["rgg2000"]()
+    r = vc.solve(vc.StaticGraph(n, off, nbr), vc.SolverConfig(timeout=120.0))
+    assert r.exact and r.cover_size == exp["mvc"]
