@@ -41,3 +41,40 @@ def test_large_config_cover_and_pvc_pair(name):
     no = vc.solve(g, vc.SolverConfig(mode="pvc", k=opt - 1))
     assert yes.found and yes.cover_size <= opt
     assert not no.found
+
+
+@pytest.mark.parametrize("name", ["gnp400", "torus60"])
+def test_time_budget_configs_return_valid_covers(name):
+    """configs[4] runs under a time budget (no exact answer in reach for
+    either side).  As in the reference (engine.py:655), a timed-out solve
+    reports its incumbent size but no cover; the incumbent is then
+    witnessed by a PVC solve at k = incumbent, whose cover must be valid.
+    The incumbent is no smaller than a maximal matching (torus60: a perfect
+    matching, 1800)."""
+    import numpy as np
+
+    import paper_2512_18334_b200 as vc
+    from paper_2512_18334_b200 import synth
+
+    n, off, nbr = synth.WORKLOADS[name]()
+    off, nbr = np.asarray(off), np.asarray(nbr)
+    g = vc.StaticGraph(n, off, nbr)
+    r = vc.solve(g, vc.SolverConfig(record_cover=True, timeout=1.0))
+    assert not r.exact and r.cover is None
+    best = r.cover_size
+    w = vc.solve(g, vc.SolverConfig(mode="pvc", k=best, record_cover=True, timeout=30.0))
+    assert w.found and w.cover is not None and len(w.cover) <= best
+    assert_valid_cover(n, off, nbr, w.cover)
+    matched = np.zeros(n, dtype=bool)
+    lb = 0
+    for v in range(n):
+        if matched[v]:
+            continue
+        for x in nbr[off[v]:off[v + 1]]:
+            if not matched[x] and x != v:
+                matched[v] = matched[x] = True
+                lb += 1
+                break
+    assert best >= lb
+    if name == "torus60":
+        assert best >= 1800
