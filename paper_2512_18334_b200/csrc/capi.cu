@@ -1127,6 +1127,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   P.ws_in_smem = in_smem;
   P.share = share;
   P.batch_live = !cfg->deterministic && !getenv("VCG_NO_BATCH");
+  P.par_rules = !cfg->deterministic && !getenv("VCG_EXACT_RULES");
   P.threshold = threshold;
   P.use_components = cfg->use_components;
   P.use_bounds = cfg->use_bounds;

@@ -937,11 +937,73 @@ __device__ PassRet degree_two_triangle_pass_fast(const NodeWs<T>& w, int b, int 
   return PassRet{applied, 2 * applied, edges, 0};
 }
 
+// Triangle sweep for the parallel search: every valid candidate v (degree
+// 2, neighbours u, x adjacent) claims its closed triangle {v, u, x} with
+// atomicMin on tmin; v applies iff it holds all three claims.  Applied
+// triangles are vertex-disjoint, so applying them together is sound (a
+// removal can only invalidate a candidate whose closed triangle it
+// touches); the minimum valid candidate always applies, and the rest are
+// revisited by the fixpoint's next sweep.  A different (but sound) choice
+// than the reference's in-order walk, so only the parallel mode uses it:
+// answers are the same, rule counts may differ.
+template <typename T>
+__device__ PassRet degree_two_triangle_pass_par(const NodeWs<T>& w, int b, int e, int* rem) {
+  VCG_HB(w.bs, 107);
+  int nvalid = 0;
+  for (int v = b; v < e; ++v) {
+    if (w.deg[v] == 2) {
+      int u = -1, x2 = -1;
+      for (int i = w.off[v]; i < w.off[v + 1]; ++i) {
+        int x = w.nbr[i];
+        if (w.deg[x] > 0) {
+          if (u < 0) {
+            u = x;
+          } else {
+            x2 = x;
+            break;
+          }
+        }
+      }
+      if (x2 >= 0 && adjacent_static(w, u, x2)) {
+        w.ia[v] = u;
+        w.ib[v] = x2;
+        w.lst[atomicAdd(&w.bs->bc[8], 1)] = v;
+        atomicMin(&w.tmin[v], v);
+        atomicMin(&w.tmin[u], v);
+        atomicMin(&w.tmin[x2], v);
+        ++nvalid;
+      }
+    }
+  }
+  nvalid = block_sum(nvalid, w.bs);
+  if (nvalid == 0) return PassRet{0, 0, 0, 0};
+  for (int k = threadIdx.x; k < nvalid; k += blockDim.x) {
+    const int v = w.lst[k], u = w.ia[v], x2 = w.ib[v];
+    if (w.tmin[v] == v && w.tmin[u] == v && w.tmin[x2] == v) {
+      w.flag[u] = 1;
+      w.flag[x2] = 1;
+      const int at = atomicAdd(&w.bs->bc[9], 2);
+      rem[at] = u;
+      rem[at + 1] = x2;
+    }
+  }
+  __syncthreads();
+  const int total = w.bs->bc[9];
+  for (int k = threadIdx.x; k < nvalid; k += blockDim.x) {
+    const int v = w.lst[k];
+    w.tmin[v] = kInf;
+    w.tmin[w.ia[v]] = kInf;
+    w.tmin[w.ib[v]] = kInf;
+  }
+  int edges = remove_list_fast(w, rem, total);
+  return PassRet{total / 2, total, edges, 0};
+}
+
 // reduce_fixpoint (pure.py:188) for the search: identical forced sets and
 // counters; one fused scan decides which sweeps have candidates.
 template <typename T>
 __device__ FixRet reduce_fixpoint_fast(const NodeWs<T>& w, int lo, int hi, int budget,
-                                      long long* maxkey) {
+                                      long long* maxkey, bool par_tri = false) {
   FixRet r{0, 0, 0, 0, 0, lo, hi, 0};
   int b, e;
   my_chunk(lo, hi, &b, &e);
@@ -995,7 +1057,8 @@ __device__ FixRet reduce_fixpoint_fast(const NodeWs<T>& w, int lo, int hi, int b
     }
     int tri = 0;
     if (st.c2 > 0) {
-      PassRet t = degree_two_triangle_pass_fast(w, b, e, rem);
+      PassRet t = par_tri ? degree_two_triangle_pass_par(w, b, e, rem)
+                          : degree_two_triangle_pass_fast(w, b, e, rem);
       rprof(w.bs, 2, &t0);
       tri = t.applied;
       r.d2t += t.applied;

@@ -555,7 +555,7 @@ struct Worker {
     const int best_s = st->best_s;
     const int budget = best_s - h.S - 1;
     long long maxkey;
-    FixRet fr = reduce_fixpoint_fast(w, h.lo, h.hi, budget, &maxkey);
+    FixRet fr = reduce_fixpoint_fast(w, h.lo, h.hi, budget, &maxkey, P.par_rules != 0);
     tick(PH_REDUCE);
     if (fr.pos < 0) {  // inconsistent degree array (a protocol bug): fail loudly
       if (threadIdx.x == 0) {
@@ -771,19 +771,26 @@ __global__ void __launch_bounds__(VCG_SEARCH_MAXT, VCG_SEARCH_MINB) search_kerne
   }
   bool cont = false;
   unsigned backoff = 32;
+  unsigned iter = 0;
   while (true) {
     VCG_HB(&bs, 50);
-    if (threadIdx.x == 0) {
-      int stop = ld_relaxed(&P.ctl->stop);
-      if (!stop && P.ctl->deadline_ns && globaltimer() > P.ctl->deadline_ns) {
-        atomicExch(&P.ctl->timed_out, 1);
-        atomicExch(&P.ctl->stop, 1);
-        stop = 1;
+    // stop / deadline poll: before every pop, and every 4th node of an
+    // include chain (the poll is an L2 round trip plus a barrier)
+    if (!cont || (++iter & 3) == 0) {
+      if (threadIdx.x == 0) {
+        const int stop0 = ld_relaxed(&P.ctl->stop);
+        const unsigned long long dl = __ldcg(&P.ctl->deadline_ns);
+        int stop = stop0;
+        if (!stop && dl && globaltimer() > dl) {
+          atomicExch(&P.ctl->timed_out, 1);
+          atomicExch(&P.ctl->stop, 1);
+          stop = 1;
+        }
+        st.flag = stop;
       }
-      st.flag = stop;
+      __syncthreads();
+      if (st.flag) break;
     }
-    __syncthreads();
-    if (st.flag) break;
     wk.tick(PH_OTHER);
     if (!cont) {
       if (wk.top > 0) {

@@ -105,6 +105,7 @@ struct SearchParams {
   int root_in_stack;
   int record;             // record-cover mode: nodes carry inclusion bitsets
   int batch_live;         // parallel mode: LiveBatch decrement batching
+  int par_rules;          // parallel mode: claim-based triangle sweep (sound, not in-order)
   int nw;                 // bitset words per record
   unsigned* wbits;        // witness arena [wcap][nw]
   int* wcount;
