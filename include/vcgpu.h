@@ -77,6 +77,11 @@ typedef struct {
  * fused order-free sweeps on an on-chip workspace (the solve path). */
 #define VCG_ROOT_RULES 1
 #define VCG_ROOT_ANY_ORDER 2
+/* MVC without a bound (has_bound == 0): the greedy cover of g may be skipped
+ * and reported as greedy_original = -1 when a matching lower bound proves it
+ * cannot change the reduction or the search's initial bound (then the search
+ * starts from greedy_reduced, achieved). */
+#define VCG_ROOT_LAZY_GREEDY 4
 
 /* Root reduction (lightweight rules on the device to a joint fixpoint with
  * the crown rule) and device compaction of the survivors.

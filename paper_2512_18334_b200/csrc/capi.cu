@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -583,10 +584,12 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
   // greedy value is known the host checks that the real budget would not
   // have fired it either (else the pipeline reruns with the real bound).
   int64_t greedy_orig = -1;
+  std::atomic<bool> greedy_cancel{false};
   std::thread greedy_thr;
   if (has_bound != 1)
     greedy_thr = std::thread([&]() {
-      greedy_orig = greedy_cover_host(g->n, g->h_off.data(), g->h_nbr.data(), nullptr);
+      greedy_orig =
+          greedy_cover_host(g->n, g->h_off.data(), g->h_nbr.data(), nullptr, &greedy_cancel);
     });
   struct JoinGuard {
     std::thread& t;
@@ -740,6 +743,28 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
   tr.mark("compaction");
   info->greedy_reduced = greedy_cover_host(red->n, red->h_off.data(), red->h_nbr.data(), nullptr);
   tr.mark("greedy_reduced");
+  // VCG_ROOT_LAZY_GREEDY (the MVC solve path): every vertex cover of g has
+  // at least forced + (maximal matching of the reduced graph) vertices --
+  // the root rules keep an optimal cover -- and so does the greedy one.  If
+  // that lower bound already certifies both uses of the greedy value (the
+  // speculative high-degree check and best_init = greedy_reduced), the
+  // greedy is abandoned and reported as -1.
+  if ((enabled & VCG_ROOT_LAZY_GREEDY) && has_bound == 0 && spec) {
+    const int64_t lb =
+        forced_count + maximal_matching_host(red->n, red->h_off.data(), red->h_nbr.data());
+    bool ok = info->greedy_reduced <= lb - forced_count;
+    for (const auto& sr : spec_rounds) ok = ok && sr.first <= lb - sr.second;
+    if (ok) {
+      greedy_cancel.store(true, std::memory_order_relaxed);
+      if (greedy_thr.joinable()) greedy_thr.join();
+      tr.mark("greedy_original skipped");
+      info->greedy_original = -1;
+      if (vertex_map_out)
+        for (size_t i = 0; i < vmap.size(); ++i) vertex_map_out[i] = vmap[i];
+      *reduced_out = red;
+      return 0;
+    }
+  }
   if (greedy_thr.joinable()) greedy_thr.join();
   tr.mark("greedy_original joined");
   info->greedy_original = greedy_orig;

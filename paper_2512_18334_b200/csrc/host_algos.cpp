@@ -23,7 +23,8 @@ namespace vcg {
 // list[d] once, when its degree reaches d) and are visited through a
 // bitmap over their index span.  O(n + m + sum over levels of span/64)
 // time, sequential memory traffic apart from the degree updates.
-int64_t greedy_cover_host(int64_t n, const int64_t* off, const int32_t* nbr, int32_t* members) {
+int64_t greedy_cover_host(int64_t n, const int64_t* off, const int32_t* nbr, int32_t* members,
+                          const std::atomic<bool>* cancel) {
   if (n <= 0) return 0;
   std::vector<int32_t> deg(n);
   int64_t m2 = 0, maxdeg = 0;
@@ -46,6 +47,7 @@ int64_t greedy_cover_host(int64_t n, const int64_t* off, const int32_t* nbr, int
   for (int64_t d = maxdeg; d >= 1; --d) {
     std::vector<int32_t>& cand = level[d];
     if (cand.empty()) continue;
+    if (cancel && cancel->load(std::memory_order_relaxed)) return -1;
     int64_t wlo = INT64_MAX, whi = -1;
     for (int32_t v : cand)
       if (deg[v] == d) {
@@ -71,6 +73,23 @@ int64_t greedy_cover_host(int64_t n, const int64_t* off, const int32_t* nbr, int
         deg[v] = 0;
         if (members) members[size] = (int32_t)v;
         ++size;
+      }
+    }
+  }
+  return size;
+}
+
+int64_t maximal_matching_host(int64_t n, const int64_t* off, const int32_t* nbr) {
+  std::vector<uint8_t> matched((size_t)std::max<int64_t>(n, 1), 0);
+  int64_t size = 0;
+  for (int64_t v = 0; v < n; ++v) {
+    if (matched[v]) continue;
+    for (int64_t i = off[v]; i < off[v + 1]; ++i) {
+      const int32_t x = nbr[i];
+      if (x != v && !matched[x]) {
+        matched[v] = matched[x] = 1;
+        ++size;
+        break;
       }
     }
   }

@@ -1,11 +1,17 @@
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <vector>
 
 namespace vcg {
 
-// greedy max-degree cover of a CSR graph; members (nullable) gets the picks
-int64_t greedy_cover_host(int64_t n, const int64_t* off, const int32_t* nbr, int32_t* members);
+// greedy max-degree cover of a CSR graph; members (nullable) gets the picks;
+// returns -1 if `cancel` (nullable) is raised before it finishes
+int64_t greedy_cover_host(int64_t n, const int64_t* off, const int32_t* nbr, int32_t* members,
+                          const std::atomic<bool>* cancel = nullptr);
+
+// size of a greedy maximal matching (a lower bound on every vertex cover)
+int64_t maximal_matching_host(int64_t n, const int64_t* off, const int32_t* nbr);
 
 // one crown reduction on deg (int32, mutated); returns #heads forced
 int64_t crown_reduce_host(int64_t n, const int64_t* off, const int32_t* nbr, int32_t* deg,

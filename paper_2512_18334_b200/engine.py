@@ -237,7 +237,7 @@ def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
     bound = cfg.k if cfg.mode == "pvc" else None
     pre = root_reduce(g, enabled=cfg.use_root_reduce, crown=cfg.use_crown, bound=bound,
                       width_override=cfg.width, need_greedy_original=bound is None,
-                      ordered=False)
+                      ordered=False, lazy_greedy=bound is None)
     stats.phase_seconds["root_reduce"] = time.perf_counter() - t0
     for key, val in pre.rule_counts.items():
         stats.rule_counts[key] = stats.rule_counts.get(key, 0) + val
@@ -273,7 +273,10 @@ def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
         best_init = min(greedy_reduced, k_red + 1)
         achieved_init = greedy_reduced <= k_red + 1
     else:
-        cap = pre.greedy_original - pre.forced_count
+        # greedy_original == -1: skipped by the library because a matching
+        # lower bound proved greedy_reduced <= greedy_original - forced
+        cap = (pre.greedy_original - pre.forced_count if pre.greedy_original >= 0
+               else greedy_reduced)
         best_init = max(1, min(greedy_reduced, cap))
         achieved_init = greedy_reduced <= cap
 

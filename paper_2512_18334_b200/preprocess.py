@@ -67,21 +67,27 @@ class Preprocessed:
 
 def root_reduce(g: StaticGraph, enabled: bool = True, crown: bool = True,
                 bound: int | None = None, width_override: int | None = None,
-                need_greedy_original: bool = True, ordered: bool = True) -> Preprocessed:
+                need_greedy_original: bool = True, ordered: bool = True,
+                lazy_greedy: bool = False) -> Preprocessed:
     """preprocess.py:397 root_reduce on the device.
 
     ``need_greedy_original=False`` (used by PVC solves, where the bound is k)
     skips the greedy cover of the input graph; ``greedy_original`` is then -1.
     ``ordered=False`` (the solve path) returns ``forced`` in index order
     instead of the reference's forcing order -- same set, same rule counts --
-    so the device can run the fused order-free sweeps on chip."""
+    so the device can run the fused order-free sweeps on chip.
+    ``lazy_greedy=True`` (the MVC solve path) lets the library skip the
+    greedy cover of the input when a matching lower bound certifies that it
+    cannot matter; ``greedy_original`` is then -1 and the search starts from
+    ``greedy_reduced`` (achieved)."""
     n = g.num_vertices
     info = _lib.Preprocessed_t()
     forced = np.zeros(max(n, 1), dtype=np.int32)
     vmap = np.zeros(max(n, 1), dtype=np.int64)
     h = C.c_void_p()
     _lib.check(_lib.lib.vcg_root_reduce(
-        g.device().handle, (1 if enabled else 0) | (0 if ordered else 2), int(crown),
+        g.device().handle,
+        (1 if enabled else 0) | (0 if ordered else 2) | (4 if lazy_greedy else 0), int(crown),
         0 if bound is None else (2 if need_greedy_original else 1),
         int(bound) if bound is not None else 0, C.byref(info), forced.ctypes.data,
         vmap.ctypes.data, C.byref(h)))
