@@ -122,6 +122,10 @@ typedef struct {
                                  vertices are solved by one warp as bitmask tasks;
                                  0 = off.  Ignored (off) in deterministic, record-cover,
                                  no-components and no-pruning runs. */
+  int gpu_share;              /* concurrent searches sharing the device (>= 1): each
+                                 takes 1/gpu_share of the resident block slots.  Calls
+                                 from different host threads run concurrently (each
+                                 thread has its own stream and pooled buffers). */
 } vcg_search_config;
 
 typedef struct {

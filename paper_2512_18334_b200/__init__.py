@@ -6,7 +6,7 @@ root reduction, compaction and the whole search running as hand-written
 sm_100a CUDA kernels behind the C-ABI in ``include/vcgpu.h``.
 """
 
-from .engine import SolveResult, SolverConfig, Stats, solve
+from .engine import SolveResult, SolverConfig, Stats, solve, solve_batch
 from .graph import StaticGraph, build_csr, induced_subgraph
 from .preprocess import Preprocessed, greedy_bound, root_reduce, select_width
 
@@ -26,5 +26,6 @@ __all__ = [
     "root_reduce",
     "select_width",
     "solve",
+    "solve_batch",
     "__version__",
 ]

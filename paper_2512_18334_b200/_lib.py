@@ -39,6 +39,7 @@ class SearchConfig_t(C.Structure):
         ("workers", C.c_int), ("threads", C.c_int), ("worklist_threshold", I64),
         ("timeout", C.c_double), ("check_registry", C.c_int), ("record_cover", C.c_int),
         ("cover_out", C.c_void_p), ("root_deg", C.c_void_p), ("warp_limit", C.c_int),
+        ("gpu_share", C.c_int),
     ]
 
 

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <unistd.h>
@@ -31,10 +32,10 @@ __global__ void search_init_kernel(SearchParams P, int root_key, unsigned long l
 }  // namespace vcg
 
 static thread_local std::string g_err;
-static unsigned long long g_launches = 0;  // kernels this library launched
+static std::atomic<unsigned long long> g_launches{0};  // kernels this library launched
 #define COUNT_LAUNCH(k) (g_launches += (k))
 
-extern "C" int64_t vcg_launch_count(void) { return (int64_t)g_launches; }
+extern "C" int64_t vcg_launch_count(void) { return (int64_t)g_launches.load(); }
 
 static int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -47,6 +48,21 @@ static int fail(int code, const std::string& msg) {
     if (e_ != cudaSuccess)                                                             \
       return fail(VCG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
   } while (0)
+
+// The dynamic shared-memory limit is a process-wide attribute of a kernel:
+// concurrent solves (solve_batch threads) must only ever raise it, or one
+// thread's launch can fail after another lowered it.
+static int raise_smem_limit(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<const void*, size_t> cur;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& c = cur[fn];
+  if (bytes > c) {
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    c = bytes;
+  }
+  return 0;
+}
 
 extern "C" const char* vcg_last_error(void) { return g_err.c_str(); }
 
@@ -72,7 +88,7 @@ struct Tracer {
   explicit Tracer(const char* w) : what(w) {}
   void mark(const char* step) {
     if (!trace_on()) return;
-    cudaDeviceSynchronize();
+    cudaStreamSynchronize(cudaStreamPerThread);
     auto now = std::chrono::steady_clock::now();
     fprintf(stderr, "[vcg %s] %-22s %8.3f ms\n", what, step,
             std::chrono::duration<double, std::milli>(now - last).count());
@@ -89,18 +105,22 @@ static int need_device() {
 
 // ------------------------------------------------------------------ graph --
 
+// Device buffers come from the stream-ordered allocator on the calling
+// thread's stream: cudaFree would synchronise the whole device and
+// serialise concurrent solves on other threads (solve_batch).
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, cudaStreamPerThread);
   }
   int ensure(size_t b) {
     if (b <= bytes && p) return 0;
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, cudaStreamPerThread);
     p = nullptr;
     bytes = 0;
-    if (cudaMalloc(&p, b ? b : 16) != cudaSuccess) return fail(VCG_ERESOURCE, "cudaMalloc failed");
+    if (cudaMallocAsync(&p, b ? b : 16, cudaStreamPerThread) != cudaSuccess)
+      return fail(VCG_ERESOURCE, "cudaMallocAsync failed");
     bytes = b;
     return 0;
   }
@@ -126,10 +146,13 @@ struct vcg_graph {
   DevBuf d_nbr;  // int32[2m]
 };
 
-// search buffers are reused across graphs and solves (grown on demand)
+// search buffers are reused across graphs and solves (grown on demand), one
+// set per host thread: the library is built with --default-stream
+// per-thread, so calls from different threads run on independent streams
+// and may overlap on the device (solve_batch)
 static SearchCtx& search_ctx() {
-  static SearchCtx* ctx = new SearchCtx();
-  return *ctx;
+  static thread_local SearchCtx ctx;  // released when its thread exits
+  return ctx;
 }
 
 extern "C" int vcg_graph_create(int64_t n, const int64_t* offsets, const int32_t* neighbors,
@@ -454,7 +477,7 @@ static int node_op_t(int op, int64_t n, const int64_t* offsets, const int32_t* n
                            dws.as<char>(), (int)lo, (int)hi, (int)budget, (int)v,
                            dout.as<int32_t>(), (int)pos, dret.as<long long>());
   CK(cudaGetLastError());
-  CK(cudaDeviceSynchronize());
+  CK(cudaStreamSynchronize(cudaStreamPerThread));
   CK(cudaMemcpy(degt.data(), ddeg.p, n * sizeof(T), cudaMemcpyDeviceToHost));
   for (int64_t i = 0; i < n; ++i) deg[i] = degt[i];
   CK(cudaMemcpy(out, dout.p, ocap * 4, cudaMemcpyDeviceToHost));
@@ -647,8 +670,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
     const bool fast = (enabled & VCG_ROOT_ANY_ORDER) && fast_smem + 8192 <= smem_optin &&
                       !getenv("VCG_ROOT_ORDERED");
     if (fast)
-      CK(cudaFuncSetAttribute(k_root_fixpoint_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)fast_smem));
+      if (int r = raise_smem_limit((const void*)k_root_fixpoint_fast, (size_t)fast_smem)) return r;
     int crown_applied_last = 1;
     static const int root_threads = getenv("VCG_ROOT_THREADS") ? atoi(getenv("VCG_ROOT_THREADS")) : 1024;
     while (true) {
@@ -974,7 +996,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   int dev = 0;
   CK(cudaGetDevice(&dev));
   // cudaGetDeviceProperties costs tens of ms per call: cache two attributes
-  static int cached_dev = -1, sm_count = 0, smem_optin = 0;
+  static thread_local int cached_dev = -1, sm_count = 0, smem_optin = 0;
   if (cached_dev != dev) {
     CK(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
     CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -1023,7 +1045,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
         else pl->warp_limit = 0;
       }
     }
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->dsmem));
+    if (int r = raise_smem_limit((const void*)kern, pl->dsmem)) return r;
     pl->per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->per_sm, kern, th, pl->dsmem));
     return 0;
@@ -1062,7 +1084,8 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   const size_t dsmem = pl.dsmem;
   const int per_sm = pl.per_sm;
   if (per_sm < 1) return fail(VCG_ERESOURCE, "search kernel does not fit on an SM");
-  const int resident = per_sm * sm_count;
+  const int share_k = cfg->gpu_share > 1 ? cfg->gpu_share : 1;
+  const int resident = std::max(1, per_sm * sm_count / share_k);
   int blocks = cfg->deterministic ? 1 : (cfg->workers > 0 ? cfg->workers : resident);
   if (blocks > resident) blocks = resident;
 
@@ -1226,15 +1249,15 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   CK(cudaGetLastError());
   tr.mark("init");
 
-  static cudaEvent_t e0 = nullptr, e1 = nullptr;
+  static thread_local cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (!e0) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
   }
   // debug heartbeat: per-warp progress codes in host-mapped memory, dumped
   // (and the process ended) when the search kernel overruns VCG_HEARTBEAT s
-  static int* hb_host = nullptr;
-  static long long hb_cap = 0;
+  static thread_local int* hb_host = nullptr;
+  static thread_local long long hb_cap = 0;
   const char* hb_env = getenv("VCG_HEARTBEAT");
   P.hb = nullptr;
   if (hb_env) {
@@ -1281,7 +1304,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   }
   tr.mark("search_kernel");
   drain_kernel<<<1, 32>>>(P);
-  CK(cudaDeviceSynchronize());
+  CK(cudaStreamSynchronize(cudaStreamPerThread));
   tr.mark("drain");
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);

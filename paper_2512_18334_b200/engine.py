@@ -59,6 +59,9 @@ class SolverConfig:
     # solved by one warp each as bitmask tasks; 0 = off.  Parallel mode only
     # (deterministic / record_cover runs keep the reference's node schedule).
     warp_limit: int = 64
+    # concurrent searches sharing the GPU (solve_batch sets it): each takes
+    # 1/gpu_share of the resident block slots
+    gpu_share: int = 1
     _disable_pruning: bool = False
 
     def validate(self) -> None:
@@ -75,6 +78,8 @@ class SolverConfig:
             raise ValueError("worklist threshold must be >= 1")
         if not 0 <= self.warp_limit <= 64:
             raise ValueError("warp_limit must be in [0, 64]")
+        if self.gpu_share < 1:
+            raise ValueError("gpu_share must be >= 1")
 
 
 @dataclass
@@ -175,6 +180,7 @@ def run_search(rg: StaticGraph, cfg: SolverConfig, width: int, best_init: int,
     sc.timeout = float(cfg.timeout or 0.0)
     sc.check_registry = int(cfg.check_registry)
     sc.warp_limit = int(cfg.warp_limit)
+    sc.gpu_share = int(cfg.gpu_share)
     cover = None
     if record:
         cover = np.zeros(max(rg.num_vertices, 1), dtype=np.int32)
@@ -335,3 +341,36 @@ def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
         result.cover_size = len(result.cover)
         stats.phase_seconds["reconstruct"] = time.perf_counter() - t2
     return result
+
+
+def solve_batch(graphs, configs) -> list[SolveResult]:
+    """Several independent solves at once on one GPU (e.g. the PVC pair
+    k = opt / opt - 1): each runs on its own host thread, stream and pooled
+    buffers with 1/len(configs) of the resident block slots
+    (``gpu_share``), so the latency-bound searches overlap on the device.
+    ``graphs`` is one StaticGraph for all configs or one per config.
+    Results are those of ``solve`` (same answers; schedules differ)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from dataclasses import replace
+
+    configs = list(configs)
+    if not isinstance(graphs, (list, tuple)):
+        graphs = [graphs] * len(configs)
+    if len(graphs) != len(configs):
+        raise ValueError("one graph per config (or a single graph)")
+    k = len(configs)
+    if k <= 1:
+        return [solve(graphs[0], configs[0])] if k else []
+    shared = [replace(c, gpu_share=max(c.gpu_share, k)) if not c.deterministic else c
+              for c in configs]
+    for g in graphs:  # upload once, before the threads share the handle
+        g.device()
+    global _BATCH_POOL
+    if _BATCH_POOL is None or _BATCH_POOL._max_workers < k:
+        # long-lived workers: each keeps its stream and pooled device buffers
+        _BATCH_POOL = ThreadPoolExecutor(max_workers=k, thread_name_prefix="vcg-batch")
+    futs = [_BATCH_POOL.submit(solve, g, c) for g, c in zip(graphs, shared)]
+    return [f.result() for f in futs]
+
+
+_BATCH_POOL = None

@@ -207,3 +207,25 @@ def test_deadline_far_in_future_is_exact():
     n, off, nbr = synth.WORKLOADS["rgg2000"]()
     r = vc.solve(vc.StaticGraph(n, off, nbr), vc.SolverConfig(timeout=120.0))
     assert r.exact and r.cover_size == exp["mvc"]
+
+
+def test_solve_batch_matches_sequential():
+    """solve_batch (concurrent searches on per-thread streams, each with a
+    share of the block slots) gives the sequential answers, repeatedly (the
+    worker threads keep their pooled buffers across calls)."""
+    import paper_2512_18334_b200 as vc
+    from paper_2512_18334_b200 import synth
+
+    exp = golden("workloads.json")["rgg2000"]
+    n, off, nbr = synth.WORKLOADS["rgg2000"]()
+    g = vc.StaticGraph(n, off, nbr)
+    opt = exp["mvc"]
+    for _ in range(5):
+        rs = vc.solve_batch(g, [vc.SolverConfig(mode="pvc", k=opt),
+                                vc.SolverConfig(mode="pvc", k=opt - 1),
+                                vc.SolverConfig()])
+        assert rs[0].found and not rs[1].found and rs[2].cover_size == opt
+    cases = golden("solve.json")[::7]
+    graphs = [_graph(c) for c in cases]
+    rs = vc.solve_batch(graphs, [vc.SolverConfig() for _ in cases])
+    assert [r.cover_size for r in rs] == [c["runs"]["det"]["cover_size"] for c in cases]
