@@ -100,6 +100,18 @@ static int need_device() {
   int c = 0;
   cudaError_t e = cudaGetDeviceCount(&c);
   if (e != cudaSuccess || c == 0) return fail(VCG_ENODEV, "no CUDA device available");
+  // keep freed stream-ordered allocations in the device's pool (per-solve
+  // graphs are allocated and released every call)
+  static thread_local int pooled_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess && dev != pooled_dev) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pooled_dev = dev;
+  }
   return 0;
 }
 
