@@ -117,22 +117,35 @@ static int need_device() {
 
 // ------------------------------------------------------------------ graph --
 
-// Device buffers come from the stream-ordered allocator on the calling
-// thread's stream: cudaFree would synchronise the whole device and
-// serialise concurrent solves on other threads (solve_batch).
+// Device buffer.  Per-call objects (graphs: allocated and released every
+// solve) use the stream-ordered allocator on the calling thread's stream --
+// cudaFree would synchronise the whole device and serialise concurrent
+// solves on other threads (solve_batch).  The long-lived pooled search
+// buffers (tens of GB for large graphs, grown rarely) use cudaMalloc, which
+// maps large sizes faster.
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
-  ~DevBuf() {
-    if (p) cudaFreeAsync(p, cudaStreamPerThread);
+  bool stream_ordered = false;
+  DevBuf() = default;
+  explicit DevBuf(bool so) : stream_ordered(so) {}
+  ~DevBuf() { release(); }
+  void release() {
+    if (!p) return;
+    if (stream_ordered) cudaFreeAsync(p, cudaStreamPerThread);
+    else cudaFree(p);
+    p = nullptr;
+    bytes = 0;
   }
   int ensure(size_t b) {
     if (b <= bytes && p) return 0;
-    if (p) cudaFreeAsync(p, cudaStreamPerThread);
-    p = nullptr;
-    bytes = 0;
-    if (cudaMallocAsync(&p, b ? b : 16, cudaStreamPerThread) != cudaSuccess)
-      return fail(VCG_ERESOURCE, "cudaMallocAsync failed");
+    release();
+    const cudaError_t e = stream_ordered ? cudaMallocAsync(&p, b ? b : 16, cudaStreamPerThread)
+                                         : cudaMalloc(&p, b ? b : 16);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      return fail(VCG_ERESOURCE, "device allocation failed");
+    }
     bytes = b;
     return 0;
   }
@@ -154,8 +167,8 @@ struct vcg_graph {
   int64_t m2 = 0;  // 2 * edges
   std::vector<int64_t> h_off;
   std::vector<int32_t> h_nbr;
-  DevBuf d_off;  // int32[n+1]
-  DevBuf d_nbr;  // int32[2m]
+  DevBuf d_off{true};  // int32[n+1]
+  DevBuf d_nbr{true};  // int32[2m]
 };
 
 // search buffers are reused across graphs and solves (grown on demand), one

@@ -27,8 +27,8 @@ def gpu_solve(n, off, nbr, reps=3, **kw):
     """Median end-to-end time over `reps` solves after one untimed warm-up
     solve (first-call costs -- module load, pooled buffer growth -- excluded)."""
     times, r = [], None
-    if not kw.get("timeout"):
-        vc.solve(vc.StaticGraph(n, np.array(off), np.array(nbr)), vc.SolverConfig(**kw))
+    warm = dict(kw, timeout=0.2) if kw.get("timeout") else kw
+    vc.solve(vc.StaticGraph(n, np.array(off), np.array(nbr)), vc.SolverConfig(**warm))
     for _ in range(reps):
         t = time.perf_counter()
         g = vc.StaticGraph(n, np.array(off), np.array(nbr))
