@@ -212,6 +212,8 @@ int64_t vcg_launch_count(void);
 int vcg_device_count(void);
 /* Make `device` current for this thread's subsequent calls. */
 int vcg_set_device(int device);
+/* The calling thread's current device (-1 on error). */
+int vcg_get_device(void);
 /* Device time in ms of the last vcg_root_reduce phases etc. is in the structs. */
 
 #ifdef __cplusplus

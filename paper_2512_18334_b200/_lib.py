@@ -75,7 +75,7 @@ EXPORTS = (
     "vcg_graph_create", "vcg_graph_destroy", "vcg_graph_num_vertices", "vcg_graph_num_edges",
     "vcg_graph_download", "vcg_induced_subgraph", "vcg_greedy_bound", "vcg_root_reduce",
     "vcg_search", "vcg_node_op", "vcg_last_error", "vcg_device_count", "vcg_launch_count",
-    "vcg_set_device", "vcg_expand",
+    "vcg_set_device", "vcg_get_device", "vcg_expand",
 )
 
 
@@ -134,3 +134,8 @@ def launch_count() -> int:
 
 def set_device(device: int) -> None:
     check(lib.vcg_set_device(int(device)))
+
+
+def get_device() -> int:
+    """The calling thread's current CUDA device."""
+    return int(lib.vcg_get_device())

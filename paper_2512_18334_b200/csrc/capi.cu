@@ -72,6 +72,12 @@ extern "C" int vcg_device_count(void) {
   return c;
 }
 
+extern "C" int vcg_get_device(void) {
+  int d = -1;
+  if (cudaGetDevice(&d) != cudaSuccess) return -1;
+  return d;
+}
+
 extern "C" int vcg_set_device(int device) {
   if (cudaSetDevice(device) != cudaSuccess) return fail(VCG_ENODEV, "cudaSetDevice failed");
   return 0;

@@ -369,7 +369,13 @@ def solve_batch(graphs, configs) -> list[SolveResult]:
     if _BATCH_POOL is None or _BATCH_POOL._max_workers < k:
         # long-lived workers: each keeps its stream and pooled device buffers
         _BATCH_POOL = ThreadPoolExecutor(max_workers=k, thread_name_prefix="vcg-batch")
-    futs = [_BATCH_POOL.submit(solve, g, c) for g, c in zip(graphs, shared)]
+    dev = _lib.get_device()  # worker threads start on device 0: adopt the caller's
+
+    def on_device(g, c):
+        _lib.set_device(dev)
+        return solve(g, c)
+
+    futs = [_BATCH_POOL.submit(on_device, g, c) for g, c in zip(graphs, shared)]
     return [f.result() for f in futs]
 
 
