@@ -196,15 +196,22 @@ def run_b200(args):
     import torch
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
+    # one rank per GPU; ranks only share a GPU when there are fewer GPUs than
+    # ranks (a functional test of the multi-process path), then over gloo
+    ndev = torch.cuda.device_count()
+    device = local % ndev
+    torch.cuda.set_device(device)
     import paper_2512_18334_b200 as vc
     from paper_2512_18334_b200 import _lib
 
-    _lib.set_device(local)
+    _lib.set_device(device)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if world <= ndev:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group("gloo")
     strong = args.mode == "strong" and world > 1
     n, off, nbr = instance(1 if strong else 1 + rank)
     g = vc.StaticGraph(n, off, nbr)
@@ -259,7 +266,7 @@ def run_b200(args):
     rec.update(bytes=0, kernel_ms=0.0, launches=0)
     l0 = _lib.launch_count()
     total_ms, nodes = 0.0, 0.0
-    with ClockSampler(local) as clk:
+    with ClockSampler(device) as clk:
         for _ in range(args.steps):
             flush.zero_()  # L2 flush between timed steps (outside the events)
             barrier()
@@ -293,7 +300,8 @@ def run_b200(args):
     d2h = 2 * ((rg.num_vertices + 1) * 4 + len(rg.neighbors) * 4 + rg.num_vertices * 4
                + n * 4 + (rg.num_vertices + 2) * 8 + 512)
 
-    t = torch.tensor([total_ms, nodes, e2e_ms, e2e_nodes], dtype=torch.float64, device="cuda")
+    t = torch.tensor([total_ms, nodes, e2e_ms, e2e_nodes], dtype=torch.float64,
+                     device="cuda" if world <= ndev else "cpu")
     if world > 1:
         tmax = t.clone()
         torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
