@@ -96,10 +96,23 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
+    def mark_start(self):
+        self.w0 = len(self.lines)
+
+    def mark_end(self):
+        # the first sample after the window closes is the nearest one when
+        # the timed region is shorter than nvidia-smi's sampling period
+        self.w1 = len(self.lines)
+        deadline = time.time() + 1.0
+        while len(self.lines) <= self.w1 and time.time() < deadline and self.proc:
+            time.sleep(0.01)
+
     def summary(self):
         sm, mx, reasons = [], [], set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
+        w0, w1 = getattr(self, "w0", 0), getattr(self, "w1", len(self.lines))
+        window = self.lines[w0:max(w1, w0 + 1)]
+        for ln in window:
             p = [x.strip() for x in ln.split(",")]
             if len(p) < 7:
                 continue
@@ -114,7 +127,8 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "samples_in_window": max(0, w1 - w0)}
 
 
 # ------------------------------------------------------------ reference ----
@@ -260,23 +274,26 @@ def run_b200(args):
 
     _eng.run_search = run_search_probe
 
+    clk = ClockSampler(device).__enter__()  # running before the timed region
     for _ in range(args.warmup):
         pair(g)
     barrier()
     rec.update(bytes=0, kernel_ms=0.0, launches=0)
     l0 = _lib.launch_count()
     total_ms, nodes = 0.0, 0.0
-    with ClockSampler(device) as clk:
-        for _ in range(args.steps):
-            flush.zero_()  # L2 flush between timed steps (outside the events)
-            barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            nd, _ = pair(g)
-            e1.record()
-            torch.cuda.synchronize()
-            total_ms += e0.elapsed_time(e1)
-            nodes += nd
+    clk.mark_start()
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        nd, _ = pair(g)
+        e1.record()
+        torch.cuda.synchronize()
+        total_ms += e0.elapsed_time(e1)
+        nodes += nd
+    clk.mark_end()
+    clk.__exit__(None, None, None)
     launches = _lib.launch_count() - l0
     search_bytes, search_ms, search_launches = rec["bytes"], rec["kernel_ms"], rec["launches"]
 
