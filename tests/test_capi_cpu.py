@@ -55,3 +55,14 @@ def test_warp_limit_validation():
     for bad in (-1, 65):
         with pytest.raises(ValueError):
             vc.SolverConfig(warp_limit=bad).validate()
+
+
+def test_gpu_share_and_batch_validation():
+    import paper_2512_18334_b200 as vc
+
+    with pytest.raises(ValueError):
+        vc.SolverConfig(gpu_share=0).validate()
+    g = vc.StaticGraph(3, [0, 1, 2, 2], [1, 0])
+    with pytest.raises(ValueError):
+        vc.solve_batch([g, g], [vc.SolverConfig()])  # one graph per config
+    assert vc.solve_batch(g, []) == []
