@@ -214,6 +214,36 @@ extern "C" int vcg_graph_create(int64_t n, const int64_t* offsets, const int32_t
   return 0;
 }
 
+// Host compaction of the survivors (deg > 0) of a graph whose final degree
+// array is on the host: same order and relabelling as compact_flagged, one
+// upload instead of the device path's scan / count / gather round trips
+// (used by the root pipeline for graphs up to kHostCompactMax vertices).
+static constexpr int kHostCompactMax = 1 << 17;
+
+static int compact_host(const vcg_graph* g, const int32_t* deg, vcg_graph** out,
+                        std::vector<int64_t>* vmap_host) {
+  const int64_t n = g->n;
+  std::vector<int32_t> newid((size_t)std::max<int64_t>(n, 1), -1);
+  std::vector<int64_t> off(1, 0), vm;
+  int64_t nk = 0;
+  for (int64_t v = 0; v < n; ++v)
+    if (deg[v] > 0) {
+      newid[v] = (int32_t)nk++;
+      vm.push_back(v);
+    }
+  std::vector<int32_t> nbr;
+  off.reserve(nk + 1);
+  for (int64_t v : vm) {
+    for (int64_t j = g->h_off[v]; j < g->h_off[v + 1]; ++j) {
+      const int32_t x = g->h_nbr[j];
+      if (deg[x] > 0) nbr.push_back(newid[x]);
+    }
+    off.push_back((int64_t)nbr.size());
+  }
+  if (vmap_host) *vmap_host = vm;
+  return vcg_graph_create(nk, off.data(), nbr.data(), out);
+}
+
 extern "C" int vcg_graph_destroy(vcg_graph* g) {
   delete g;
   return 0;
@@ -661,6 +691,8 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
   if (flag.ensure((size_t)(n + 1) * 4)) return VCG_ERESOURCE;
   std::vector<int64_t> vmap;
   int64_t forced_count = 0;
+  bool host_compact = false;
+  std::vector<int32_t> host_deg;
   if (!rules_on) {
     std::vector<int32_t> ones(n + 1, 1);
     ones[n] = 0;
@@ -703,6 +735,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
     if (fast)
       if (int r = raise_smem_limit((const void*)k_root_fixpoint_fast, (size_t)fast_smem)) return r;
     int crown_applied_last = 1;
+    bool hdeg_current = false;  // hdeg mirrors the device degrees
     static const int root_threads = getenv("VCG_ROOT_THREADS") ? atoi(getenv("VCG_ROOT_THREADS")) : 1024;
     while (true) {
       int64_t progressed = 0;
@@ -712,6 +745,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
       // unchanged and the crown again empty: skip it (same counts)
       if (!first && !crown_applied_last) break;
       COUNT_LAUNCH(1);
+      hdeg_current = false;
       const int budget = spec ? kSpecBudget : (int)(bound0 - forced_count);
       if (fast) {
         k_root_fixpoint_fast<<<1, root_threads, fast_smem>>>(
@@ -745,6 +779,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
       if (crown) {
         auto t1 = std::chrono::steady_clock::now();
         CK(cudaMemcpy(hdeg.data(), ws.p, (size_t)n * 4, cudaMemcpyDeviceToHost));
+        hdeg_current = true;
         std::vector<int32_t> heads;
         int64_t er = 0;
         int64_t nh = crown_reduce_host(n, g->h_off.data(), g->h_nbr.data(), hdeg.data(), lo, hi,
@@ -778,14 +813,25 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
     (void)pos;
     if (forced_out)
       for (size_t i = 0; i < forced.size(); ++i) forced_out[i] = forced[i];
-    COUNT_LAUNCH(1);
-    k_flags_from_deg<<<(n + 256) / 256 + 1, 256>>>(ws.as<uint32_t>(), n, flag.as<int32_t>());
-    CK(cudaGetLastError());
+    if (n <= kHostCompactMax) {
+      if (!hdeg_current)
+        CK(cudaMemcpy(hdeg.data(), ws.p, (size_t)n * 4, cudaMemcpyDeviceToHost));
+      host_compact = true;
+      host_deg.swap(hdeg);
+    } else {
+      COUNT_LAUNCH(1);
+      k_flags_from_deg<<<(n + 256) / 256 + 1, 256>>>(ws.as<uint32_t>(), n, flag.as<int32_t>());
+      CK(cudaGetLastError());
+    }
   }
   tr.mark("rules+crown");
   auto t2 = std::chrono::steady_clock::now();
   vcg_graph* red = nullptr;
-  if (int r = compact_flagged(g, flag, &red, &vmap)) return r;
+  if (host_compact) {
+    if (int r = compact_host(g, host_deg.data(), &red, &vmap)) return r;
+  } else if (int r = compact_flagged(g, flag, &red, &vmap)) {
+    return r;
+  }
   info->seconds[2] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t2).count();
   info->forced_count = forced_count;
   info->n_reduced = red->n;
