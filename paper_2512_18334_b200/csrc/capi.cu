@@ -600,6 +600,8 @@ __global__ void __launch_bounds__(1024, 1)
                          int hi, int budget, int32_t* out, long long* ret, int init) {
   extern __shared__ __align__(16) unsigned char rsm[];
   __shared__ BlockScratch bs;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 4; ++i) bs.rcyc[i] = bs.rcnt[i] = 0;
   init_block_scratch(&bs);
   NodeWs<uint32_t> w = carve_ws<uint32_t>((char*)rsm, n, &bs, off, nbr);
   const int nwords = (n + 31) / 32;
@@ -641,6 +643,10 @@ __global__ void __launch_bounds__(1024, 1)
     ret[7] = tot;
     ret[8] = f.pos < 0 ? 1 : 0;
     ret[9] = bs.spec_m;
+    for (int i = 0; i < 4; ++i) {  // sweep profile: scans, degree-one, triangle, high-degree
+      ret[10 + i] = (long long)bs.rcnt[i];
+      ret[14 + i] = (long long)bs.rcyc[i];
+    }
   }
 }
 
@@ -700,7 +706,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
   } else {
     DevBuf &ws = X.r_ws, &dout = X.r_out, &dret = X.r_ret;
     if (ws.ensure(ws_total<uint32_t>(n)) || dout.ensure((size_t)(2 * n + 4) * 4) ||
-        dret.ensure(128))
+        dret.ensure(256))
       return VCG_ERESOURCE;
     NodeWs<uint32_t> layout = {};
     (void)layout;
@@ -740,7 +746,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
     while (true) {
       int64_t progressed = 0;
       auto t0 = std::chrono::steady_clock::now();
-      long long ret[10];
+      long long ret[18];
       // a round after a crown that applied nothing finds the fixpoint
       // unchanged and the crown again empty: skip it (same counts)
       if (!first && !crown_applied_last) break;
@@ -757,7 +763,10 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
                                      dout.as<int32_t>(), 0, dret.as<long long>(), first);
       }
       CK(cudaGetLastError());
-      CK(cudaMemcpy(ret, dret.p, 80, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(ret, dret.p, fast ? 144 : 80, cudaMemcpyDeviceToHost));
+      if (fast && trace_on())
+        fprintf(stderr, "[vcg root] fixpoint sweeps: scans %lld (%lld cyc) d1 %lld (%lld) tri %lld (%lld) hd %lld (%lld)\n",
+                ret[10], ret[14], ret[11], ret[15], ret[12], ret[16], ret[13], ret[17]);
       if (fast && ret[8]) return fail(VCG_ECUDA, "root fixpoint: inconsistent degree array");
       if (spec) spec_rounds.emplace_back(fast ? ret[9] : ret[8], forced_count);
       first = 0;
