@@ -874,14 +874,18 @@ __device__ PassRet degree_one_pass_fast(const NodeWs<T>& w, int b, int e, int nc
   return PassRet{total, total, edges, 0};
 }
 
-// triangle sweep (pure.py:113) for the search: valid candidates are marked
-// in a bitmap (w.vbits, all-zero between sweeps); lane 0 walks it in index
-// order -- exactly the reference's in-order conflict resolution -- clearing
-// each word as it goes; removals use the one-barrier path.
+// Triangle sweep with the reference's exact outcome, resolved in parallel.
+// The in-order walk applies candidate c iff no earlier applied candidate's
+// closed triangle T = {v, u, x} meets T(c) (a shared vertex is always a
+// removed neighbour of one of them), i.e. the applied set is the
+// lexicographically-first maximal independent set of the triangles'
+// intersection graph.  Rounds: every undecided candidate claims its three
+// vertices (atomicMin); one holding all three claims has no undecided
+// earlier conflicting candidate, so it is in; one touching a removed vertex
+// is out.  The minimum undecided candidate is decided every round.
 template <typename T>
-__device__ PassRet degree_two_triangle_pass_fast(const NodeWs<T>& w, int b, int e, int* rem) {
-  VCG_HB(w.bs, 103);
-  unsigned* vbits = w.vbits;
+__device__ PassRet degree_two_triangle_pass_lfmis(const NodeWs<T>& w, int b, int e, int* rem) {
+  VCG_HB(w.bs, 108);
   int nvalid = 0;
   for (int v = b; v < e; ++v) {
     if (w.deg[v] == 2) {
@@ -900,41 +904,54 @@ __device__ PassRet degree_two_triangle_pass_fast(const NodeWs<T>& w, int b, int 
       if (x2 >= 0 && adjacent_static(w, u, x2)) {
         w.ia[v] = u;
         w.ib[v] = x2;
-        atomicOr(&vbits[v >> 5], 1u << (v & 31));
+        const int k = atomicAdd(&w.bs->bc[8], 1);
+        w.lst[k] = v;
+        w.ic[k] = 0;  // undecided
         ++nvalid;
       }
     }
   }
-  VCG_FENCE();
   nvalid = block_sum(nvalid, w.bs);
   if (nvalid == 0) return PassRet{0, 0, 0, 0};
-  if (threadIdx.x == 0) {
-    int p = 0, applied = 0;
-    const int w0 = b >> 5;  // thread 0's chunk starts at the window start
-    int found = 0;
-    for (int wi = w0; found < nvalid; ++wi) {
-      unsigned m = vbits[wi];
-      vbits[wi] = 0u;
-      while (m) {
-        const int v = (wi << 5) + __ffs(m) - 1;
-        m &= m - 1;
-        ++found;
-        const int u = w.ia[v], x2 = w.ib[v];
-        if (!w.flag[v] && !w.flag[u] && !w.flag[x2]) {
-          w.flag[u] = 1;
-          w.flag[x2] = 1;
-          rem[p++] = u;
-          rem[p++] = x2;
-          ++applied;
-        }
+  while (true) {
+    for (int k = threadIdx.x; k < nvalid; k += blockDim.x) {
+      if (w.ic[k] != 0) continue;
+      const int v = w.lst[k];
+      atomicMin(&w.tmin[v], v);
+      atomicMin(&w.tmin[w.ia[v]], v);
+      atomicMin(&w.tmin[w.ib[v]], v);
+    }
+    __syncthreads();
+    int open = 0;
+    for (int k = threadIdx.x; k < nvalid; k += blockDim.x) {
+      if (w.ic[k] != 0) continue;
+      const int v = w.lst[k], u = w.ia[v], x2 = w.ib[v];
+      if (((volatile uint8_t*)w.flag)[v] | ((volatile uint8_t*)w.flag)[u] |
+          ((volatile uint8_t*)w.flag)[x2]) {
+        w.ic[k] = 2;  // meets an applied triangle's removed vertex
+      } else if (w.tmin[v] == v && w.tmin[u] == v && w.tmin[x2] == v) {
+        w.ic[k] = 1;
+        w.flag[u] = 1;
+        w.flag[x2] = 1;
+        const int at = atomicAdd(&w.bs->bc[9], 2);
+        rem[at] = u;
+        rem[at + 1] = x2;
+      } else {
+        open = 1;
       }
     }
-    w.bs->bc[0] = applied;
+    __syncthreads();
+    for (int k = threadIdx.x; k < nvalid; k += blockDim.x) {
+      const int v = w.lst[k];
+      w.tmin[v] = kInf;
+      w.tmin[w.ia[v]] = kInf;
+      w.tmin[w.ib[v]] = kInf;
+    }
+    if (!__syncthreads_or(open)) break;
   }
-  __syncthreads();
-  const int applied = w.bs->bc[0];
-  int edges = remove_list_fast(w, rem, 2 * applied);
-  return PassRet{applied, 2 * applied, edges, 0};
+  const int total = w.bs->bc[9];
+  int edges = remove_list_fast(w, rem, total);
+  return PassRet{total / 2, total, edges, 0};
 }
 
 // Triangle sweep for the parallel search: every valid candidate v (degree
@@ -1058,7 +1075,7 @@ __device__ FixRet reduce_fixpoint_fast(const NodeWs<T>& w, int lo, int hi, int b
     int tri = 0;
     if (st.c2 > 0) {
       PassRet t = par_tri ? degree_two_triangle_pass_par(w, b, e, rem)
-                          : degree_two_triangle_pass_fast(w, b, e, rem);
+                          : degree_two_triangle_pass_lfmis(w, b, e, rem);
       rprof(w.bs, 2, &t0);
       tri = t.applied;
       r.d2t += t.applied;
