@@ -1084,12 +1084,22 @@ __device__ FixRet reduce_fixpoint_fast(const NodeWs<T>& w, int lo, int hi, int b
       cycle += t.applied;
     }
     if (tri > 0 || st.ch > 0) {
-      PassRet h = high_degree_pass(w, lo, hi, budget - r.forced, rem, 0);
-      rprof(w.bs, 3, &t0);
-      r.hd += h.applied;
-      r.forced += h.forced;
-      r.edges += h.edges;
-      cycle += h.applied;
+      // the last scan's maximum degree bounds every degree now (degrees only
+      // fall): if it is within the budget the sweep could force nothing
+      const int bud_now = budget - r.forced;
+      const int dmax_ub = st.key >= 0 ? (int)(st.key >> 32) : 0;
+      if (st.ch == 0 && dmax_ub <= bud_now) {
+        if (bud_now > kSpecBudget / 2 && threadIdx.x == 0 &&
+            dmax_ub + (kSpecBudget - bud_now) > w.bs->spec_m)
+          w.bs->spec_m = dmax_ub + (kSpecBudget - bud_now);  // speculative-budget record
+      } else {
+        PassRet h = high_degree_pass(w, lo, hi, bud_now, rem, 0);
+        rprof(w.bs, 3, &t0);
+        r.hd += h.applied;
+        r.forced += h.forced;
+        r.edges += h.edges;
+        cycle += h.applied;
+      }
     }
     if (cycle == 0) break;
   }
