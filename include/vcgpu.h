@@ -7,19 +7,19 @@
  *
  * Reference interfaces replaced (arxiv/paper_2512_18334 = python package
  * `vcsolver`, /root/reference/pkg/src/vcsolver):
- *   vcg_graph_create / vcg_graph_destroy  <- graph.py:69 build_csr / StaticGraph
+ *   vcg_graph_create / vcg_graph_destroy  <- graph.py:74 build_csr / graph.py:33 StaticGraph
  *                                            (the CSR is uploaded once to HBM)
- *   vcg_induced_subgraph                   <- graph.py:112 induced_subgraph
- *   vcg_greedy_bound                       <- preprocess.py:348 greedy_bound,
- *                                            oracle.py:632 greedy_cover
- *   vcg_root_reduce                        <- preprocess.py:397 root_reduce
+ *   vcg_induced_subgraph                   <- graph.py:99 induced_subgraph
+ *   vcg_greedy_bound                       <- preprocess.py:28 greedy_bound
+ *                                            (kernels/pure.py:306 greedy_cover)
+ *   vcg_root_reduce                        <- preprocess.py:77 root_reduce
  *                                            (reductions.py:110 reduce_to_fixpoint
  *                                            + reductions.py:263 crown_reduce
- *                                            + graph.py:112 induced_subgraph)
+ *                                            + graph.py:99 induced_subgraph)
  *   vcg_search                             <- engine.py:160 _Engine.run (the
  *                                            threaded search behind solve(),
  *                                            engine.py:561)
- *   vcg_node_op                            <- kernels/__init__.py:38-49, the
+ *   vcg_node_op                            <- kernels/__init__.py:36-47, the
  *                                            per-node kernel API (pure.py /
  *                                            _native.pyx), one node per call
  */
@@ -214,7 +214,12 @@ int vcg_device_count(void);
 int vcg_set_device(int device);
 /* The calling thread's current device (-1 on error). */
 int vcg_get_device(void);
-/* Device time in ms of the last vcg_root_reduce phases etc. is in the structs. */
+/* Process teardown (call once, e.g. from atexit, after the calling program's
+ * solver threads have finished): waits for the device, then turns every later
+ * device-memory release into a no-op so that no CUDA call runs from static or
+ * thread-local destructors while the runtimes unload.  No reference
+ * counterpart (the reference holds no device state). */
+void vcg_shutdown(void);
 
 #ifdef __cplusplus
 }

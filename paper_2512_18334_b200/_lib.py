@@ -7,6 +7,7 @@ with ``VCG_ENODEV`` when no CUDA device is present.
 
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
 import subprocess
@@ -75,7 +76,7 @@ EXPORTS = (
     "vcg_graph_create", "vcg_graph_destroy", "vcg_graph_num_vertices", "vcg_graph_num_edges",
     "vcg_graph_download", "vcg_induced_subgraph", "vcg_greedy_bound", "vcg_root_reduce",
     "vcg_search", "vcg_node_op", "vcg_last_error", "vcg_device_count", "vcg_launch_count",
-    "vcg_set_device", "vcg_get_device", "vcg_expand",
+    "vcg_set_device", "vcg_get_device", "vcg_expand", "vcg_shutdown",
 )
 
 
@@ -111,10 +112,33 @@ def _load():
     lib.vcg_search.argtypes = [P, C.POINTER(SearchConfig_t), C.POINTER(SearchResult_t), P]
     lib.vcg_expand.argtypes = [P, C.POINTER(ExpandConfig_t), C.POINTER(ExpandResult_t), P, P, I64]
     lib.vcg_node_op.argtypes = [C.c_int, C.c_int, I64, P, P, P, I64, I64, I64, I64, P, I64, P]
+    lib.vcg_shutdown.restype = None
     return lib
 
 
 lib = _load()
+
+_exit_hooks = []
+
+
+def at_shutdown(fn) -> None:
+    """Run ``fn`` at interpreter exit before the library stops releasing
+    device memory (the solve_batch pool registers its shutdown here)."""
+    _exit_hooks.append(fn)
+
+
+@atexit.register
+def _shutdown() -> None:
+    # join the library's worker threads first, then make every later device
+    # release a no-op: objects finalised after this point (and thread-local
+    # contexts) leave their memory to the process exit, so no CUDA call runs
+    # while the CUDA runtimes tear down
+    for fn in reversed(_exit_hooks):
+        try:
+            fn()
+        except Exception:  # noqa: BLE001 -- best effort at exit
+            pass
+    lib.vcg_shutdown()
 
 
 def check(rc: int) -> None:

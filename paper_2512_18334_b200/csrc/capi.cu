@@ -49,19 +49,50 @@ static int fail(int code, const std::string& msg) {
       return fail(VCG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
   } while (0)
 
-// The dynamic shared-memory limit is a process-wide attribute of a kernel:
+// The dynamic shared-memory limit is a per-device attribute of a kernel:
 // concurrent solves (solve_batch threads) must only ever raise it, or one
-// thread's launch can fail after another lowered it.
+// thread's launch can fail after another lowered it.  Keyed by (device, fn)
+// so a process driving several GPUs raises it on each.
 static int raise_smem_limit(const void* fn, size_t bytes) {
   static std::mutex mu;
-  static std::map<const void*, size_t> cur;
+  static std::map<std::pair<int, const void*>, size_t> cur;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(mu);
-  size_t& c = cur[fn];
+  size_t& c = cur[{dev, fn}];
   if (bytes > c) {
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     c = bytes;
   }
   return 0;
+}
+
+// Device attributes of the calling thread's current device, cached per
+// thread (cudaGetDeviceProperties costs tens of ms per call).
+struct DevAttrs {
+  int dev = -1, sm_count = 0, smem_optin = 0;
+};
+static int dev_attrs(DevAttrs** out) {
+  static thread_local DevAttrs a;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (a.dev != dev) {
+    CK(cudaDeviceGetAttribute(&a.sm_count, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaDeviceGetAttribute(&a.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    a.dev = dev;
+  }
+  *out = &a;
+  return 0;
+}
+
+// Process teardown: once vcg_shutdown() ran (the Python binding calls it
+// from atexit, after its worker threads are joined) no device memory is
+// released any more -- the process exit reclaims it, and no CUDA call is
+// made from static / thread-local destructors while runtimes unload.
+static std::atomic<bool> g_shutdown{false};
+extern "C" void vcg_shutdown(void) {
+  if (g_shutdown.exchange(true)) return;
+  cudaDeviceSynchronize();
 }
 
 extern "C" const char* vcg_last_error(void) { return g_err.c_str(); }
@@ -138,6 +169,11 @@ struct DevBuf {
   ~DevBuf() { release(); }
   void release() {
     if (!p) return;
+    if (g_shutdown.load(std::memory_order_relaxed)) {  // teardown: the exit reclaims it
+      p = nullptr;
+      bytes = 0;
+      return;
+    }
     if (stream_ordered) cudaFreeAsync(p, cudaStreamPerThread);
     else cudaFree(p);
     p = nullptr;
@@ -178,12 +214,38 @@ struct vcg_graph {
 };
 
 // search buffers are reused across graphs and solves (grown on demand), one
-// set per host thread: the library is built with --default-stream
+// set per (host thread, device): the library is built with --default-stream
 // per-thread, so calls from different threads run on independent streams
-// and may overlap on the device (solve_batch)
+// and may overlap on the device (solve_batch).  Contexts are never freed:
+// when a thread exits, its contexts return to a per-device pool (no CUDA
+// call from a thread-local destructor) and the next thread reuses them.
+static std::mutex g_ctx_mu;
+static std::map<int, std::vector<SearchCtx*>>* g_ctx_pool = new std::map<int, std::vector<SearchCtx*>>();
+
+struct CtxHolder {
+  std::map<int, SearchCtx*> by_dev;
+  ~CtxHolder() {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    for (auto& kv : by_dev) (*g_ctx_pool)[kv.first].push_back(kv.second);
+  }
+};
+
 static SearchCtx& search_ctx() {
-  static thread_local SearchCtx ctx;  // released when its thread exits
-  return ctx;
+  static thread_local CtxHolder holder;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SearchCtx*& c = holder.by_dev[dev];
+  if (!c) {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    auto& pool = (*g_ctx_pool)[dev];
+    if (!pool.empty()) {
+      c = pool.back();
+      pool.pop_back();
+    } else {
+      c = new SearchCtx();
+    }
+  }
+  return *c;
 }
 
 extern "C" int vcg_graph_create(int64_t n, const int64_t* offsets, const int32_t* neighbors,
@@ -260,7 +322,7 @@ extern "C" int vcg_graph_download(const vcg_graph* g, int64_t* offsets, int32_t*
 }
 
 // ------------------------------------------------------------ compaction --
-// graph.py:112 induced_subgraph, on the device: flag -> scan (new ids) ->
+// graph.py:99 induced_subgraph, on the device: flag -> scan (new ids) ->
 // per-vertex surviving-neighbour counts -> scan (offsets) -> gather.
 
 __global__ void k_keep_flags(const int32_t* deg_or_null, const int64_t* keep_list, int64_t nkeep,
@@ -732,9 +794,9 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
     std::vector<int32_t> forced;
     // any-order callers (the solve path) get the order-free sweeps on an
     // on-chip workspace when it fits; the degrees then live at ws.p as int32
-    static int smem_optin = 0;
-    if (!smem_optin)
-      CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0));
+    DevAttrs* da = nullptr;
+    if (int r = dev_attrs(&da)) return r;
+    const int smem_optin = da->smem_optin;
     const long long fast_smem = ws_bytes<uint32_t>(n);
     const bool fast = (enabled & VCG_ROOT_ANY_ORDER) && fast_smem + 8192 <= smem_optin &&
                       !getenv("VCG_ROOT_ORDERED");
@@ -1079,15 +1141,9 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   SearchCtx& C = search_ctx();
   Tracer tr("search");
   const int n = (int)g->n;
-  int dev = 0;
-  CK(cudaGetDevice(&dev));
-  // cudaGetDeviceProperties costs tens of ms per call: cache two attributes
-  static thread_local int cached_dev = -1, sm_count = 0, smem_optin = 0;
-  if (cached_dev != dev) {
-    CK(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    cached_dev = dev;
-  }
+  DevAttrs* da = nullptr;
+  if (int r = dev_attrs(&da)) return r;
+  const int sm_count = da->sm_count, smem_optin = da->smem_optin;
 
   const bool auto_threads = cfg->threads <= 0;
   int threads = cfg->threads;

@@ -12,7 +12,7 @@
 
 namespace vcg {
 
-// preprocess.py:348 greedy_bound -> pure.py:306 greedy_cover: repeatedly take
+// preprocess.py:28 greedy_bound -> pure.py:306 greedy_cover: repeatedly take
 // the lowest-index vertex of maximum residual degree.
 //
 // Level form of the same pick sequence: with D the current maximum degree,

@@ -154,7 +154,7 @@ struct Worker {
   // arena: local ids follow the current graph's order, so every
   // lowest-index rule and tie-break of the reference is unchanged inside the
   // component, while the child's degree array, window and sweeps shrink
-  // from the parent's span to the component (graph.py:112 induced_subgraph,
+  // from the parent's span to the component (graph.py:99 induced_subgraph,
   // applied per component).  Writes the local degrees to dd[0, size).
   // Returns the subgraph's graph number (id + 1), 0 when the arena is full.
   __device__ int compact_component(int root, int size, int m2c, int lo, int hi, T* dd) {

@@ -115,7 +115,7 @@ class Stats:
 
 
 class RegistrySummary:
-    """Post-solve view of the device registry (registry.py:522-548 diagnostics)."""
+    """Post-solve view of the device registry (registry.py:198-224 diagnostics)."""
 
     def __init__(self, entries: int, violations: int | None):
         self.entries = entries
@@ -368,6 +368,10 @@ def solve_batch(graphs, configs) -> list[SolveResult]:
     global _BATCH_POOL
     if _BATCH_POOL is None or _BATCH_POOL._max_workers < k:
         # long-lived workers: each keeps its stream and pooled device buffers
+        # (a replaced pool's threads exit; their buffers go back to the
+        # library's per-device context pool)
+        if _BATCH_POOL is not None:
+            _BATCH_POOL.shutdown(wait=True)
         _BATCH_POOL = ThreadPoolExecutor(max_workers=k, thread_name_prefix="vcg-batch")
     dev = _lib.get_device()  # worker threads start on device 0: adopt the caller's
 
@@ -380,3 +384,13 @@ def solve_batch(graphs, configs) -> list[SolveResult]:
 
 
 _BATCH_POOL = None
+
+
+def _shutdown_pool() -> None:
+    global _BATCH_POOL
+    if _BATCH_POOL is not None:
+        _BATCH_POOL.shutdown(wait=True)
+        _BATCH_POOL = None
+
+
+_lib.at_shutdown(_shutdown_pool)

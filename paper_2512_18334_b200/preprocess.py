@@ -1,4 +1,4 @@
-"""Root reduction + compaction (mirror of vcsolver.preprocess, preprocess.py:321-468).
+"""Root reduction + compaction (mirror of vcsolver.preprocess, preprocess.py:28-148).
 
 The lightweight rules run to a fixpoint on the device, the crown rule's
 matching runs natively on the host, survivors are compacted into a fresh CSR
@@ -20,7 +20,7 @@ ROOT_RULE_KEYS = ("degree_one", "degree_two_triangle", "high_degree", "crown")
 
 
 def greedy_bound(g: StaticGraph, members: bool = False):
-    """preprocess.py:348 -- max-degree greedy cover size (optionally the picks)."""
+    """preprocess.py:28 -- max-degree greedy cover size (optionally the picks)."""
     if g.num_vertices == 0 or g.num_edges == 0:
         return (0, []) if members else 0
     out = np.zeros(g.num_vertices, dtype=np.int32) if members else None
@@ -33,7 +33,7 @@ def greedy_bound(g: StaticGraph, members: bool = False):
 
 
 def select_width(max_degree: int, override: int | None = None) -> int:
-    """preprocess.py:362 -- smallest supported width whose capacity fits."""
+    """preprocess.py:42 -- smallest supported width whose capacity fits."""
     if override is not None:
         if override not in SUPPORTED_WIDTHS:
             raise ValueError(
@@ -49,7 +49,7 @@ def select_width(max_degree: int, override: int | None = None) -> int:
 
 @dataclass
 class Preprocessed:
-    """preprocess.py:380 -- result of the root reduction pass."""
+    """preprocess.py:61 -- result of the root reduction pass."""
 
     graph: StaticGraph
     vertex_map: np.ndarray  # reduced id -> original id
@@ -69,7 +69,7 @@ def root_reduce(g: StaticGraph, enabled: bool = True, crown: bool = True,
                 bound: int | None = None, width_override: int | None = None,
                 need_greedy_original: bool = True, ordered: bool = True,
                 lazy_greedy: bool = False) -> Preprocessed:
-    """preprocess.py:397 root_reduce on the device.
+    """preprocess.py:77 root_reduce on the device.
 
     ``need_greedy_original=False`` (used by PVC solves, where the bound is k)
     skips the greedy cover of the input graph; ``greedy_original`` is then -1.

@@ -3,7 +3,7 @@
 Host-side data plumbing only (numpy): every generator returns a canonical
 ``(num_vertices, offsets, neighbors)`` CSR triple -- sorted neighbour slices,
 both directions, no self-loops or duplicates -- which is exactly the
-``StaticGraph`` layout of the reference (vcsolver/graph.py:69-133).
+``StaticGraph`` layout of the reference (vcsolver/graph.py:33-123).
 
 The five workloads (BASELINE.json ``configs``):
 
