@@ -1,24 +1,31 @@
-"""Benchmark: PVC yes/no pair on the 2,000-vertex random geometric graph
-(BASELINE.json configs[1]) -- time-to-solution and search-tree nodes/s.
+"""Benchmark: MVC time-to-solution on the 1M-vertex planted-cover graph
+(BASELINE.json configs[3], the config the metric's 1/2/4/8-GPU scaling is
+quoted on), with the other configs as secondary measurements.
 
-One step = the batch {PVC k=opt, PVC k=opt-1} through the package's public
-API (solve_batch: the two independent queries run concurrently, each with
-its own host thread, stream and half of the resident block slots; root
-reduction, compaction and the persistent search kernel all on the device).  `value` is whole-job search-tree nodes/s with the input CSR
-already resident in HBM; `e2e` repeats the step from host numpy buffers
-(upload, solve, result readback inside the timed region).
+One step = one ``solve(g, SolverConfig())`` MVC call through the package's
+public API on the planted1m instance: the grid-wide root fixpoint, crown,
+device compaction and (when anything is left) the persistent search kernel.
+``value`` is the time-to-solution with the input CSR already resident in
+HBM; ``e2e`` repeats the step from pinned host buffers (upload, solve,
+result readback inside the timed region).  ``other_configs`` holds
+configs[0]-[2] (er200 MVC, the rgg2000 PVC pair with its search-tree
+nodes/s, ba100k MVC).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
 N > 1 runs under torchrun, one rank per GPU; rank r solves its own seeded
-instance of the same shape (seed 1 + r: independent objects, weak scaling).
---impl reference times the reference algorithm's CPU implementation (the C
-restatement in oracle/, threaded, every host core) on the same workload.
+instance of the same shape (seed 1 + r: independent objects, weak scaling),
+and ``value`` is the max over ranks.  ``--impl reference`` times the
+reference algorithm's CPU implementation (the C restatement in oracle/, its
+threaded engine on every host core) on the same workload; that arm never
+imports the product package (the generators are loaded from synth.py by
+path), so no CUDA library is mapped into it.
 """
 
 from __future__ import annotations
 
 import argparse
+import importlib.util
 import json
 import os
 import statistics
@@ -31,19 +38,23 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "MVC time-to-solution (s) & search-tree nodes/s at 1/2/4/8 B200 vs CPU ref"
-WORKLOAD = "PVC yes/no pair (k=opt, k=opt-1) on random geometric graph n=2000 r=0.027"
+WORKLOAD = ("configs[3]: MVC on a 1M-vertex sparse synthetic graph (planted cover of 50,000 "
+            "plus noise)")
+GENERATOR = ("synth.planted(n=1_000_000, cover=50_000, cc=1.0, oo=0.3, seed=1+rank): every "
+             "outside vertex attaches to 2-3 random cover vertices, 50,000 random cover-cover "
+             "edges, 300,000 random outside-outside noise edges; the reference's root rules "
+             "resolve it completely (no search-tree nodes), so its time-to-solution is the "
+             "root pipeline's")
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--mode", default="weak", choices=["weak", "strong"],
-                    help="weak: each rank solves its own seeded instance; strong: all ranks "
-                         "solve instance 1 together (root-subtree partition + bound exchange)")
+    ap.add_argument("--no-other-configs", action="store_true")
     return ap.parse_args()
 
 
@@ -52,10 +63,26 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def instance(seed):
-    from paper_2512_18334_b200 import synth
+def load_synth():
+    """synth.py by path: plain numpy generators, no package import."""
+    spec = importlib.util.spec_from_file_location(
+        "vc_synth", os.path.join(ROOT, "paper_2512_18334_b200", "synth.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
 
-    return synth.rgg(2000, 0.027, seed)
+
+def instance(seed):
+    return load_synth().planted(1_000_000, 50_000, seed)
+
+
+def config(world, n, m):
+    """Identical in both arms (same N)."""
+    return {"workload": WORKLOAD, "generator": GENERATOR, "n": n, "m": m,
+            "parallelism": (f"{world} GPUs, independent seeded instances (weak scaling)"
+                            if world > 1 else "1 GPU"),
+            "l2": "inputs (31 MB CSR) well below L2 size: L2 flushed between timed steps "
+                  "(512 MiB write outside the timed region)"}
 
 
 # --------------------------------------------------------------- clocks ----
@@ -134,6 +161,8 @@ class ClockSampler:
 # ------------------------------------------------------------ reference ----
 
 def run_reference(args):
+    """The reference algorithm's CPU implementation (oracle/, threaded engine
+    on every host core) on the same workload; rank 0 only."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -141,34 +170,40 @@ def run_reference(args):
 
     n, off, nbr = instance(1)
     cores = os.cpu_count() or 1
-    opt = oracle.solve(n, off, nbr, deterministic=True)["cover_size"]
+    opt = None
 
     def step():
-        nodes = 0
-        for k, want in ((opt, True), (opt - 1, False)):
-            r = oracle.solve(n, off, nbr, mode="pvc", k=k, workers=cores)
-            assert r["found"] == want, (k, r["found"])
-            nodes += r["stats"]["tree_nodes_visited"]
-        return nodes
+        nonlocal opt
+        t = time.perf_counter()
+        r = oracle.solve(n, off, nbr, workers=cores)
+        dt = time.perf_counter() - t
+        if opt is None:
+            opt = r["cover_size"]
+        elif r["cover_size"] != opt:
+            raise RuntimeError("reference arm: unstable answer")
+        return dt, r["stats"]["tree_nodes_visited"]
 
     for _ in range(args.warmup):
         step()
-    nodes, t0 = 0, time.perf_counter()
+    total, nodes = 0.0, 0
     for _ in range(args.steps):
-        nodes += step()
-    dt = time.perf_counter() - t0
-    value = nodes / dt
+        dt, nd = step()
+        total += dt
+        nodes += nd
+    tts = total / args.steps
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "nodes/s",
+        "impl": "reference", "metric": METRIC, "value": tts, "unit": "s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int32", "data": "synthetic (seeded RGG)",
-        "config": {"workload": WORKLOAD, "seed": 1, "opt": opt},
-        "cpu_baseline": {"value": value, "unit": "nodes/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} PVC pairs on rgg2000 seed 1 "
-                                   f"(oracle/vc_oracle.c threaded engine, {cores} threads)"},
-        "e2e": {"value": value, "unit": "nodes/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "ms_per_step": tts * 1e3, "time_to_solution_s": tts, "nodes_per_s": nodes / total,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (seeded planted-cover graph, seed 1)",
+        "config": config(world, n, int(off[-1]) // 2),
+        "answer": {"mvc": opt},
+        "cpu_baseline": {"value": tts, "unit": "s", "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} MVC solves of planted1m seed 1 "
+                                   f"(oracle/vc_oracle.c, threaded engine, {cores} threads; "
+                                   f"the root pipeline is sequential)"},
+        "e2e": {"value": tts, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -180,29 +215,80 @@ def cpu_baseline_sample():
     import oracle
 
     n, off, nbr = instance(1)
-    opt = oracle.solve(n, off, nbr, deterministic=True)["cover_size"]
-    nodes, reps, t0 = 0, 0, time.perf_counter()
+    reps, t0 = 0, time.perf_counter()
     while reps < 5 and (reps == 0 or time.perf_counter() - t0 < 10.0):
-        for k in (opt, opt - 1):
-            nodes += oracle.solve(n, off, nbr, mode="pvc", k=k, deterministic=True)[
-                "stats"]["tree_nodes_visited"]
+        oracle.solve(n, off, nbr, deterministic=True)
         reps += 1
     dt = time.perf_counter() - t0
-    return {"value": nodes / dt, "unit": "nodes/s", "cores": 1, "kind": "port",
-            "sample": f"{reps} PVC pairs (k=opt, opt-1) on rgg2000 seed 1, single-thread "
-                      f"C restatement (oracle/vc_oracle.c), {dt:.1f} s",
-            "ms_per_pair": dt / reps * 1e3}
+    return {"value": dt / reps, "unit": "s", "cores": 1, "kind": "port",
+            "sample": f"{reps} MVC solves of planted1m seed 1, single-thread C restatement "
+                      f"(oracle/vc_oracle.c), {dt:.1f} s"}
 
 
 def load_traffic():
-    """dram bytes per search-kernel launch from the committed ncu capture."""
-    p = os.path.join(ROOT, "profiles", "search_kernel_ncu.json")
+    """dram bytes per root-kernel launch from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "r02_root_grid_ncu.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_launch"), d
+        return d.get("dram_bytes_per_launch"), os.path.relpath(p, ROOT)
     except (OSError, ValueError):
         return None, None
+
+
+def other_configs(vc, torch, reps=5):
+    """configs[0]-[2] through the public API, device-timed with CUDA events."""
+    synth = load_synth()
+    out = {}
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), r
+
+    for key, name, gen in (("configs[0]", "er200 MVC", lambda: synth.er(200, 4.0, 1)),
+                           ("configs[2]", "ba100k MVC", lambda: synth.ba(100_000, 3, 1))):
+        n, off, nbr = gen()
+        g = vc.StaticGraph(n, off, nbr)
+        vc.solve(g)
+        ms = []
+        for _ in range(reps):
+            t, r = timed(lambda: vc.solve(g))
+            ms.append(t)
+        out[key] = {"workload": name, "mvc": r.cover_size,
+                    "time_to_solution_s": statistics.median(ms) * 1e-3,
+                    "tree_nodes": r.stats.tree_nodes_visited}
+    n, off, nbr = synth.rgg(2000, 0.027, 1)
+    g = vc.StaticGraph(n, off, nbr)
+    opt = vc.solve(g).cover_size
+    cfgs = [vc.SolverConfig(mode="pvc", k=opt), vc.SolverConfig(mode="pvc", k=opt - 1)]
+    vc.solve_batch(g, cfgs)
+    pair_ms, pair_nodes, single = [], 0, {opt: [], opt - 1: []}
+    for _ in range(reps * 4):
+        t, rs = timed(lambda: vc.solve_batch(g, cfgs))
+        assert rs[0].found and not rs[1].found
+        pair_ms.append(t)
+        pair_nodes += sum(r.stats.tree_nodes_visited for r in rs)
+    for k in single:
+        for _ in range(reps * 2):
+            t, r = timed(lambda: vc.solve(g, vc.SolverConfig(mode="pvc", k=k)))
+            single[k].append((t, r.stats.tree_nodes_visited))
+    out["configs[1]"] = {
+        "workload": "PVC yes/no pair (k=opt, opt-1) on random geometric graph n=2000 r=0.027",
+        "opt": opt,
+        "pair_solve_batch_s": statistics.median(pair_ms) * 1e-3,
+        "pair_nodes_per_s": pair_nodes / (sum(pair_ms) * 1e-3),
+        "single_query_time_to_solution_s": {
+            f"k={k}": statistics.median(t for t, _ in v) * 1e-3 for k, v in single.items()},
+        "single_query_nodes_per_s": {
+            f"k={k}": sum(nd for _, nd in v) / (sum(t for t, _ in v) * 1e-3)
+            for k, v in single.items()},
+    }
+    return out
 
 
 def run_b200(args):
@@ -210,8 +296,6 @@ def run_b200(args):
     import torch
 
     rank, world, local = dist_env()
-    # one rank per GPU; ranks only share a GPU when there are fewer GPUs than
-    # ranks (a functional test of the multi-process path), then over gloo
     ndev = torch.cuda.device_count()
     device = local % ndev
     torch.cuda.set_device(device)
@@ -224,111 +308,84 @@ def run_b200(args):
 
         if world <= ndev:
             dist.init_process_group("nccl", device_id=torch.device("cuda", device))
-        else:
+        else:  # fewer GPUs than ranks: a functional run of the multi-process path
             dist.init_process_group("gloo")
-    strong = args.mode == "strong" and world > 1
-    n, off, nbr = instance(1 if strong else 1 + rank)
+    n, off, nbr = instance(1 + rank)
+    m = int(off[-1]) // 2
     g = vc.StaticGraph(n, off, nbr)
-    opt = vc.solve(g, vc.SolverConfig()).cover_size  # untimed: defines the pair
-    if strong:
-        from paper_2512_18334_b200.distributed import solve_distributed
+    opt = vc.solve(g, vc.SolverConfig()).cover_size  # untimed: the answer every step must give
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    # pinned host copies of the input for the end-to-end leg
+    off_pin = torch.empty(len(off), dtype=torch.int64, pin_memory=True).numpy()
+    nbr_pin = torch.empty(len(nbr), dtype=torch.int32, pin_memory=True).numpy()
+    off_pin[:] = off
+    nbr_pin[:] = nbr
 
     def barrier():
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    def pair(graph):
-        # the step's two PVC queries are independent: solve_batch runs them
-        # concurrently (own host thread, stream and half the block slots each)
-        nodes = kms = 0.0
-        ks = ((opt, True), (opt - 1, False))
-        if strong:
-            rs = [solve_distributed(graph, vc.SolverConfig(mode="pvc", k=k)) for k, _ in ks]
-        else:
-            rs = vc.solve_batch(graph, [vc.SolverConfig(mode="pvc", k=k) for k, _ in ks])
-        for (k, want), r in zip(ks, rs):
-            if r.found != want:
-                raise RuntimeError(f"PVC k={k}: found={r.found}, expected {want}")
-            nodes += r.stats.tree_nodes_visited
-            kms += r.search_ms
-        return nodes, kms
-
-    # per-solve record traffic comes from the search result; wrap solve once
-    from paper_2512_18334_b200 import engine as _eng
-
-    rec = {"bytes": 0, "kernel_ms": 0.0, "launches": 0}
-    orig = _eng.run_search
-
-    rec_lock = threading.Lock()  # solve_batch calls it from worker threads
-
-    def run_search_probe(*a, **kw):
-        out = orig(*a, **kw)
-        res = out[0]
-        with rec_lock:
-            rec["bytes"] += (res.records_loaded + res.records_stored) * res.slot_bytes
-            rec["kernel_ms"] += res.kernel_ms
-            rec["launches"] += 1
-        return out
-
-    _eng.run_search = run_search_probe
+    def step(graph):
+        r = vc.solve(graph, vc.SolverConfig())
+        if r.cover_size != opt or not r.exact:
+            raise RuntimeError(f"MVC {r.cover_size}, expected {opt}")
+        return r
 
     clk = ClockSampler(device).__enter__()  # running before the timed region
     for _ in range(args.warmup):
-        pair(g)
+        step(g)
     barrier()
-    rec.update(bytes=0, kernel_ms=0.0, launches=0)
     l0 = _lib.launch_count()
-    total_ms, nodes = 0.0, 0.0
+    total_ms, nodes = 0.0, 0
+    kern_ms, kern_launches, kern_scans, kind = 0.0, 0, 0, None
     clk.mark_start()
     for _ in range(args.steps):
         flush.zero_()  # L2 flush between timed steps (outside the events)
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        nd, _ = pair(g)
+        r = step(g)
         e1.record()
         torch.cuda.synchronize()
         total_ms += e0.elapsed_time(e1)
-        nodes += nd
+        nodes += r.stats.tree_nodes_visited
+        kern_ms += r.root_kernel.get("ms", 0.0)
+        kern_launches += r.root_kernel.get("launches", 0)
+        kern_scans += r.root_kernel.get("scans", 0)
+        kind = r.root_kernel.get("kind")
     clk.mark_end()
-    clk.__exit__(None, None, None)
     launches = _lib.launch_count() - l0
-    search_bytes, search_ms, search_launches = rec["bytes"], rec["kernel_ms"], rec["launches"]
 
-    # e2e: from host numpy buffers every step (upload + solve + readback)
-    h2d = (n + 1) * 4 + len(nbr) * 4
-    e2e_ms, e2e_nodes = 0.0, 0.0
+    # e2e: from pinned host buffers every step (upload + solve + readback)
+    e2e_ms = 0.0
     for _ in range(args.steps):
         flush.zero_()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        gh = vc.StaticGraph(n, np.array(off), np.array(nbr))
-        nd, _ = pair(gh)
+        gh = vc.StaticGraph(n, off_pin, nbr_pin)
+        r = step(gh)
         e1.record()
         torch.cuda.synchronize()
         e2e_ms += e0.elapsed_time(e1)
-        e2e_nodes += nd
-    # per solve the host reads back the reduced CSR + vertex map + forced ids
-    # (int32), the components histogram (int64) and the result structs
-    rg = vc.root_reduce(g, bound=opt).graph
-    d2h = 2 * ((rg.num_vertices + 1) * 4 + len(rg.neighbors) * 4 + rg.num_vertices * 4
-               + n * 4 + (rg.num_vertices + 2) * 8 + 512)
+        del gh
+    clk.__exit__(None, None, None)
+    h2d = off_pin.nbytes + nbr_pin.nbytes
+    rn, rm = r.stats.root_vertices_after, 0
+    pre_forced = len(r.forced_ids)
+    # per solve the host reads back the forced ids, the vertex map, the
+    # reduced CSR (int32) and the result structs
+    d2h = 4 * pre_forced + 8 * rn + 4 * (rn + 1) + 8 * rm + 512
 
-    t = torch.tensor([total_ms, nodes, e2e_ms, e2e_nodes], dtype=torch.float64,
+    t = torch.tensor([total_ms, e2e_ms, nodes], dtype=torch.float64,
                      device="cuda" if world <= ndev else "cpu")
     if world > 1:
         tmax = t.clone()
         torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
         tsum = t.clone()
         torch.distributed.all_reduce(tsum, op=torch.distributed.ReduceOp.SUM)
-        total_ms, e2e_ms = float(tmax[0]), float(tmax[2])
-        if strong:  # solve_distributed already reports whole-job node counts
-            nodes, e2e_nodes = float(t[1]), float(t[3])
-        else:
-            nodes, e2e_nodes = float(tsum[1]), float(tsum[3])
+        total_ms, e2e_ms, nodes = float(tmax[0]), float(tmax[1]), float(tsum[2])
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -340,47 +397,53 @@ def run_b200(args):
             peaks = json.load(f)
     except (OSError, ValueError):
         pass
-    peak = peaks.get("hbm_gbs") or 6650.0
-    peak_src = "measured" if peaks.get("hbm_gbs") else "fallback"
-    per_launch_bytes = search_bytes / max(search_launches, 1)
-    per_launch_ms = search_ms / max(search_launches, 1)
-    achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms else 0.0
-    traffic, _ = load_traffic()
+    peak = peaks.get("hbm_gbs") or 7672.0
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks.get("hbm_gbs") else \
+        "fallback (B200_PROFILING.md)"
+    # algorithmic bytes of one root-fixpoint launch ("Kernels"):
+    # the CSR read once (int32 offsets + neighbours), the int32 degree array
+    # written once and read once per grid-wide scan
+    per_launch_scans = kern_scans / max(kern_launches, 1)
+    alg_bytes = 4 * (n + 1) + 8 * m + 4 * n * (per_launch_scans + 1)
+    launch_ms = kern_ms / max(kern_launches, 1)
+    achieved = alg_bytes / (launch_ms * 1e-3) / 1e9 if launch_ms else 0.0
+    traffic, traffic_src = load_traffic()
+    tts = total_ms / args.steps * 1e-3
     line = {
         "metric": METRIC,
-        "value": nodes / (total_ms * 1e-3),
-        "unit": "nodes/s",
+        "value": tts,
+        "unit": "s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps,
-        "time_to_solution_s": total_ms / args.steps * 1e-3,
-        "higher_is_better": True,
-        "scaling": "strong" if strong else "weak",
+        "time_to_solution_s": tts,
+        "nodes_per_s": nodes / (total_ms * 1e-3),
+        "higher_is_better": False,
+        "scaling": "weak",
         "vs_baseline": None,
         "dtype": "int32",
-        "data": "synthetic (seeded random geometric graph, seed 1)" if strong else
-                "synthetic (seeded random geometric graph, seed 1 + rank)",
-        "config": {"workload": WORKLOAD, "opt": opt, "n": n, "m": len(nbr) // 2,
-                   "parallelism": (f"{world} GPUs on one instance (root-subtree partition, "
-                                   "NCCL MIN all-reduce of the bound)") if strong else
-                                  f"dp{world} (independent instances)",
-                   "l2": "flushed between timed steps (512 MiB write)"},
-        "e2e": {"value": e2e_nodes / (e2e_ms * 1e-3), "unit": "nodes/s",
+        "data": "synthetic (seeded planted-cover graph, seed 1 + rank)",
+        "config": config(world, n, m),
+        "answer": {"mvc": opt, "tree_nodes_per_solve": nodes / args.steps / world,
+                   "root_forced": pre_forced, "reduced_vertices": rn},
+        "e2e": {"value": e2e_ms / args.steps * 1e-3, "unit": "s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_ms / args.steps},
+                "ms_per_step": e2e_ms / args.steps,
+                "input": "pinned host numpy arrays (int64 offsets, int32 neighbours)"},
         "gpu_launches": launches,
         "roofline": {
-            "bound": "hbm", "kernel": "search_kernel", "achieved": achieved, "peak": peak,
-            "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic,
-            "algorithmic_bytes_per_launch": per_launch_bytes,
-            "launch_ms": per_launch_ms,
-            # summed over the step's two concurrent searches: may exceed 1
-            "kernel_share_of_step": search_ms / total_ms if total_ms else None,
+            "bound": "hbm", "kernel": f"k_root_grid (root fixpoint, kind={kind})",
+            "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+            "algorithmic_bytes_per_launch": alg_bytes, "scans_per_launch": per_launch_scans,
+            "launch_ms": launch_ms, "launches_per_step": kern_launches / args.steps,
+            "kernel_share_of_step": kern_ms / total_ms if total_ms else None,
         },
         "clocks": clk.summary(),
     }
+    if not args.no_other_configs:
+        line["other_configs"] = other_configs(vc, torch)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample()
     print(json.dumps(line), flush=True)

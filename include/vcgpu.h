@@ -45,6 +45,14 @@ typedef struct vcg_graph vcg_graph;
  * sorted slices, symmetric) to the current device. */
 int vcg_graph_create(int64_t n, const int64_t* offsets, const int32_t* neighbors,
                      vcg_graph** out);
+/* Same, without copying the host arrays: the graph keeps pointers to
+ * `offsets` / `neighbors` as its host view (the root pipeline's host-side
+ * crown and greedy read them), so the caller must keep both alive and
+ * unchanged until vcg_graph_destroy.  Uploads from pinned buffers run at
+ * full PCIe speed.  (graph.py:33 StaticGraph: the Python mirror passes its
+ * own arrays and holds them for the handle's lifetime.) */
+int vcg_graph_create_borrowed(int64_t n, const int64_t* offsets, const int32_t* neighbors,
+                              vcg_graph** out);
 int vcg_graph_destroy(vcg_graph* g);
 int64_t vcg_graph_num_vertices(const vcg_graph* g);
 int64_t vcg_graph_num_edges(const vcg_graph* g);
@@ -69,6 +77,14 @@ typedef struct {
   int64_t max_degree_reduced;
   int64_t rule_counts[4]; /* degree_one, degree_two_triangle, high_degree, crown */
   double seconds[3];      /* device reduction, crown, compaction */
+  /* device time of the rule kernels (CUDA events on the calling thread's
+   * stream), their launches, grid-wide scans of the degree array, and the
+   * kernel kind (0 none, 1 single block on chip, 2 single block in HBM,
+   * 3 grid-wide cooperative) */
+  double kernel_ms;
+  int64_t kernel_launches;
+  int64_t kernel_scans;
+  int64_t kernel_kind;
 } vcg_preprocessed;
 
 /* `enabled` flags of vcg_root_reduce: bit 0 applies the rules; with

@@ -29,6 +29,8 @@ class Preprocessed_t(C.Structure):
         ("n_reduced", I64), ("m_reduced", I64), ("forced_count", I64),
         ("greedy_original", I64), ("greedy_reduced", I64), ("max_degree_reduced", I64),
         ("rule_counts", I64 * 4), ("seconds", C.c_double * 3),
+        ("kernel_ms", C.c_double), ("kernel_launches", I64), ("kernel_scans", I64),
+        ("kernel_kind", I64),
     ]
 
 
@@ -73,7 +75,7 @@ PHASES = ("idle", "load", "reduce", "label", "split", "select", "exclude", "incl
 
 
 EXPORTS = (
-    "vcg_graph_create", "vcg_graph_destroy", "vcg_graph_num_vertices", "vcg_graph_num_edges",
+    "vcg_graph_create", "vcg_graph_create_borrowed", "vcg_graph_destroy", "vcg_graph_num_vertices", "vcg_graph_num_edges",
     "vcg_graph_download", "vcg_induced_subgraph", "vcg_greedy_bound", "vcg_root_reduce",
     "vcg_search", "vcg_node_op", "vcg_last_error", "vcg_device_count", "vcg_launch_count",
     "vcg_set_device", "vcg_get_device", "vcg_expand", "vcg_shutdown",
@@ -101,6 +103,7 @@ def _load():
     lib.vcg_graph_num_edges.restype = I64
     lib.vcg_launch_count.restype = I64
     lib.vcg_graph_create.argtypes = [I64, P, P, C.POINTER(P)]
+    lib.vcg_graph_create_borrowed.argtypes = [I64, P, P, C.POINTER(P)]
     lib.vcg_graph_destroy.argtypes = [P]
     lib.vcg_graph_num_vertices.argtypes = [P]
     lib.vcg_graph_num_edges.argtypes = [P]

@@ -19,6 +19,7 @@
 
 #include "../../include/vcgpu.h"
 #include "host_algos.h"
+#include "root_grid.cuh"
 #include "search.cuh"
 #include "warp_solve.cuh"
 
@@ -201,16 +202,24 @@ struct SearchCtx {
   DevBuf stacks, qseq, qdata, qctl, reg, ctl, hist, gws, wbits, wcount, bseq, bdata, bctl, sg, arena;
   // root pipeline / compaction / expansion scratch, reused across calls
   // (per-call cudaMalloc/cudaFree of tens of MB costs milliseconds, with outliers)
-  DevBuf r_flag, r_ws, r_out, r_ret, c_newid, c_cnt, c_vmap, c_tmp, x_ws, x_fifo, x_out;
+  DevBuf r_flag, r_ws, r_out, r_ret, r_gctl, c_newid, c_cnt, c_vmap, c_tmp, x_ws, x_fifo, x_out;
 };
 
 struct vcg_graph {
   int64_t n = 0;
   int64_t m2 = 0;  // 2 * edges
-  std::vector<int64_t> h_off;
-  std::vector<int32_t> h_nbr;
+  // host view of the CSR (the reference's StaticGraph is host data): owned
+  // copies, or the caller's arrays for a borrowed graph
+  const int64_t* hoff = nullptr;
+  const int32_t* hnbr = nullptr;
+  std::vector<int64_t> own_off;
+  std::vector<int32_t> own_nbr;
   DevBuf d_off{true};  // int32[n+1]
   DevBuf d_nbr{true};  // int32[2m]
+  void adopt_owned() {
+    hoff = own_off.data();
+    hnbr = own_nbr.data();
+  }
 };
 
 // search buffers are reused across graphs and solves (grown on demand), one
@@ -248,26 +257,47 @@ static SearchCtx& search_ctx() {
   return *c;
 }
 
-extern "C" int vcg_graph_create(int64_t n, const int64_t* offsets, const int32_t* neighbors,
-                                vcg_graph** out) {
+__global__ void k_narrow_offsets(const int64_t* off64, int64_t count, int32_t* off32) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    off32[i] = (int32_t)off64[i];
+}
+
+// Upload: neighbours straight from the caller's buffer (fast when it is
+// pinned), offsets as int64 into a pooled staging buffer and narrowed to
+// int32 on the device (no host pass over the offsets).
+static int graph_create_impl(int64_t n, const int64_t* offsets, const int32_t* neighbors,
+                             bool borrow, vcg_graph** out) {
   if (int r = need_device()) return r;
   if (n < 0 || !offsets || !out) return fail(VCG_EINVAL, "bad arguments");
   int64_t m2 = offsets[n];
   if (m2 >= (int64_t)1 << 31) return fail(VCG_EINVAL, "graph too large for int32 CSR offsets");
+  if (m2 && !neighbors) return fail(VCG_EINVAL, "bad arguments");
   auto* g = new vcg_graph();
   g->n = n;
   g->m2 = m2;
-  g->h_off.assign(offsets, offsets + n + 1);
-  g->h_nbr.assign(neighbors, neighbors + m2);
-  std::vector<int32_t> off32(n + 1);
-  for (int64_t i = 0; i <= n; ++i) off32[i] = (int32_t)offsets[i];
-  if (g->d_off.ensure((n + 1) * 4) || g->d_nbr.ensure(m2 * 4 + 4)) {
+  if (borrow) {
+    g->hoff = offsets;
+    g->hnbr = neighbors;
+  } else {
+    g->own_off.assign(offsets, offsets + n + 1);
+    g->own_nbr.assign(neighbors, neighbors + m2);
+    g->adopt_owned();
+  }
+  DevBuf off64{true};
+  if (g->d_off.ensure((n + 1) * 4) || g->d_nbr.ensure(m2 * 4 + 4) || off64.ensure((n + 1) * 8)) {
     delete g;
     return VCG_ERESOURCE;
   }
-  cudaMemcpy(g->d_off.p, off32.data(), (n + 1) * 4, cudaMemcpyHostToDevice);
-  if (m2) cudaMemcpy(g->d_nbr.p, neighbors, m2 * 4, cudaMemcpyHostToDevice);
-  cudaError_t e = cudaGetLastError();
+  cudaMemcpyAsync(off64.p, offsets, (n + 1) * 8, cudaMemcpyHostToDevice, cudaStreamPerThread);
+  if (m2)
+    cudaMemcpyAsync(g->d_nbr.p, neighbors, m2 * 4, cudaMemcpyHostToDevice, cudaStreamPerThread);
+  COUNT_LAUNCH(1);
+  k_narrow_offsets<<<(int)std::min<int64_t>((n + 256) / 256, 148 * 8), 256>>>(
+      off64.as<int64_t>(), n + 1, g->d_off.as<int32_t>());
+  off64.release();  // stream-ordered: freed after the narrowing kernel
+  cudaError_t e = cudaStreamSynchronize(cudaStreamPerThread);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     delete g;
     return fail(VCG_ECUDA, cudaGetErrorString(e));
@@ -276,11 +306,23 @@ extern "C" int vcg_graph_create(int64_t n, const int64_t* offsets, const int32_t
   return 0;
 }
 
+extern "C" int vcg_graph_create(int64_t n, const int64_t* offsets, const int32_t* neighbors,
+                                vcg_graph** out) {
+  return graph_create_impl(n, offsets, neighbors, false, out);
+}
+
+extern "C" int vcg_graph_create_borrowed(int64_t n, const int64_t* offsets,
+                                         const int32_t* neighbors, vcg_graph** out) {
+  return graph_create_impl(n, offsets, neighbors, true, out);
+}
+
 // Host compaction of the survivors (deg > 0) of a graph whose final degree
 // array is on the host: same order and relabelling as compact_flagged, one
 // upload instead of the device path's scan / count / gather round trips
 // (used by the root pipeline for graphs up to kHostCompactMax vertices).
-static constexpr int kHostCompactMax = 1 << 17;
+// Larger graphs (and every graph under VCG_DEVICE_COMPACT=1, the parity
+// tests' knob) compact on the device.
+static constexpr int kHostCompactMax = 1 << 14;
 
 static int compact_host(const vcg_graph* g, const int32_t* deg, vcg_graph** out,
                         std::vector<int64_t>* vmap_host) {
@@ -296,8 +338,8 @@ static int compact_host(const vcg_graph* g, const int32_t* deg, vcg_graph** out,
   std::vector<int32_t> nbr;
   off.reserve(nk + 1);
   for (int64_t v : vm) {
-    for (int64_t j = g->h_off[v]; j < g->h_off[v + 1]; ++j) {
-      const int32_t x = g->h_nbr[j];
+    for (int64_t j = g->hoff[v]; j < g->hoff[v + 1]; ++j) {
+      const int32_t x = g->hnbr[j];
       if (deg[x] > 0) nbr.push_back(newid[x]);
     }
     off.push_back((int64_t)nbr.size());
@@ -316,8 +358,8 @@ extern "C" int64_t vcg_graph_num_edges(const vcg_graph* g) { return g ? g->m2 / 
 extern "C" int vcg_graph_download(const vcg_graph* g, int64_t* offsets, int32_t* neighbors) {
   if (!g) return fail(VCG_EINVAL, "null graph");
   // the host mirror is built together with the device CSR (create/compaction)
-  std::copy(g->h_off.begin(), g->h_off.end(), offsets);
-  std::copy(g->h_nbr.begin(), g->h_nbr.end(), neighbors);
+  std::copy(g->hoff, g->hoff + g->n + 1, offsets);
+  std::copy(g->hnbr, g->hnbr + g->m2, neighbors);
   return 0;
 }
 
@@ -441,10 +483,11 @@ static int compact_flagged(const vcg_graph* g, DevBuf& flag, vcg_graph** out,
   // host mirror of the compacted CSR (the reference's StaticGraph is host data)
   std::vector<int32_t> off32(nk + 1), vm(nk);
   CK(cudaMemcpy(off32.data(), r->d_off.p, (size_t)(nk + 1) * 4, cudaMemcpyDeviceToHost));
-  r->h_off.resize(nk + 1);
-  for (int i = 0; i <= nk; ++i) r->h_off[i] = off32[i];
-  r->h_nbr.resize(m2);
-  if (m2) CK(cudaMemcpy(r->h_nbr.data(), r->d_nbr.p, (size_t)m2 * 4, cudaMemcpyDeviceToHost));
+  r->own_off.resize(nk + 1);
+  for (int i = 0; i <= nk; ++i) r->own_off[i] = off32[i];
+  r->own_nbr.resize(m2);
+  if (m2) CK(cudaMemcpy(r->own_nbr.data(), r->d_nbr.p, (size_t)m2 * 4, cudaMemcpyDeviceToHost));
+  r->adopt_owned();
   if (nk) CK(cudaMemcpy(vm.data(), vmap.p, (size_t)nk * 4, cudaMemcpyDeviceToHost));
   if (vmap_host) vmap_host->assign(vm.begin(), vm.end());
   *out = r;
@@ -473,7 +516,7 @@ extern "C" int vcg_induced_subgraph(const vcg_graph* g, const int64_t* keep, int
 
 extern "C" int vcg_greedy_bound(const vcg_graph* g, int32_t* members, int64_t* size) {
   if (!g || !size) return fail(VCG_EINVAL, "bad arguments");
-  *size = greedy_cover_host(g->n, g->h_off.data(), g->h_nbr.data(), members);
+  *size = greedy_cover_host(g->n, g->hoff, g->hnbr, members);
   return 0;
 }
 
@@ -741,7 +784,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
   if (has_bound != 1)
     greedy_thr = std::thread([&]() {
       greedy_orig =
-          greedy_cover_host(g->n, g->h_off.data(), g->h_nbr.data(), nullptr, &greedy_cancel);
+          greedy_cover_host(g->n, g->hoff, g->hnbr, nullptr, &greedy_cancel);
     });
   struct JoinGuard {
     std::thread& t;
@@ -770,13 +813,28 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
     if (ws.ensure(ws_total<uint32_t>(n)) || dout.ensure((size_t)(2 * n + 4) * 4) ||
         dret.ensure(256))
       return VCG_ERESOURCE;
-    NodeWs<uint32_t> layout = {};
-    (void)layout;
+    // any-order callers (the solve path) get the order-free sweeps on an
+    // on-chip workspace when it fits; larger graphs run the grid-wide
+    // cooperative kernel (root_grid.cu); the degrees live at ws.p as int32
+    DevAttrs* da = nullptr;
+    if (int r = dev_attrs(&da)) return r;
+    const int smem_optin = da->smem_optin;
+    const long long fast_smem = ws_bytes<uint32_t>(n);
+    // VCG_ROOT_GRID=1 forces the grid-wide kernel (tests), =0 the single-block ones
+    const char* grid_env = getenv("VCG_ROOT_GRID");
+    const bool on_chip = fast_smem + 8192 <= smem_optin;
+    const bool fast = (enabled & VCG_ROOT_ANY_ORDER) && on_chip && !getenv("VCG_ROOT_ORDERED") &&
+                      !(grid_env && atoi(grid_env) == 1);
+    const bool use_grid = !fast && (grid_env ? atoi(grid_env) == 1 : !on_chip);
+    if (use_grid && X.r_gctl.ensure(root_grid_ctl_bytes())) return VCG_ERESOURCE;
+    if (fast)
+      if (int r = raise_smem_limit((const void*)k_root_fixpoint_fast, (size_t)fast_smem)) return r;
+    info->kernel_kind = use_grid ? 3 : fast ? 1 : 2;
     int lo = 0, hi = n - 1;
-    {
+    if (!use_grid) {  // the single-block kernels take the initial live window
       int l = -1, h = -1;
       for (int v = 0; v < n; ++v)
-        if (g->h_off[v + 1] > g->h_off[v]) {
+        if (g->hoff[v + 1] > g->hoff[v]) {
           if (l < 0) l = v;
           h = v;
         }
@@ -788,20 +846,15 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
         hi = h;
       }
     }
-    std::vector<int32_t> hdeg(n);
+    std::vector<int32_t> hdeg;  // host copy of the degrees (crown / host compaction)
     int first = 1;
     int pos = 0;
     std::vector<int32_t> forced;
-    // any-order callers (the solve path) get the order-free sweeps on an
-    // on-chip workspace when it fits; the degrees then live at ws.p as int32
-    DevAttrs* da = nullptr;
-    if (int r = dev_attrs(&da)) return r;
-    const int smem_optin = da->smem_optin;
-    const long long fast_smem = ws_bytes<uint32_t>(n);
-    const bool fast = (enabled & VCG_ROOT_ANY_ORDER) && fast_smem + 8192 <= smem_optin &&
-                      !getenv("VCG_ROOT_ORDERED");
-    if (fast)
-      if (int r = raise_smem_limit((const void*)k_root_fixpoint_fast, (size_t)fast_smem)) return r;
+    static thread_local cudaEvent_t rk0 = nullptr, rk1 = nullptr;
+    if (!rk0) {
+      CK(cudaEventCreate(&rk0));
+      CK(cudaEventCreate(&rk1));
+    }
     int crown_applied_last = 1;
     bool hdeg_current = false;  // hdeg mirrors the device degrees
     static const int root_threads = getenv("VCG_ROOT_THREADS") ? atoi(getenv("VCG_ROOT_THREADS")) : 1024;
@@ -815,7 +868,11 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
       COUNT_LAUNCH(1);
       hdeg_current = false;
       const int budget = spec ? kSpecBudget : (int)(bound0 - forced_count);
-      if (fast) {
+      CK(cudaEventRecord(rk0, cudaStreamPerThread));
+      if (use_grid) {
+        CK(root_grid_launch(n, g->d_off.as<int32_t>(), g->d_nbr.as<int32_t>(), ws.as<char>(),
+                            budget, dout.as<int32_t>(), dret.as<long long>(), first, X.r_gctl.p));
+      } else if (fast) {
         k_root_fixpoint_fast<<<1, root_threads, fast_smem>>>(
             n, g->d_off.as<int32_t>(), g->d_nbr.as<int32_t>(), ws.as<uint32_t>(), lo, hi,
             budget, dout.as<int32_t>(), dret.as<long long>(), first);
@@ -825,12 +882,23 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
                                      dout.as<int32_t>(), 0, dret.as<long long>(), first);
       }
       CK(cudaGetLastError());
-      CK(cudaMemcpy(ret, dret.p, fast ? 144 : 80, cudaMemcpyDeviceToHost));
+      CK(cudaEventRecord(rk1, cudaStreamPerThread));
+      CK(cudaMemcpy(ret, dret.p, fast ? 144 : use_grid ? 88 : 80, cudaMemcpyDeviceToHost));
+      {
+        float kms = 0.f;
+        CK(cudaEventElapsedTime(&kms, rk0, rk1));
+        info->kernel_ms += kms;
+        info->kernel_launches += 1;
+        info->kernel_scans += use_grid ? ret[10] : fast ? ret[10] : 0;
+      }
       if (fast && trace_on())
         fprintf(stderr, "[vcg root] fixpoint sweeps: scans %lld (%lld cyc) d1 %lld (%lld) tri %lld (%lld) hd %lld (%lld)\n",
                 ret[10], ret[14], ret[11], ret[15], ret[12], ret[16], ret[13], ret[17]);
-      if (fast && ret[8]) return fail(VCG_ECUDA, "root fixpoint: inconsistent degree array");
-      if (spec) spec_rounds.emplace_back(fast ? ret[9] : ret[8], forced_count);
+      if (use_grid && trace_on())
+        fprintf(stderr, "[vcg root] grid fixpoint (%d blocks): %lld scans, forced %lld\n",
+                root_grid_blocks(), ret[10], ret[0]);
+      if ((fast || use_grid) && ret[8]) return fail(VCG_ECUDA, "root fixpoint: inconsistent degree array");
+      if (spec) spec_rounds.emplace_back((fast || use_grid) ? ret[9] : ret[8], forced_count);
       first = 0;
       if (ret[7] > 0) {
         size_t old = forced.size();
@@ -847,13 +915,15 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
       info->seconds[0] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       tr.mark("  device rules round");
       if (has_bound && forced_count > bound) break;
-      if (crown) {
+      if (crown && lo > hi) crown_applied_last = 0;  // an empty residual has no crown
+      if (crown && lo <= hi) {
         auto t1 = std::chrono::steady_clock::now();
+        hdeg.resize(n);
         CK(cudaMemcpy(hdeg.data(), ws.p, (size_t)n * 4, cudaMemcpyDeviceToHost));
         hdeg_current = true;
         std::vector<int32_t> heads;
         int64_t er = 0;
-        int64_t nh = crown_reduce_host(n, g->h_off.data(), g->h_nbr.data(), hdeg.data(), lo, hi,
+        int64_t nh = crown_reduce_host(n, g->hoff, g->hnbr, hdeg.data(), lo, hi,
                                        &heads, &er);
         crown_applied_last = nh > 0;
         if (nh > 0) {
@@ -884,9 +954,12 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
     (void)pos;
     if (forced_out)
       for (size_t i = 0; i < forced.size(); ++i) forced_out[i] = forced[i];
-    if (n <= kHostCompactMax) {
-      if (!hdeg_current)
+    const char* dc_env = getenv("VCG_DEVICE_COMPACT");
+    if (n <= kHostCompactMax && !(dc_env && atoi(dc_env) == 1)) {
+      if (!hdeg_current) {
+        hdeg.resize(n);
         CK(cudaMemcpy(hdeg.data(), ws.p, (size_t)n * 4, cudaMemcpyDeviceToHost));
+      }
       host_compact = true;
       host_deg.swap(hdeg);
     } else {
@@ -908,10 +981,10 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
   info->n_reduced = red->n;
   info->m_reduced = red->m2 / 2;
   int64_t md = 0;
-  for (int64_t v = 0; v < red->n; ++v) md = std::max<int64_t>(md, red->h_off[v + 1] - red->h_off[v]);
+  for (int64_t v = 0; v < red->n; ++v) md = std::max<int64_t>(md, red->hoff[v + 1] - red->hoff[v]);
   info->max_degree_reduced = md;
   tr.mark("compaction");
-  info->greedy_reduced = greedy_cover_host(red->n, red->h_off.data(), red->h_nbr.data(), nullptr);
+  info->greedy_reduced = greedy_cover_host(red->n, red->hoff, red->hnbr, nullptr);
   tr.mark("greedy_reduced");
   // VCG_ROOT_LAZY_GREEDY (the MVC solve path): every vertex cover of g has
   // at least forced + (maximal matching of the reduced graph) vertices --
@@ -921,7 +994,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
   // greedy is abandoned and reported as -1.
   if ((enabled & VCG_ROOT_LAZY_GREEDY) && has_bound == 0 && spec) {
     const int64_t lb =
-        forced_count + maximal_matching_host(red->n, red->h_off.data(), red->h_nbr.data());
+        forced_count + maximal_matching_host(red->n, red->hoff, red->hnbr);
     bool ok = info->greedy_reduced <= lb - forced_count;
     for (const auto& sr : spec_rounds) ok = ok && sr.first <= lb - sr.second;
     if (ok) {
@@ -1095,7 +1168,7 @@ extern "C" int vcg_expand(const vcg_graph* g, const vcg_expand_config* cfg, vcg_
   std::vector<int32_t> root(rec_bytes / 4, 0);
   int lo = -1, hi = -1;
   for (int v = 0; v < n; ++v) {
-    int d = (int)(g->h_off[v + 1] - g->h_off[v]);
+    int d = (int)(g->hoff[v + 1] - g->hoff[v]);
     root[8 + v] = d;
     if (d) {
       if (lo < 0) lo = v;
@@ -1359,7 +1432,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   int lo = -1, hi = -1;
   int64_t dsum = 0;
   for (int v = 0; v < n; ++v) {
-    int64_t d = cfg->root_deg ? cfg->root_deg[v] : g->h_off[v + 1] - g->h_off[v];
+    int64_t d = cfg->root_deg ? cfg->root_deg[v] : g->hoff[v + 1] - g->hoff[v];
     rdeg[v] = (T)d;
     dsum += d;
     if (d) {

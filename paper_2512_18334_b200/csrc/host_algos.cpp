@@ -28,10 +28,13 @@ int64_t greedy_cover_host(int64_t n, const int64_t* off, const int32_t* nbr, int
   if (n <= 0) return 0;
   std::vector<int32_t> deg(n);
   int64_t m2 = 0, maxdeg = 0;
+  // a cancelled greedy (the solve path's lazy bound) must return promptly
+  auto cancelled = [&]() { return cancel && cancel->load(std::memory_order_relaxed); };
   for (int64_t v = 0; v < n; ++v) {
     deg[v] = (int32_t)(off[v + 1] - off[v]);
     m2 += deg[v];
     maxdeg = std::max<int64_t>(maxdeg, deg[v]);
+    if ((v & 0xffff) == 0 && cancelled()) return -1;
   }
   if (m2 == 0) return 0;
   std::vector<std::vector<int32_t>> level(maxdeg + 1);
@@ -47,7 +50,7 @@ int64_t greedy_cover_host(int64_t n, const int64_t* off, const int32_t* nbr, int
   for (int64_t d = maxdeg; d >= 1; --d) {
     std::vector<int32_t>& cand = level[d];
     if (cand.empty()) continue;
-    if (cancel && cancel->load(std::memory_order_relaxed)) return -1;
+    if (cancelled()) return -1;
     int64_t wlo = INT64_MAX, whi = -1;
     for (int32_t v : cand)
       if (deg[v] == d) {
@@ -63,6 +66,7 @@ int64_t greedy_cover_host(int64_t n, const int64_t* off, const int32_t* nbr, int
         const int64_t v = w * 64 + __builtin_ctzll(bits);
         bits &= bits - 1;
         if (deg[v] != d) continue;  // demoted by an earlier pick of this level
+        if ((size & 0xfff) == 0 && cancelled()) return -1;
         for (int64_t i = off[v]; i < off[v + 1]; ++i) {
           const int32_t u = nbr[i];
           if (deg[u] > 0) {

@@ -126,7 +126,7 @@ def solve_distributed(g, config: SolverConfig | None = None, group=None,
     stats.degree_width = pre.width
     rg = pre.graph
     result = SolveResult(cover_size=None, found=False, exact=True, cover=None, stats=stats,
-                         mode=cfg.mode, k=cfg.k, forced=list(pre.forced))
+                         mode=cfg.mode, k=cfg.k, forced_ids=pre.forced_ids)
     if cfg.mode == "pvc" and pre.forced_count > cfg.k:
         return result
     if rg.num_edges == 0:

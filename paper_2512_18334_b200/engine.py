@@ -146,13 +146,24 @@ class SolveResult:
     k: int | None = None
     registry: RegistrySummary | None = None
     root_index: int | None = None
-    forced: list[int] = field(default_factory=list)
+    forced_ids: np.ndarray | None = None  # int32 root-forced ids (``forced`` as a list)
     warp_tasks: int = 0     # warp-tier tasks solved
     warp_nodes: int = 0     # tree nodes processed by the warp tier
     search_ms: float = 0.0  # device time of the search kernel
     blocks: int = 0         # search-kernel launch: resident blocks (workers)
     threads: int = 0        # and threads per block
     phase_cycles: dict = field(default_factory=dict)  # block time by phase (SM cycles)
+    root_kernel: dict = field(default_factory=dict)   # root rule kernels (Preprocessed.kernel)
+
+    @property
+    def forced(self) -> list[int]:
+        """engine.py:120 ``forced``: original ids the root reduction forced
+        (built from ``forced_ids`` on first access)."""
+        cached = self.__dict__.get("_forced_list")
+        if cached is None:
+            cached = [] if self.forced_ids is None else self.forced_ids.tolist()
+            self.__dict__["_forced_list"] = cached
+        return cached
 
 
 def run_search(rg: StaticGraph, cfg: SolverConfig, width: int, best_init: int,
@@ -221,9 +232,12 @@ def witness_cover(rg: StaticGraph, cfg: SolverConfig, width: int, target: int,
 
 def _assemble_cover(g: StaticGraph, pre: Preprocessed, local: list[int]) -> list[int]:
     """engine.py:550 -- map a reduced-graph cover to original ids and verify it."""
-    cover = sorted(set(pre.forced) | {int(pre.vertex_map[v]) for v in local})
+    forced = np.asarray(pre.forced_ids, dtype=np.int64)
+    local_orig = np.asarray(pre.vertex_map, dtype=np.int64)[np.asarray(local, dtype=np.int64)]
+    cover_arr = np.union1d(forced, local_orig)
+    cover = cover_arr.tolist()
     covered = np.zeros(g.num_vertices, dtype=bool)
-    covered[cover] = True
+    covered[cover_arr] = True
     heads = np.repeat(np.arange(g.num_vertices), np.diff(g.offsets))
     if not np.all(covered[heads] | covered[g.neighbors]):
         raise RuntimeError("reconstructed cover misses an edge")
@@ -252,7 +266,8 @@ def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
     rg = pre.graph
 
     result = SolveResult(cover_size=None, found=False, exact=True, cover=None, stats=stats,
-                         mode=cfg.mode, k=cfg.k, forced=list(pre.forced))
+                         mode=cfg.mode, k=cfg.k, forced_ids=pre.forced_ids,
+                         root_kernel=dict(pre.kernel))
 
     if cfg.mode == "pvc" and pre.forced_count > cfg.k:
         return result

@@ -53,16 +53,28 @@ class Preprocessed:
 
     graph: StaticGraph
     vertex_map: np.ndarray  # reduced id -> original id
-    forced: list[int]
+    forced_ids: np.ndarray  # int32, original ids forced into the cover
     greedy_original: int
     greedy_reduced: int
     width: int
     rule_counts: dict[str, int] = field(default_factory=dict)
     seconds: dict[str, float] = field(default_factory=dict)
+    kernel: dict = field(default_factory=dict)  # rule kernels: device ms, launches, scans, kind
+
+    @property
+    def forced(self) -> list[int]:
+        """The reference's ``forced`` list (built on first access: a 1M-vertex
+        root reduction forces ~10^5 vertices, and the solve path only needs
+        their count)."""
+        cached = self.__dict__.get("_forced_list")
+        if cached is None:
+            cached = self.forced_ids.tolist()
+            self.__dict__["_forced_list"] = cached
+        return cached
 
     @property
     def forced_count(self) -> int:
-        return len(self.forced)
+        return len(self.forced_ids)
 
 
 def root_reduce(g: StaticGraph, enabled: bool = True, crown: bool = True,
@@ -96,11 +108,14 @@ def root_reduce(g: StaticGraph, enabled: bool = True, crown: bool = True,
     return Preprocessed(
         graph=reduced,
         vertex_map=vmap[: info.n_reduced].copy(),
-        forced=forced[: info.forced_count].tolist(),
+        forced_ids=forced[: info.forced_count],
         greedy_original=int(info.greedy_original),
         greedy_reduced=int(info.greedy_reduced),
         width=select_width(md, width_override),
         rule_counts=dict(zip(ROOT_RULE_KEYS, (int(x) for x in info.rule_counts))),
         seconds={"device_reduce": info.seconds[0], "crown": info.seconds[1],
                  "compaction": info.seconds[2]},
+        kernel={"ms": info.kernel_ms, "launches": int(info.kernel_launches),
+                "scans": int(info.kernel_scans),
+                "kind": ("none", "block_smem", "block_hbm", "grid")[int(info.kernel_kind)]},
     )

@@ -31,6 +31,7 @@ class OracleBackend:
         greedy_red = oracle.greedy_bound(rn, pre["offsets"], pre["neighbors"])
         return types.SimpleNamespace(graph=rg, rule_counts=pre["rule_counts"],
                                      forced=pre["forced"], forced_count=len(pre["forced"]),
+                                     forced_ids=np.asarray(pre["forced"], dtype=np.int32),
                                      greedy_original=pre["greedy_original"],
                                      greedy_reduced=greedy_red, width=32)
 

@@ -2,21 +2,16 @@
 size-independent properties: the recorded cover is a valid vertex cover of
 exactly the reported size, the PVC pair at k = opt / opt - 1 answers
 yes / no (so the reported size is the minimum), and the deterministic
-(reference-schedule) and parallel modes agree.  ba100k's optimum is pinned
-to the C oracle's answer (profiles/r01_configs.json, cpu_cover: the
-oracle's 13 s solve is too slow for the test suite); planted1m is beyond
-the oracle's O(n x picks) greedy, so its optimum is pinned by the PVC pair
-only."""
+(reference-schedule) and parallel modes agree.  The optima are pinned to
+the C oracle's (tests/golden/scale.json, make_scale_golden.py)."""
 
 from __future__ import annotations
 
 import pytest
 
-from helpers import assert_valid_cover
+from helpers import assert_valid_cover, golden
 
 pytestmark = pytest.mark.gpu
-
-ORACLE_MVC = {"ba100k": 48591}
 
 
 @pytest.mark.parametrize("name", ["ba100k", "planted1m"])
@@ -33,8 +28,7 @@ def test_large_config_cover_and_pvc_pair(name):
     assert len(r.cover) == r.cover_size == len(set(r.cover))
     assert_valid_cover(n, np.asarray(off), np.asarray(nbr), r.cover)
     opt = r.cover_size
-    if name in ORACLE_MVC:
-        assert opt == ORACLE_MVC[name]
+    assert opt == golden("scale.json")[name]["mvc"]
     assert vc.solve(g, vc.SolverConfig(deterministic=True)).cover_size == opt
     assert vc.solve(g, vc.SolverConfig()).cover_size == opt
     yes = vc.solve(g, vc.SolverConfig(mode="pvc", k=opt))
