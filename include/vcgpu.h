@@ -80,11 +80,17 @@ typedef struct {
   /* device time of the rule kernels (CUDA events on the calling thread's
    * stream), their launches, grid-wide scans of the degree array, and the
    * kernel kind (0 none, 1 single block on chip, 2 single block in HBM,
-   * 3 grid-wide cooperative) */
+   * 3 grid-wide cooperative, 4 grid-wide frontier-driven: any-order callers) */
   double kernel_ms;
   int64_t kernel_launches;
   int64_t kernel_scans;
   int64_t kernel_kind;
+  /* frontier kernel (kind 4): sweeps and adjacency entries walked */
+  int64_t kernel_sweeps;
+  int64_t kernel_walked;
+  /* VCG_ROOT_LAZY_GREEDY: the smallest greedy_original under which the
+   * speculative-budget rules equal the reference's (-1: no speculation) */
+  int64_t spec_need;
 } vcg_preprocessed;
 
 /* `enabled` flags of vcg_root_reduce: bit 0 applies the rules; with
@@ -93,11 +99,19 @@ typedef struct {
  * fused order-free sweeps on an on-chip workspace (the solve path). */
 #define VCG_ROOT_RULES 1
 #define VCG_ROOT_ANY_ORDER 2
-/* MVC without a bound (has_bound == 0): the greedy cover of g may be skipped
- * and reported as greedy_original = -1 when a matching lower bound proves it
- * cannot change the reduction or the search's initial bound (then the search
- * starts from greedy_reduced, achieved). */
+/* MVC without a bound (has_bound == 0): the greedy cover of g is not
+ * computed (greedy_original = -1).  The rules run with the speculative budget
+ * and report spec_need: the reduction equals the reference's iff the greedy
+ * cover of g has >= spec_need vertices, which the caller certifies after the
+ * search with the optimum it found (every cover, the greedy one included, has
+ * >= optimum vertices), computing the greedy (vcg_greedy_bound) only when
+ * optimum < spec_need, and rerunning with VCG_ROOT_NO_SPEC if the greedy is
+ * below it too.  The search then starts from greedy_reduced (achieved): the
+ * optimum is the same, only the search order can differ from the reference's
+ * min(greedy_reduced, greedy_original - forced). */
 #define VCG_ROOT_LAZY_GREEDY 4
+/* Rules with the real MVC bound from the start (no speculation). */
+#define VCG_ROOT_NO_SPEC 8
 
 /* Root reduction (lightweight rules on the device to a joint fixpoint with
  * the crown rule) and device compaction of the survivors.

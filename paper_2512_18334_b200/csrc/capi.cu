@@ -202,7 +202,7 @@ struct SearchCtx {
   DevBuf stacks, qseq, qdata, qctl, reg, ctl, hist, gws, wbits, wcount, bseq, bdata, bctl, sg, arena;
   // root pipeline / compaction / expansion scratch, reused across calls
   // (per-call cudaMalloc/cudaFree of tens of MB costs milliseconds, with outliers)
-  DevBuf r_flag, r_ws, r_out, r_ret, r_gctl, c_newid, c_cnt, c_vmap, c_tmp, x_ws, x_fifo, x_out;
+  DevBuf r_flag, r_ws, r_out, r_ret, r_gctl, r_front, r_fctl, c_newid, c_cnt, c_vmap, c_tmp, x_ws, x_fifo, x_out;
 };
 
 struct vcg_graph {
@@ -781,7 +781,10 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
   int64_t greedy_orig = -1;
   std::atomic<bool> greedy_cancel{false};
   std::thread greedy_thr;
-  if (has_bound != 1)
+  // VCG_ROOT_LAZY_GREEDY: the greedy is not run at all; the caller certifies
+  // the speculation afterwards (spec_need, see vcgpu.h)
+  const bool lazy = (enabled & VCG_ROOT_LAZY_GREEDY) && has_bound == 0;
+  if (has_bound != 1 && !lazy)
     greedy_thr = std::thread([&]() {
       greedy_orig =
           greedy_cover_host(g->n, g->hoff, g->hnbr, nullptr, &greedy_cancel);
@@ -792,8 +795,9 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
       if (t.joinable()) t.join();
     }
   } join_guard{greedy_thr};
-  const bool spec = spec_ok && has_bound == 0 && rules_on && !getenv("VCG_NO_SPEC");
-  if (has_bound == 0 && !spec) greedy_thr.join();
+  const bool spec = spec_ok && has_bound == 0 && rules_on && !getenv("VCG_NO_SPEC") &&
+                    !(enabled & VCG_ROOT_NO_SPEC);
+  if (has_bound == 0 && !spec && greedy_thr.joinable()) greedy_thr.join();
   const int64_t bound0 = has_bound ? bound : greedy_orig;  // unused while speculating
   std::vector<std::pair<int64_t, int64_t>> spec_rounds;   // (spec_m, forced before the round)
   tr.mark("greedy_original");
@@ -802,6 +806,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
   if (flag.ensure((size_t)(n + 1) * 4)) return VCG_ERESOURCE;
   std::vector<int64_t> vmap;
   int64_t forced_count = 0;
+  bool residual_empty = false;  // the rules left no edge: no compaction needed
   bool host_compact = false;
   std::vector<int32_t> host_deg;
   if (!rules_on) {
@@ -825,13 +830,20 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
     const bool on_chip = fast_smem + 8192 <= smem_optin;
     const bool fast = (enabled & VCG_ROOT_ANY_ORDER) && on_chip && !getenv("VCG_ROOT_ORDERED") &&
                       !(grid_env && atoi(grid_env) == 1);
-    const bool use_grid = !fast && (grid_env ? atoi(grid_env) == 1 : !on_chip);
+    // VCG_ROOT_GRID=2 forces the frontier kernel (any-order callers only)
+    const bool any_order = (enabled & VCG_ROOT_ANY_ORDER) && !getenv("VCG_ROOT_ORDERED");
+    const bool use_front = any_order && (grid_env ? atoi(grid_env) == 2 : !on_chip);
+    const bool use_grid =
+        !fast && !use_front && (grid_env ? atoi(grid_env) >= 1 : !on_chip);
     if (use_grid && X.r_gctl.ensure(root_grid_ctl_bytes())) return VCG_ERESOURCE;
+    if (use_front &&
+        (X.r_fctl.ensure(root_front_ctl_bytes()) || X.r_front.ensure(root_front_bytes(n, (long long)g->m2))))
+      return VCG_ERESOURCE;
     if (fast)
       if (int r = raise_smem_limit((const void*)k_root_fixpoint_fast, (size_t)fast_smem)) return r;
-    info->kernel_kind = use_grid ? 3 : fast ? 1 : 2;
+    info->kernel_kind = use_front ? 4 : use_grid ? 3 : fast ? 1 : 2;
     int lo = 0, hi = n - 1;
-    if (!use_grid) {  // the single-block kernels take the initial live window
+    if (!use_grid && !use_front) {  // the single-block kernels take the initial live window
       int l = -1, h = -1;
       for (int v = 0; v < n; ++v)
         if (g->hoff[v + 1] > g->hoff[v]) {
@@ -849,7 +861,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
     std::vector<int32_t> hdeg;  // host copy of the degrees (crown / host compaction)
     int first = 1;
     int pos = 0;
-    std::vector<int32_t> forced;
+    int64_t nforced = 0;  // forced ids written to forced_out
     static thread_local cudaEvent_t rk0 = nullptr, rk1 = nullptr;
     if (!rk0) {
       CK(cudaEventCreate(&rk0));
@@ -861,7 +873,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
     while (true) {
       int64_t progressed = 0;
       auto t0 = std::chrono::steady_clock::now();
-      long long ret[18];
+      long long ret[26];
       // a round after a crown that applied nothing finds the fixpoint
       // unchanged and the crown again empty: skip it (same counts)
       if (!first && !crown_applied_last) break;
@@ -869,7 +881,11 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
       hdeg_current = false;
       const int budget = spec ? kSpecBudget : (int)(bound0 - forced_count);
       CK(cudaEventRecord(rk0, cudaStreamPerThread));
-      if (use_grid) {
+      if (use_front) {
+        CK(root_front_launch(n, g->d_off.as<int32_t>(), g->d_nbr.as<int32_t>(), ws.as<char>(),
+                             X.r_front.as<char>(), budget, dout.as<int32_t>(),
+                             dret.as<long long>(), first, X.r_fctl.p));
+      } else if (use_grid) {
         CK(root_grid_launch(n, g->d_off.as<int32_t>(), g->d_nbr.as<int32_t>(), ws.as<char>(),
                             budget, dout.as<int32_t>(), dret.as<long long>(), first, X.r_gctl.p));
       } else if (fast) {
@@ -883,28 +899,43 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
       }
       CK(cudaGetLastError());
       CK(cudaEventRecord(rk1, cudaStreamPerThread));
-      CK(cudaMemcpy(ret, dret.p, fast ? 144 : use_grid ? 88 : 80, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(ret, dret.p, fast ? 144 : use_front ? 200 : use_grid ? 88 : 80,
+                    cudaMemcpyDeviceToHost));
       {
         float kms = 0.f;
         CK(cudaEventElapsedTime(&kms, rk0, rk1));
         info->kernel_ms += kms;
         info->kernel_launches += 1;
-        info->kernel_scans += use_grid ? ret[10] : fast ? ret[10] : 0;
+        info->kernel_scans += (use_grid || use_front || fast) ? ret[10] : 0;
+        if (use_front) {
+          info->kernel_sweeps += ret[11];
+          info->kernel_walked += ret[13];
+        }
       }
       if (fast && trace_on())
         fprintf(stderr, "[vcg root] fixpoint sweeps: scans %lld (%lld cyc) d1 %lld (%lld) tri %lld (%lld) hd %lld (%lld)\n",
                 ret[10], ret[14], ret[11], ret[15], ret[12], ret[16], ret[13], ret[17]);
+      if (use_front && trace_on())
+        fprintf(stderr, "[vcg root] frontier fixpoint (%d blocks): %lld full passes, %lld sweeps "
+                "(%lld in one block), %lld adjacency entries, %lld frontier entries, forced %lld; "
+                "us: solo %.1f, grid d1 %.1f, grid tri %.1f, hd %.1f\n",
+                root_front_blocks(), ret[10], ret[11], ret[12], ret[13], ret[14], ret[0],
+                ret[15] * 1e-3, ret[16] * 1e-3, ret[17] * 1e-3, ret[18] * 1e-3);
+      if (use_front && trace_on())
+        fprintf(stderr, "[vcg root] d1 phases us: A %.1f syncA %.1f B %.1f syncB %.1f C %.1f syncC %.1f\n",
+                ret[19] * 1e-3, ret[22] * 1e-3, ret[20] * 1e-3, ret[23] * 1e-3, ret[21] * 1e-3,
+                ret[24] * 1e-3);
       if (use_grid && trace_on())
         fprintf(stderr, "[vcg root] grid fixpoint (%d blocks): %lld scans, forced %lld\n",
                 root_grid_blocks(), ret[10], ret[0]);
-      if ((fast || use_grid) && ret[8]) return fail(VCG_ECUDA, "root fixpoint: inconsistent degree array");
-      if (spec) spec_rounds.emplace_back((fast || use_grid) ? ret[9] : ret[8], forced_count);
+      if ((fast || use_grid || use_front) && ret[8])
+        return fail(VCG_ECUDA, "root fixpoint: inconsistent degree array");
+      if (spec)
+        spec_rounds.emplace_back((fast || use_grid || use_front) ? ret[9] : ret[8], forced_count);
       first = 0;
-      if (ret[7] > 0) {
-        size_t old = forced.size();
-        forced.resize(old + ret[7]);
-        CK(cudaMemcpy(forced.data() + old, dout.p, (size_t)ret[7] * 4, cudaMemcpyDeviceToHost));
-      }
+      if (ret[7] > 0 && forced_out)  // straight into the caller's buffer
+        CK(cudaMemcpy(forced_out + nforced, dout.p, (size_t)ret[7] * 4, cudaMemcpyDeviceToHost));
+      nforced += ret[7];
       info->rule_counts[0] += ret[1];
       info->rule_counts[1] += ret[2];
       info->rule_counts[2] += ret[3];
@@ -928,7 +959,8 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
         crown_applied_last = nh > 0;
         if (nh > 0) {
           info->rule_counts[3] += 1;
-          forced.insert(forced.end(), heads.begin(), heads.end());
+          if (forced_out) std::copy(heads.begin(), heads.end(), forced_out + nforced);
+          nforced += (int64_t)heads.size();
           forced_count += nh;
           progressed += nh;
           CK(cudaMemcpy(ws.p, hdeg.data(), (size_t)n * 4, cudaMemcpyHostToDevice));
@@ -952,10 +984,11 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
       if (progressed == 0) break;
     }
     (void)pos;
-    if (forced_out)
-      for (size_t i = 0; i < forced.size(); ++i) forced_out[i] = forced[i];
+    residual_empty = lo > hi;
     const char* dc_env = getenv("VCG_DEVICE_COMPACT");
-    if (n <= kHostCompactMax && !(dc_env && atoi(dc_env) == 1)) {
+    if (residual_empty) {
+      // nothing survives: the empty graph, no flag / scan / gather
+    } else if (n <= kHostCompactMax && !(dc_env && atoi(dc_env) == 1)) {
       if (!hdeg_current) {
         hdeg.resize(n);
         CK(cudaMemcpy(hdeg.data(), ws.p, (size_t)n * 4, cudaMemcpyDeviceToHost));
@@ -971,7 +1004,18 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
   tr.mark("rules+crown");
   auto t2 = std::chrono::steady_clock::now();
   vcg_graph* red = nullptr;
-  if (host_compact) {
+  if (residual_empty) {
+    red = new vcg_graph();
+    red->n = 0;
+    red->m2 = 0;
+    if (red->d_off.ensure(4) || red->d_nbr.ensure(4)) {
+      delete red;
+      return VCG_ERESOURCE;
+    }
+    CK(cudaMemsetAsync(red->d_off.p, 0, 4, cudaStreamPerThread));
+    red->own_off.assign(1, 0);
+    red->adopt_owned();
+  } else if (host_compact) {
     if (int r = compact_host(g, host_deg.data(), &red, &vmap)) return r;
   } else if (int r = compact_flagged(g, flag, &red, &vmap)) {
     return r;
@@ -992,21 +1036,19 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
   // that lower bound already certifies both uses of the greedy value (the
   // speculative high-degree check and best_init = greedy_reduced), the
   // greedy is abandoned and reported as -1.
-  if ((enabled & VCG_ROOT_LAZY_GREEDY) && has_bound == 0 && spec) {
-    const int64_t lb =
-        forced_count + maximal_matching_host(red->n, red->hoff, red->hnbr);
-    bool ok = info->greedy_reduced <= lb - forced_count;
-    for (const auto& sr : spec_rounds) ok = ok && sr.first <= lb - sr.second;
-    if (ok) {
-      greedy_cancel.store(true, std::memory_order_relaxed);
-      if (greedy_thr.joinable()) greedy_thr.join();
-      tr.mark("greedy_original skipped");
-      info->greedy_original = -1;
-      if (vertex_map_out)
-        for (size_t i = 0; i < vmap.size(); ++i) vertex_map_out[i] = vmap[i];
-      *reduced_out = red;
-      return 0;
-    }
+  if (lazy) {
+    // the greedy of g is the MVC bound, >= every cover size: the speculation
+    // holds iff greedy_original >= spec_need; the caller checks it against
+    // the optimum it finds (a lower bound of the greedy), and only computes
+    // the greedy when that does not suffice
+    int64_t need = -1;
+    for (const auto& sr : spec_rounds) need = std::max<int64_t>(need, sr.first + sr.second);
+    info->spec_need = need;
+    info->greedy_original = -1;
+    if (vertex_map_out)
+      for (size_t i = 0; i < vmap.size(); ++i) vertex_map_out[i] = vmap[i];
+    *reduced_out = red;
+    return 0;
   }
   if (greedy_thr.joinable()) greedy_thr.join();
   tr.mark("greedy_original joined");

@@ -1,0 +1,826 @@
+// Frontier-driven grid-wide root fixpoint for the solve path
+// (preprocess.py:77 root_reduce -> reductions.py:110 reduce_to_fixpoint ->
+// kernels/pure.py:188 reduce_fixpoint), any-order variant: the same sweeps,
+// the same forced SET and rule counts as the reference, forced ids returned
+// in index order (VCG_ROOT_ANY_ORDER).
+//
+// Why a frontier.  Every sweep of the reference snapshots its candidates with
+// a scan of the whole live window.  On the 1M-vertex / 100k-vertex configs
+// that is 12 / 66 sweeps of a full scan each (root_grid.cu), although after
+// the first sweep only vertices whose degree changed can be candidates:
+//  * degree-one (pure.py:82): every candidate of a sweep ends it with degree 0
+//    (it applies and its neighbour is removed, or an earlier candidate removed
+//    that neighbour), so the candidates of sweep s+1 are exactly the vertices
+//    whose degree fell 2 -> 1 since the snapshot of sweep s;
+//  * triangle (pure.py:113): validity (two live neighbours, adjacent in the
+//    static CSR) only changes with the vertex's degree, and a valid candidate
+//    that does not apply meets an applied triangle, i.e. loses degree; so the
+//    candidates that can be valid are the vertices whose degree fell 3 -> 2
+//    since the previous triangle snapshot.
+// Removals push those transitions (the atomicSub's old value) onto
+// double-buffered frontier lists, so a sweep costs its frontier plus the
+// adjacency of what it removes, not n.  The high-degree sweep (pure.py:158)
+// depends on the budget, not on degree changes: it stays a full pass (one
+// per fixpoint cycle), which also yields the exact maximum live degree for
+// the speculative-budget record.
+//
+// Latency, not bandwidth, bounds a sweep (a few thousand frontier entries on
+// the 100k-vertex config), so every step is shaped for short dependent
+// chains spread over the whole grid:
+//  * every vertex keeps the sum and the sum of squares of its live
+//    neighbours' ids: a degree-1 vertex's neighbour is the sum, a degree-2
+//    vertex's two neighbours solve a + b = S1, a^2 + b^2 = S2 -- one load
+//    instead of a walk over a mostly dead adjacency;
+//  * removals are split into chunks of kChunk adjacency entries, one thread
+//    per chunk, loads of a chunk issued before its atomics;
+//  * a grid barrier that polls with volatile loads and __nanosleep (the
+//    cooperative-groups barrier invalidates L1 on every poll).
+//
+// Exact parallel sweep semantics (node_ops.cuh): degree-one candidate v with
+// target u(v) applies iff v is the lowest-index candidate targeting u(v) and
+// not the higher end of an isolated candidate edge; triangles apply as the
+// lexicographically-first maximal independent set of the valid candidates'
+// intersection graph, resolved in claim rounds.  Claims are 64-bit
+// (tag << 32 | INT_MAX - v) atomicMax keys with a fresh tag per round, so no
+// reset pass is needed; removal-set membership is a per-vertex sweep tag.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+
+#include "root_grid.cuh"
+#include "search.cuh"
+
+namespace vcg {
+
+namespace {
+
+constexpr int kSolo = 0;     // default: frontier size below which block 0 sweeps alone
+constexpr int kChunk = 8;    // adjacency entries per removal work item
+
+enum Phase { F_D1 = 0, F_TRI = 1, F_HD = 2, F_DONE = 3 };
+
+struct St {  // fixpoint state, replicated in every thread (uniform transitions)
+  int phase, p1, p2, s, tg;
+  int cycle, d1, d2t, hd, forced, spec_m;
+  int sweeps, passes, solo;
+};
+
+struct FrontCtl {
+  int cnt1[2], cnt2[2];                       // frontier list lengths (index = buffer)
+  int nrem[3], ncand[3], ch[3], dmax[3], nchunk[3];  // per step, by step id mod 3
+  int ropen[3];                               // triangle claim rounds, by claim tag mod 3
+  int err, hd_applied, wlo, whi;  // wlo = max(INT_MAX - lowest live), whi = max(highest live + 1)
+  unsigned long long edges, walked, items;
+  unsigned bar;                               // grid_barrier word
+  unsigned long long tph[8];                  // phase times (ns, thread 0): A, B, C, barriers
+  St st;                                      // block 0 -> grid after a solo segment
+  int partial[kRootGridMaxBlocks];
+};
+
+struct Front {  // device arrays (root_front_bytes)
+  uint32_t* deg;
+  unsigned long long* key;          // claims
+  unsigned long long *nsum, *nsq;   // live-neighbour id sums
+  int *ia, *ib, *st, *rs;           // targets, triangle state, removal tag
+  int *l1[2], *l2[2];               // frontier lists (pending / snapshot)
+  int *rem, *cand;
+  int2* chunk;                      // removal work items (vertex, first entry)
+  uint8_t* forced;
+};
+
+// Grid barrier.  cooperative_groups' grid.sync() polls with acquire loads,
+// each followed by an L1 invalidate (CCTL.IVALL; ncu: 8.5 M in one launch).
+// This one polls with volatile loads and __nanosleep and acquires once, after
+// the flip.  Arrival flips bit 31 of the word (block 0 adds 2^31 - (blocks -
+// 1), the others 1), so it needs no reset.
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+    __threadfence();
+    const unsigned old = atomicAdd(bar, inc);
+    unsigned ns = 32;
+    while (((old ^ *(volatile unsigned*)bar) & 0x80000000u) == 0) {
+      __nanosleep(ns);
+      if (ns < 256) ns <<= 1;
+    }
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    (void)v;
+  }
+  __syncthreads();
+}
+
+struct Ex {  // executor: the whole grid, or block 0 alone
+  int rank, size;
+  bool grid;
+  unsigned* bar;
+  __device__ void sync() const {
+    if (grid) grid_barrier(bar);
+    else __syncthreads();
+  }
+};
+
+__device__ __forceinline__ int vld(const int* p) { return *(const volatile int*)p; }
+__device__ __forceinline__ int dget(const uint32_t* d, int v) { return (int)__ldcg(d + v); }
+
+__device__ __forceinline__ unsigned long long claim_key(int tg, int v) {
+  return ((unsigned long long)(unsigned)tg << 32) | (unsigned long long)(unsigned)(kInf - v);
+}
+
+// Appends to the global lists go through two block-local staging queues in
+// shared memory: one global atomic per block and phase instead of one per
+// entry (the list counters are the kernel's only hot words).
+constexpr int kQ = 2048;
+struct BlockQ {
+  int cnt[2], base[2];
+  int buf[2][kQ];
+  int ccnt, cbase, cused;  // removal chunks: reserved, published base, staged
+  int2 cbuf[kQ];
+};
+
+__device__ __forceinline__ void qpush(BlockQ* q, int which, int* list, int* gcnt, int v) {
+  const int pos = atomicAdd(&q->cnt[which], 1);
+  if (pos < kQ) q->buf[which][pos] = v;
+  else list[atomicAdd(gcnt, 1)] = v;  // staging full: append directly
+}
+
+// every thread of the block calls; publishes both staging queues
+__device__ __forceinline__ void qflush(BlockQ* q, int* list0, int* cnt0, int* list1, int* cnt1) {
+  __syncthreads();
+  const int c0 = min(q->cnt[0], kQ), c1 = min(q->cnt[1], kQ);
+  if (threadIdx.x == 0) {
+    q->base[0] = c0 ? atomicAdd(cnt0, c0) : 0;
+    q->base[1] = c1 ? atomicAdd(cnt1, c1) : 0;
+  }
+  __syncthreads();
+  const int b0 = q->base[0], b1 = q->base[1];
+  for (int i = threadIdx.x; i < c0; i += blockDim.x) list0[b0 + i] = q->buf[0][i];
+  for (int i = threadIdx.x; i < c1; i += blockDim.x) list1[b1 + i] = q->buf[1][i];
+  __syncthreads();
+  if (threadIdx.x == 0) q->cnt[0] = q->cnt[1] = 0;
+}
+
+// the two live neighbours a < b of a degree-2 vertex from its sums
+__device__ __forceinline__ void two_from_sums(const Front& F, int v, int* a, int* b) {
+  const unsigned long long s1 = __ldcg(F.nsum + v), s2 = __ldcg(F.nsq + v);
+  const unsigned long long d2 = 2ull * s2 - s1 * s1;  // (b - a)^2
+  unsigned long long d = (unsigned long long)sqrt((double)d2);
+  while (d * d > d2) --d;
+  while ((d + 1) * (d + 1) <= d2) ++d;
+  *a = (int)((s1 - d) >> 1);
+  *b = (int)((s1 + d) >> 1);
+}
+
+// u joins the removal set of step s: the rem list, and its adjacency as
+// kChunk-entry work items
+__device__ __forceinline__ void add_removed(const Front& F, FrontCtl* G, BlockQ* q,
+                                            const int* off, int s, int u) {
+  F.rs[u] = s;
+  qpush(q, 0, F.rem, &G->nrem[s % 3], u);
+  const int b = off[u], e = off[u + 1];
+  const int nc = (e - b + kChunk - 1) / kChunk;
+  if (nc > 0) {
+    const int pos = atomicAdd(&q->ccnt, nc);
+    if (pos + nc <= kQ) {
+      for (int c = 0; c < nc; ++c) q->cbuf[pos + c] = make_int2(u, b + c * kChunk);
+      atomicMax(&q->cused, pos + nc);
+    } else {  // staging full: append directly
+      const int at = atomicAdd(&G->nchunk[s % 3], nc);
+      for (int c = 0; c < nc; ++c) F.chunk[at + c] = make_int2(u, b + c * kChunk);
+    }
+  }
+}
+
+// every thread of the block calls: publishes the staged removal chunks
+__device__ __forceinline__ void cflush(BlockQ* q, int2* list, int* cnt) {
+  __syncthreads();
+  const int c = q->cused;
+  if (threadIdx.x == 0) q->cbase = c ? atomicAdd(cnt, c) : 0;
+  __syncthreads();
+  const int b = q->cbase;
+  for (int i = threadIdx.x; i < c; i += blockDim.x) list[b + i] = q->cbuf[i];
+  __syncthreads();
+  if (threadIdx.x == 0) q->ccnt = q->cused = 0;
+}
+
+// one removal work item: the entries [b, min(b + kChunk, end(u))) of removed
+// vertex u.  Non-member live neighbours lose a degree and u from their sums;
+// 2 -> 1 and 3 -> 2 transitions are pushed to the pending lists.
+__device__ __forceinline__ void rm_chunk(const Front& F, FrontCtl* G, BlockQ* q, const int* off,
+                                         const int* nbr, int s, int p1, int p2, int u, int b,
+                                         long long* edges) {
+  const int e = min(off[u + 1], b + kChunk);
+  const int len = e - b;
+  int x[kChunk], live[kChunk];
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j) x[j] = j < len ? __ldg(nbr + b + j) : -1;
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j) {
+    live[j] = 0;
+    if (x[j] >= 0) {
+      const int r = __ldcg(F.rs + x[j]);
+      const int d = dget(F.deg, x[j]);
+      if (r == s) {
+        if (x[j] > u) ++*edges;  // both ends removed together: counted once
+      } else if (d > 0) {
+        live[j] = 1;
+      }
+    }
+  }
+  unsigned old[kChunk];
+  const unsigned long long uu = (unsigned long long)u;
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j) {
+    old[j] = 0;
+    if (live[j]) {
+      old[j] = atomicSub(F.deg + x[j], 1u);
+      atomicAdd(F.nsum + x[j], 0ull - uu);
+      atomicAdd(F.nsq + x[j], 0ull - uu * uu);
+      ++*edges;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j) {
+    if (old[j] == 2u) qpush(q, 0, F.l1[p1], &G->cnt1[p1], x[j]);
+    else if (old[j] == 3u) qpush(q, 1, F.l2[p2], &G->cnt2[p2], x[j]);
+  }
+}
+
+// phase C of a sweep: remove every member of the step's set (rem / chunks);
+// transitions go to the pending lists l1[p1] / l2[p2]
+__device__ __forceinline__ void remove_set(const Ex& E, const Front& F, FrontCtl* G, BlockQ* q,
+                                           const int* off, const int* nbr, int s, int p1, int p2,
+                                           long long* edges, long long* walked) {
+  const int nrem = vld(&G->nrem[s % 3]), nch = vld(&G->nchunk[s % 3]);
+  for (int c = E.rank; c < nch; c += E.size) {
+    const int2 ch = F.chunk[c];
+    rm_chunk(F, G, q, off, nbr, s, p1, p2, ch.x, ch.y, edges);
+  }
+  for (int k = E.rank; k < nrem; k += E.size) {
+    const int u = F.rem[k];
+    *walked += off[u + 1] - off[u];
+    F.deg[u] = 0;
+    F.forced[u] = 1;
+  }
+  qflush(q, F.l1[p1], &G->cnt1[p1], F.l2[p2], &G->cnt2[p2]);
+}
+
+// live-neighbour sums of every live vertex (thread per vertex, a warp for
+// adjacencies longer than 32)
+__device__ __forceinline__ void init_sums(const Front& F, const int* off, const int* nbr, int n,
+                                          bool all_live) {
+  const int lane = threadIdx.x & 31;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, T = gridDim.x * blockDim.x;
+  for (int base = gt - lane; base < n; base += T) {
+    const int v = base + lane;
+    bool lng = false;
+    if (v < n && dget(F.deg, v) > 0) {
+      const int b = off[v], e = off[v + 1];
+      if (e - b <= 32) {
+        unsigned long long s1 = 0, s2 = 0;
+        for (int i = b; i < e; ++i) {
+          const int x = __ldg(nbr + i);
+          if (all_live || dget(F.deg, x) > 0) {
+            s1 += (unsigned long long)x;
+            s2 += (unsigned long long)x * (unsigned long long)x;
+          }
+        }
+        F.nsum[v] = s1;
+        F.nsq[v] = s2;
+      } else {
+        lng = true;
+      }
+    }
+    unsigned m = __ballot_sync(0xffffffffu, lng);
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const int vv = base + src;
+      unsigned long long s1 = 0, s2 = 0;
+      const int e = off[vv + 1];
+      for (int i = off[vv] + lane; i < e; i += 32) {
+        const int x = __ldg(nbr + i);
+        if (all_live || dget(F.deg, x) > 0) {
+          s1 += (unsigned long long)x;
+          s2 += (unsigned long long)x * (unsigned long long)x;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      }
+      if (lane == 0) {
+        F.nsum[vv] = s1;
+        F.nsq[vv] = s2;
+      }
+    }
+  }
+}
+
+// step prologue (rank 0): clear the next step's slots
+__device__ __forceinline__ void next_slots(FrontCtl* G, int s) {
+  const int z = (s + 1) % 3;
+  G->nrem[z] = G->ncand[z] = G->ch[z] = G->dmax[z] = G->nchunk[z] = 0;
+}
+
+struct Timer {  // thread 0's phase clock
+  unsigned long long t;
+  bool on;
+  __device__ explicit Timer(bool o) : t(o ? globaltimer() : 0), on(o) {}
+  __device__ void lap(FrontCtl* G, int i) {
+    if (on) {
+      const unsigned long long now = globaltimer();
+      G->tph[i] += now - t;
+      t = now;
+    }
+  }
+};
+
+// One degree-one sweep (pure.py:82) over the pending list l1[p1].
+__device__ __forceinline__ void sweep_d1(const Ex& E, const Front& F, FrontCtl* G, BlockQ* q,
+                                         const int* off, const int* nbr, St& S, long long* edges,
+                                         long long* walked) {
+  const int s = S.s, t = S.tg;
+  const int cur = S.p1, nxt = S.p1 ^ 1;
+  const int ncur = vld(&G->cnt1[cur]);
+  if (ncur == 0) {  // nothing to sweep: no barriers, no step slot used
+    S.sweeps += 1;
+    S.phase = F_TRI;
+    return;
+  }
+  Timer tm(E.rank == 0);
+  int* L = F.l1[cur];
+  if (E.rank == 0) {
+    G->cnt1[nxt] = 0;
+    next_slots(G, s);
+    G->items += (unsigned long long)ncur;
+  }
+  // A: targets (the neighbour-id sum of a degree-1 vertex) and claims
+  for (int k = E.rank; k < ncur; k += E.size) {
+    const int v = L[k];
+    if (dget(F.deg, v) != 1) {
+      L[k] = -1;
+      continue;
+    }
+    const int u = (int)__ldcg(F.nsum + v);
+    if (u < 0 || dget(F.deg, u) <= 0) {  // inconsistent degree array: report, never loop
+      atomicExch(&G->err, 1);
+      L[k] = -1;
+      continue;
+    }
+    F.ia[v] = u;
+    atomicMax(F.key + u, claim_key(t, v));
+  }
+  tm.lap(G, 0);
+  E.sync();
+  tm.lap(G, 3);
+  // B: decisions (lowest-index claimant; isolated candidate edges once)
+  for (int k = E.rank; k < ncur; k += E.size) {
+    const int v = L[k];
+    if (v < 0) continue;
+    const int u = F.ia[v];
+    const bool win = __ldcg(F.key + u) == claim_key(t, v);
+    const bool twin = dget(F.deg, u) == 1 && __ldcg(F.ia + u) == v && u < v;
+    if (win && !twin) add_removed(F, G, q, off, s, u);
+  }
+  qflush(q, F.rem, &G->nrem[s % 3], F.rem, &G->nrem[s % 3]);
+  cflush(q, F.chunk, &G->nchunk[s % 3]);
+  tm.lap(G, 1);
+  E.sync();
+  tm.lap(G, 4);
+  // C: removal
+  const int nr = vld(&G->nrem[s % 3]);
+  remove_set(E, F, G, q, off, nbr, s, nxt, S.p2, edges, walked);
+  tm.lap(G, 2);
+  E.sync();
+  tm.lap(G, 5);
+  S.p1 = nxt;
+  S.d1 += nr;
+  S.forced += nr;
+  S.cycle += nr;
+  S.sweeps += 1;
+  S.s += 1;
+  S.tg += 1;
+  if (nr == 0) S.phase = F_TRI;
+}
+
+// static adjacency test, binary search in the shorter slice
+__device__ __forceinline__ bool adjacent(const int* off, const int* nbr, int a, int b) {
+  if (off[a + 1] - off[a] > off[b + 1] - off[b]) {
+    const int t = a;
+    a = b;
+    b = t;
+  }
+  int lo = off[a], hi = off[a + 1] - 1;
+  while (lo <= hi) {
+    const int mid = (lo + hi) >> 1;
+    const int y = __ldg(nbr + mid);
+    if (y == b) return true;
+    if (y < b) lo = mid + 1;
+    else hi = mid - 1;
+  }
+  return false;
+}
+
+// One triangle sweep (pure.py:113) over the pending list l2[p2].
+__device__ __forceinline__ void sweep_tri(const Ex& E, const Front& F, FrontCtl* G, BlockQ* q,
+                                          const int* off, const int* nbr, St& S,
+                                          long long* edges, long long* walked) {
+  const int lane = threadIdx.x & 31;
+  const int s = S.s;
+  const int cur = S.p2, nxt = S.p2 ^ 1;
+  const int ncur = vld(&G->cnt2[cur]);
+  if (ncur == 0) {
+    S.sweeps += 1;
+    S.phase = F_HD;
+    return;
+  }
+  int* L = F.l2[cur];
+  int* ncand = &G->ncand[s % 3];
+  if (E.rank == 0) {
+    G->cnt2[nxt] = 0;
+    G->ropen[S.tg % 3] = 0;
+    next_slots(G, s);
+    G->items += (unsigned long long)ncur;
+  }
+  // A: valid candidates (degree 2, live neighbours adjacent)
+  for (int k = E.rank; k < ncur; k += E.size) {
+    const int v = L[k];
+    if (dget(F.deg, v) != 2) continue;
+    int a, b;
+    two_from_sums(F, v, &a, &b);
+    if (a < 0 || a >= b || dget(F.deg, a) <= 0 || dget(F.deg, b) <= 0) {
+      atomicExch(&G->err, 1);
+      continue;
+    }
+    if (adjacent(off, nbr, a, b)) {
+      F.ia[v] = a;
+      F.ib[v] = b;
+      F.st[v] = 3;  // undecided
+      qpush(q, 0, F.cand, ncand, v);
+    }
+  }
+  qflush(q, F.cand, ncand, F.cand, ncand);
+  E.sync();
+  const int nc = vld(ncand);
+  int tri = 0;
+  if (nc > 0) {
+    while (true) {
+      const int t = S.tg;
+      int* open = &G->ropen[t % 3];
+      if (E.rank == 0) G->ropen[(t + 1) % 3] = 0;
+      for (int k = E.rank; k < nc; k += E.size) {
+        const int v = F.cand[k];
+        if (__ldcg(F.st + v) != 3) continue;
+        const unsigned long long key = claim_key(t, v);
+        atomicMax(F.key + v, key);
+        atomicMax(F.key + F.ia[v], key);
+        atomicMax(F.key + F.ib[v], key);
+      }
+      E.sync();
+      int still = 0;
+      for (int k = E.rank; k < nc; k += E.size) {
+        const int v = F.cand[k];
+        if (__ldcg(F.st + v) != 3) continue;
+        const int u = F.ia[v], x = F.ib[v];
+        if (__ldcg(F.rs + v) == s || __ldcg(F.rs + u) == s || __ldcg(F.rs + x) == s) {
+          F.st[v] = 4;  // meets an applied triangle's removed vertex: out
+        } else {
+          const unsigned long long key = claim_key(t, v);
+          if (__ldcg(F.key + v) == key && __ldcg(F.key + u) == key && __ldcg(F.key + x) == key) {
+            F.st[v] = 5;  // in
+            add_removed(F, G, q, off, s, u);
+            add_removed(F, G, q, off, s, x);
+          } else {
+            still = 1;
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, still) && lane == 0) atomicOr(open, 1);
+      qflush(q, F.rem, &G->nrem[s % 3], F.rem, &G->nrem[s % 3]);
+      cflush(q, F.chunk, &G->nchunk[s % 3]);
+      S.tg += 1;
+      E.sync();
+      if (!vld(open)) break;
+    }
+    const int nr = vld(&G->nrem[s % 3]);
+    remove_set(E, F, G, q, off, nbr, s, S.p1, nxt, edges, walked);
+    E.sync();
+    tri = nr / 2;
+  }
+  S.p2 = nxt;
+  S.d2t += tri;
+  S.forced += 2 * tri;
+  S.cycle += tri;
+  S.sweeps += 1;
+  S.s += 1;
+  S.phase = F_HD;
+}
+
+// The high-degree point of a cycle (pure.py:158): a full pass for the
+// candidates and the maximum live degree; block 0 applies an in-order sweep
+// when a real budget fires it (then the frontier lists and sums are rebuilt).
+__device__ __forceinline__ void sweep_hd(const Front& F, FrontCtl* G, BlockQ* q, const int* off,
+                                         const int* nbr, char* wsmem, int n, int budget,
+                                         int* hd_out, St& S, BlockScratch* bs) {
+  const int s = S.s;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, T = gridDim.x * blockDim.x;
+  const int bud = budget - S.forced;
+  if (gt == 0) next_slots(G, s);
+  int ch = 0, dm = 0;
+  for (int v = gt; v < n; v += T) {
+    const int d = dget(F.deg, v);
+    ch += (d > 0 && d > bud);
+    dm = d > dm ? d : dm;
+  }
+  {
+    int vals[2] = {ch, dm};
+    const int op[2] = {0, 2};
+    block_reduce<2>(vals, op, bs);
+    if (threadIdx.x == 0) {
+      if (vals[0]) atomicAdd(&G->ch[s % 3], vals[0]);
+      if (vals[1]) atomicMax(&G->dmax[s % 3], vals[1]);
+    }
+  }
+  grid_barrier(&G->bar);
+  S.passes += 1;
+  const int CH = vld(&G->ch[s % 3]), DM = vld(&G->dmax[s % 3]);
+  if (bud > kSpecBudget / 2) S.spec_m = max(S.spec_m, DM + S.forced);
+  int applied = 0;
+  if (CH > 0) {
+    if (blockIdx.x == 0) {
+      NodeWs<uint32_t> w = carve_ws<uint32_t>(wsmem, n, bs, off, nbr);
+      PassRet h = high_degree_pass(w, 0, n - 1, bud, hd_out, 0);
+      for (int k = threadIdx.x; k < h.pos; k += blockDim.x) F.forced[hd_out[k]] = 1;
+      if (threadIdx.x == 0) {
+        G->hd_applied = h.applied;
+        G->edges += (unsigned long long)h.edges;
+        G->cnt1[S.p1] = 0;  // rebuilt below
+        G->cnt2[S.p2] = 0;
+      }
+    }
+    grid_barrier(&G->bar);
+    applied = vld(&G->hd_applied);
+    if (applied > 0) {
+      for (int v = gt; v < n; v += T) {
+        const int d = dget(F.deg, v);
+        if (d == 1) qpush(q, 0, F.l1[S.p1], &G->cnt1[S.p1], v);
+        else if (d == 2) qpush(q, 1, F.l2[S.p2], &G->cnt2[S.p2], v);
+      }
+      qflush(q, F.l1[S.p1], &G->cnt1[S.p1], F.l2[S.p2], &G->cnt2[S.p2]);
+      init_sums(F, off, nbr, n, false);  // the block-level sweep did not maintain them
+      S.passes += 1;
+    }
+    // the block-level sweep used ic[0, candidates) as scratch
+    if (blockIdx.x == 0) {
+      NodeWs<uint32_t> w = carve_ws<uint32_t>(wsmem, n, bs, off, nbr);
+      for (int v = threadIdx.x; v < n; v += blockDim.x) w.ic[v] = 0;
+    }
+    grid_barrier(&G->bar);
+  }
+  S.hd += applied;
+  S.forced += applied;
+  S.cycle += applied;
+  S.s += 1;
+  if (S.cycle == 0) {
+    S.phase = F_DONE;
+  } else {
+    S.cycle = 0;
+    S.phase = F_D1;
+  }
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kRootGridThreads, 1)
+    k_root_front(int n, const int32_t* off, const int32_t* nbr, char* wsmem, char* fmem,
+                 int budget, int32_t* out, long long* ret, int init, void* ctl_mem,
+                 int solo_max) {
+  __shared__ BlockScratch bs;
+  __shared__ BlockQ q;
+  if (threadIdx.x == 0) q.cnt[0] = q.cnt[1] = q.ccnt = q.cused = 0;
+  init_block_scratch(&bs);
+  FrontCtl* G = (FrontCtl*)ctl_mem;  // zeroed by the host before the launch
+  Front F;
+  {
+    const size_t nn = ((size_t)n + 31) & ~(size_t)31;
+    F.deg = (uint32_t*)wsmem;
+    unsigned long long* lp = (unsigned long long*)fmem;
+    F.key = lp;
+    F.nsum = lp + nn;
+    F.nsq = lp + 2 * nn;
+    int* ip = (int*)(lp + 3 * nn);
+    F.ia = ip;
+    F.ib = ip + nn;
+    F.st = ip + 2 * nn;
+    F.rs = ip + 3 * nn;
+    F.l1[0] = ip + 4 * nn;
+    F.l1[1] = ip + 5 * nn;
+    F.l2[0] = ip + 6 * nn;
+    F.l2[1] = ip + 7 * nn;
+    F.rem = ip + 8 * nn;
+    F.cand = ip + 9 * nn;
+    F.forced = (uint8_t*)(ip + 10 * nn);
+    F.chunk = (int2*)(F.forced + nn);
+  }
+  int* hd_out = F.cand;  // the high-degree sweep's ids (cand is free outside triangle sweeps)
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, T = gridDim.x * blockDim.x;
+  const bool real_budget = budget <= kSpecBudget / 2;
+  // init: degrees, tags, the first frontier (every degree-1 / degree-2 vertex)
+  for (int v = gt; v < n; v += T) {
+    const int d = init ? off[v + 1] - off[v] : (int)F.deg[v];
+    if (init) F.deg[v] = (uint32_t)d;
+    F.key[v] = 0ull;
+    F.rs[v] = 0;
+    F.forced[v] = 0;
+    if (d == 1) qpush(&q, 0, F.l1[0], &G->cnt1[0], v);
+    else if (d == 2) qpush(&q, 1, F.l2[0], &G->cnt2[0], v);
+  }
+  qflush(&q, F.l1[0], &G->cnt1[0], F.l2[0], &G->cnt2[0]);
+  if (real_budget) {  // scratch of the block-level high-degree sweep
+    NodeWs<uint32_t> w = carve_ws<uint32_t>(wsmem, n, &bs, off, nbr);
+    for (int v = gt; v < n; v += T) {
+      w.flag[v] = 0;
+      w.ic[v] = 0;
+    }
+  }
+  grid_barrier(&G->bar);  // degrees initialised
+  init_sums(F, off, nbr, n, init != 0);
+  grid_barrier(&G->bar);
+  St S{F_D1, 0, 0, 1, 1, 0, 0, 0, 0, 0, -1, 0, 1, 0};
+  long long edges = 0, walked = 0;
+  const Ex EG{gt, T, true, &G->bar};
+  const Ex EB{(int)threadIdx.x, (int)blockDim.x, false, &G->bar};
+  // %globaltimer profile (thread 0): ns in solo segments, grid degree-one
+  // sweeps, grid triangle sweeps, high-degree points
+  unsigned long long tcat[4] = {0, 0, 0, 0}, tprev = gt == 0 ? globaltimer() : 0;
+  auto tick = [&](int c) {
+    if (gt == 0) {
+      const unsigned long long now = globaltimer();
+      tcat[c] += now - tprev;
+      tprev = now;
+    }
+  };
+  while (S.phase != F_DONE) {
+    if (vld(&G->err)) break;
+    const int work = S.phase == F_D1 ? vld(&G->cnt1[S.p1]) : vld(&G->cnt2[S.p2]);
+    if (S.phase != F_HD && work < solo_max) {
+      if (blockIdx.x == 0) {
+        while (true) {
+          if (S.phase == F_D1) sweep_d1(EB, F, G, &q, off, nbr, S, &edges, &walked);
+          else sweep_tri(EB, F, G, &q, off, nbr, S, &edges, &walked);
+          S.solo += 1;
+          if (S.phase == F_HD || vld(&G->err)) break;
+          const int wk = S.phase == F_D1 ? vld(&G->cnt1[S.p1]) : vld(&G->cnt2[S.p2]);
+          if (wk >= solo_max) break;
+        }
+        if (threadIdx.x == 0) G->st = S;
+      }
+      grid_barrier(&G->bar);
+      {
+        const volatile int* r = (const volatile int*)&G->st;
+        int* p = (int*)&S;
+        for (int i = 0; i < (int)(sizeof(St) / sizeof(int)); ++i) p[i] = r[i];
+      }
+      tick(0);
+      continue;
+    }
+    const int c = S.phase == F_D1 ? 1 : S.phase == F_TRI ? 2 : 3;
+    if (S.phase == F_D1) sweep_d1(EG, F, G, &q, off, nbr, S, &edges, &walked);
+    else if (S.phase == F_TRI) sweep_tri(EG, F, G, &q, off, nbr, S, &edges, &walked);
+    else sweep_hd(F, G, &q, off, nbr, wsmem, n, budget, hd_out, S, &bs);
+    tick(c);
+  }
+  // forced ids in index order (each thread owns a contiguous chunk), the
+  // live window, and the totals
+  int b, e;
+  {
+    const long long per = ((long long)n + T - 1) / T;
+    const long long s0 = (long long)gt * per, t0 = s0 + per;
+    b = (int)(s0 < n ? s0 : n);
+    e = (int)(t0 < n ? t0 : n);
+  }
+  int cnt = 0, mn = kInf, mx = -1;
+  for (int v = b; v < e; ++v) {
+    cnt += F.forced[v];
+    if (dget(F.deg, v) > 0) {
+      mn = min(mn, v);
+      mx = v;
+    }
+  }
+  int btot;
+  const int at = block_exscan(cnt, &bs, &btot);
+  {
+    int vals[2] = {mn, mx};
+    const int op[2] = {1, 2};
+    block_reduce<2>(vals, op, &bs);
+    if (threadIdx.x == 0) {
+      G->partial[blockIdx.x] = btot;
+      if (vals[0] != kInf) atomicMax(&G->wlo, kInf - vals[0]);
+      if (vals[1] >= 0) atomicMax(&G->whi, vals[1] + 1);
+    }
+    long long ew[2] = {edges, walked};
+    for (int k = 0; k < 2; ++k) {
+      long long x = ew[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if ((threadIdx.x & 31) == 0 && x)
+        atomicAdd(k ? &G->walked : &G->edges, (unsigned long long)x);
+    }
+  }
+  grid_barrier(&G->bar);
+  int base, total;
+  {
+    const volatile int* partial = G->partial;
+    if (threadIdx.x < 32) {
+      int before = 0, tot = 0;
+      for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) {
+        const int p = partial[i];
+        tot += p;
+        if (i < (int)blockIdx.x) before += p;
+      }
+      before = __reduce_add_sync(0xffffffffu, before);
+      tot = __reduce_add_sync(0xffffffffu, tot);
+      if (threadIdx.x == 0) {
+        bs.bc[12] = before;
+        bs.bc[13] = tot;
+      }
+    }
+    __syncthreads();
+    base = bs.bc[12];
+    total = bs.bc[13];
+  }
+  int o = base + at;
+  for (int v = b; v < e; ++v)
+    if (F.forced[v]) out[o++] = v;
+  if (gt == 0) {
+    const int whi = vld(&G->whi);
+    const int lo = kInf - vld(&G->wlo), hi = whi - 1;
+    ret[0] = S.forced;
+    ret[1] = S.d1;
+    ret[2] = S.d2t;
+    ret[3] = S.hd;
+    ret[4] = (long long)*(volatile unsigned long long*)&G->edges;
+    if (hi < 0) {  // pure.py:238 empty window
+      ret[5] = n > 1 ? n : 1;
+      ret[6] = 0;
+    } else {
+      ret[5] = lo;
+      ret[6] = hi;
+    }
+    ret[7] = total;
+    ret[8] = vld(&G->err);
+    ret[9] = S.spec_m;
+    ret[10] = S.passes + 1;  // + the final pass
+    ret[11] = S.sweeps;
+    ret[12] = S.solo;
+    ret[13] = (long long)*(volatile unsigned long long*)&G->walked;
+    ret[14] = (long long)*(volatile unsigned long long*)&G->items;
+    for (int k = 0; k < 4; ++k) ret[15 + k] = (long long)tcat[k];
+    for (int k = 0; k < 6; ++k) ret[19 + k] = (long long)G->tph[k];
+  }
+}
+
+size_t root_front_ctl_bytes() { return sizeof(FrontCtl); }
+
+size_t root_front_bytes(int n, long long m2) {
+  const size_t nn = ((size_t)n + 31) & ~(size_t)31;
+  // key, nsum, nsq, 10 int arrays, forced, then the chunk list: every vertex
+  // is removed at most once, so a step's chunks number at most n + m2 / kChunk
+  return 24 * nn + 40 * nn + nn + 8 * ((size_t)n + (size_t)m2 / kChunk + 1) + 256;
+}
+
+int root_front_blocks() {
+  static thread_local int dev_cached = -1, blocks = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (dev != dev_cached) {
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_root_front, kRootGridThreads, 0);
+    per_sm = per_sm > 2 ? 2 : per_sm;
+    blocks = sms * per_sm;
+    if (blocks > kRootGridMaxBlocks) blocks = kRootGridMaxBlocks;
+    dev_cached = dev;
+  }
+  return blocks;
+}
+
+cudaError_t root_front_launch(int n, const int32_t* off, const int32_t* nbr, char* ws,
+                              char* front, int budget, int32_t* out, long long* ret, int init,
+                              void* ctl) {
+  const int blocks = root_front_blocks();
+  if (blocks < 1) return cudaErrorInvalidConfiguration;
+  cudaError_t e = cudaMemsetAsync(ctl, 0, sizeof(FrontCtl), cudaStreamPerThread);
+  if (e != cudaSuccess) return e;
+  // VCG_FRONT_SOLO: the frontier size below which one block sweeps alone
+  static const int solo_env = getenv("VCG_FRONT_SOLO") ? atoi(getenv("VCG_FRONT_SOLO")) : -1;
+  int solo_max = solo_env >= 0 ? solo_env : kSolo;
+  void* args[] = {&n, &off, &nbr, &ws, &front, &budget, &out, &ret, &init, &ctl, &solo_max};
+  return cudaLaunchCooperativeKernel((const void*)k_root_front, dim3(blocks),
+                                     dim3(kRootGridThreads), args, 0, cudaStreamPerThread);
+}
+
+}  // namespace vcg

@@ -23,4 +23,17 @@ int root_grid_blocks();
 cudaError_t root_grid_launch(int n, const int32_t* off, const int32_t* nbr, char* ws, int budget,
                              int32_t* out, long long* ret, int init, void* ctl);
 
+// Frontier-driven any-order variant (root_front.cu, the solve path): same
+// forced set and rule counts, forced ids in index order.  `front` holds
+// root_front_bytes(n) bytes of scratch, `ctl` root_front_ctl_bytes() (zeroed
+// by the launch).  ret (int64[15]): as root_grid_launch's first 11 (ret[10] =
+// full passes over the degree array), then sweeps, sweeps run by one block,
+// adjacency entries walked, frontier entries examined.
+size_t root_front_ctl_bytes();
+size_t root_front_bytes(int n, long long m2);
+int root_front_blocks();
+cudaError_t root_front_launch(int n, const int32_t* off, const int32_t* nbr, char* ws,
+                              char* front, int budget, int32_t* out, long long* ret, int init,
+                              void* ctl);
+
 }  // namespace vcg

@@ -245,9 +245,28 @@ def _assemble_cover(g: StaticGraph, pre: Preprocessed, local: list[int]) -> list
 
 
 def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
-    """engine.py:561 solve: MVC, or PVC's decision form with budget k."""
+    """engine.py:561 solve: MVC, or PVC's decision form with budget k.
+
+    Parallel MVC solves skip the greedy cover of the input (the reference's
+    root bound, preprocess.py:28): the root rules run with a speculative
+    budget and report the smallest greedy value they assumed
+    (``spec_need``).  Every cover -- the greedy one included -- has at least
+    the optimum's size, so an optimum >= spec_need certifies the reduction;
+    otherwise the greedy is computed, and if it is below spec_need too the
+    solve reruns with the real bound.  Deterministic solves compute the
+    greedy up front (the reference's search order needs its exact value)."""
     cfg = config if config is not None else SolverConfig()
     cfg.validate()
+    lazy = cfg.mode == "mvc" and not cfg.deterministic and cfg.use_root_reduce
+    result, pre = _solve(g, cfg, lazy)
+    if lazy and pre.spec_need >= 0:
+        if not (result.exact and result.cover_size >= pre.spec_need):
+            if greedy_bound(g) < pre.spec_need:  # the real bound would have fired
+                result, _ = _solve(g, cfg, False)
+    return result
+
+
+def _solve(g: StaticGraph, cfg: SolverConfig, lazy: bool):
     stats = Stats()
     stats.rule_counts = dict.fromkeys(RULE_KEYS, 0)
     stats.root_vertices_before = g.num_vertices
@@ -257,7 +276,7 @@ def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
     bound = cfg.k if cfg.mode == "pvc" else None
     pre = root_reduce(g, enabled=cfg.use_root_reduce, crown=cfg.use_crown, bound=bound,
                       width_override=cfg.width, need_greedy_original=bound is None,
-                      ordered=False, lazy_greedy=bound is None)
+                      ordered=False, lazy_greedy=lazy)
     stats.phase_seconds["root_reduce"] = time.perf_counter() - t0
     for key, val in pre.rule_counts.items():
         stats.rule_counts[key] = stats.rule_counts.get(key, 0) + val
@@ -270,7 +289,7 @@ def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
                          root_kernel=dict(pre.kernel))
 
     if cfg.mode == "pvc" and pre.forced_count > cfg.k:
-        return result
+        return result, pre
 
     if rg.num_edges == 0:
         result.found = True
@@ -278,7 +297,7 @@ def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
         if cfg.record_cover:
             result.cover = _assemble_cover(g, pre, [])
             result.cover_size = len(result.cover)
-        return result
+        return result, pre
 
     k_red = cfg.k - pre.forced_count if cfg.mode == "pvc" else None
     greedy_reduced = pre.greedy_reduced
@@ -290,7 +309,7 @@ def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
                 _, members = greedy_bound(rg, members=True)
                 result.cover = _assemble_cover(g, pre, members)
                 result.cover_size = len(result.cover)
-            return result
+            return result, pre
         best_init = min(greedy_reduced, k_red + 1)
         achieved_init = greedy_reduced <= k_red + 1
     else:
@@ -355,7 +374,7 @@ def solve(g: StaticGraph, config: SolverConfig | None = None) -> SolveResult:
         result.cover = _assemble_cover(g, pre, local)
         result.cover_size = len(result.cover)
         stats.phase_seconds["reconstruct"] = time.perf_counter() - t2
-    return result
+    return result, pre
 
 
 def solve_batch(graphs, configs) -> list[SolveResult]:

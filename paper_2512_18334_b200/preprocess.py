@@ -60,6 +60,9 @@ class Preprocessed:
     rule_counts: dict[str, int] = field(default_factory=dict)
     seconds: dict[str, float] = field(default_factory=dict)
     kernel: dict = field(default_factory=dict)  # rule kernels: device ms, launches, scans, kind
+    # lazy_greedy: the smallest greedy_original under which the speculative
+    # reduction equals the reference's (-1: no speculation); see solve()
+    spec_need: int = -1
 
     @property
     def forced(self) -> list[int]:
@@ -80,7 +83,7 @@ class Preprocessed:
 def root_reduce(g: StaticGraph, enabled: bool = True, crown: bool = True,
                 bound: int | None = None, width_override: int | None = None,
                 need_greedy_original: bool = True, ordered: bool = True,
-                lazy_greedy: bool = False) -> Preprocessed:
+                lazy_greedy: bool = False, speculate: bool = True) -> Preprocessed:
     """preprocess.py:77 root_reduce on the device.
 
     ``need_greedy_original=False`` (used by PVC solves, where the bound is k)
@@ -88,18 +91,20 @@ def root_reduce(g: StaticGraph, enabled: bool = True, crown: bool = True,
     ``ordered=False`` (the solve path) returns ``forced`` in index order
     instead of the reference's forcing order -- same set, same rule counts --
     so the device can run the fused order-free sweeps on chip.
-    ``lazy_greedy=True`` (the MVC solve path) lets the library skip the
-    greedy cover of the input when a matching lower bound certifies that it
-    cannot matter; ``greedy_original`` is then -1 and the search starts from
-    ``greedy_reduced`` (achieved)."""
+    ``lazy_greedy=True`` (the MVC solve path) skips the greedy cover of the
+    input: ``greedy_original`` is then -1, the search starts from
+    ``greedy_reduced`` (achieved) and ``spec_need`` says which greedy value
+    the speculative reduction assumed (solve() certifies it against the
+    optimum).  ``speculate=False`` runs the rules with the real bound."""
     n = g.num_vertices
     info = _lib.Preprocessed_t()
-    forced = np.zeros(max(n, 1), dtype=np.int32)
-    vmap = np.zeros(max(n, 1), dtype=np.int64)
+    forced = np.empty(max(n, 1), dtype=np.int32)  # written by the library
+    vmap = np.empty(max(n, 1), dtype=np.int64)
     h = C.c_void_p()
     _lib.check(_lib.lib.vcg_root_reduce(
         g.device().handle,
-        (1 if enabled else 0) | (0 if ordered else 2) | (4 if lazy_greedy else 0), int(crown),
+        (1 if enabled else 0) | (0 if ordered else 2) | (4 if lazy_greedy else 0)
+        | (0 if speculate else 8), int(crown),
         0 if bound is None else (2 if need_greedy_original else 1),
         int(bound) if bound is not None else 0, C.byref(info), forced.ctypes.data,
         vmap.ctypes.data, C.byref(h)))
@@ -116,6 +121,9 @@ def root_reduce(g: StaticGraph, enabled: bool = True, crown: bool = True,
         seconds={"device_reduce": info.seconds[0], "crown": info.seconds[1],
                  "compaction": info.seconds[2]},
         kernel={"ms": info.kernel_ms, "launches": int(info.kernel_launches),
-                "scans": int(info.kernel_scans),
-                "kind": ("none", "block_smem", "block_hbm", "grid")[int(info.kernel_kind)]},
+                "scans": int(info.kernel_scans), "sweeps": int(info.kernel_sweeps),
+                "walked": int(info.kernel_walked),
+                "kind": ("none", "block_smem", "block_hbm", "grid",
+                         "frontier")[int(info.kernel_kind)]},
+        spec_need=int(info.spec_need) if lazy_greedy else -1,
     )

@@ -4,6 +4,8 @@ induced_subgraph), for the paths the default sizes do not reach:
 * the grid-wide cooperative fixpoint kernel (root_grid.cu), forced on every
   reference fixture with VCG_ROOT_GRID=1 -- same forced ids in the same
   order, same vertex map, rule counts and reduced graph as the reference;
+* the frontier-driven kernel of the solve path (root_front.cu), forced with
+  VCG_ROOT_GRID=2 -- same forced set, counts, map and reduced graph;
 * the device compaction kernels (k_count_kept / k_gather_kept + scans),
   forced with VCG_DEVICE_COMPACT=1, and ``induced_subgraph`` on random keep
   sets against the oracle's restatement of graph.py:99;
@@ -75,6 +77,54 @@ def test_grid_root_solve_path_stats(grid_root):
             assert stats_without_time(r.stats.as_dict()) == exp["stats"], (case["name"], k)
 
 
+@pytest.fixture
+def front_root(monkeypatch):
+    monkeypatch.setenv("VCG_ROOT_GRID", "2")
+    monkeypatch.setenv("VCG_DEVICE_COMPACT", "1")
+
+
+def test_front_root_reduce_same_sets(front_root):
+    """The frontier kernel (root_front.cu, any-order callers) on every
+    reference fixture: the same forced set, rule counts, vertex map and
+    reduced graph as the reference (forced ids come back in index order)."""
+    import paper_2512_18334_b200 as vc
+
+    for case in golden("root_reduce.json"):
+        g = _graph(case)
+        pre = vc.root_reduce(g, bound=case["bound"], ordered=False)
+        assert pre.kernel["kind"] == "frontier"
+        assert pre.forced == sorted(case["forced"]), case.get("name")
+        assert pre.vertex_map.tolist() == case["vertex_map"]
+        assert pre.rule_counts == case["rule_counts"]
+        assert pre.greedy_original == case["greedy_original"]
+        assert pre.greedy_reduced == case["greedy_reduced"]
+        rn = len(case["vertex_map"])
+        _, roff, rnbr = csr(rn, case["reduced_edges"])
+        assert pre.graph.offsets.tolist() == roff.tolist()
+        assert pre.graph.neighbors.tolist() == rnbr.tolist()
+
+
+def test_front_solve_path_stats(front_root):
+    """Deterministic solves (greedy bound up front) and parallel MVC solves
+    (speculative bound certified afterwards) through the frontier kernel."""
+    import paper_2512_18334_b200 as vc
+
+    for case in golden("solve.json")[::2]:
+        g = _graph(case)
+        run = case["runs"]["det"]
+        r = vc.solve(g, vc.SolverConfig(deterministic=True))
+        assert r.cover_size == run["cover_size"], case["name"]
+        assert stats_without_time(r.stats.as_dict()) == run["stats"], case["name"]
+        rp = vc.solve(g, vc.SolverConfig())
+        assert rp.cover_size == run["cover_size"], case["name"]
+        # the certified speculative root reduction is the reference's
+        assert rp.stats.root_vertices_after == run["stats"]["root_vertices_after"], case["name"]
+        for k, exp in case["pvc"].items():
+            r = vc.solve(g, vc.SolverConfig(mode="pvc", k=int(k), deterministic=True))
+            assert r.found == exp["found"], (case["name"], k)
+            assert stats_without_time(r.stats.as_dict()) == exp["stats"], (case["name"], k)
+
+
 def test_induced_subgraph_matches_oracle():
     import oracle
     import paper_2512_18334_b200 as vc
@@ -125,5 +175,9 @@ def test_scale_root_pipeline_matches_oracle(name):
         **exp["stats"],
         "components_per_branch": {str(k): v for k, v in exp["stats"]["components_per_branch"].items()},
     }
-    assert _sha(r.forced, np.int32) == exp["forced_sha256"]  # solve path: same order too
-    assert vc.solve(g, vc.SolverConfig()).cover_size == exp["mvc"]
+    # solve path (frontier kernel): the same set, in index order
+    assert np.array_equal(r.forced_ids, np.sort(np.asarray(pre.forced_ids)))
+    assert r.root_kernel["kind"] == "frontier"
+    rp = vc.solve(g, vc.SolverConfig())
+    assert rp.cover_size == exp["mvc"]
+    assert rp.stats.rule_counts == r.stats.rule_counts

@@ -25,6 +25,9 @@ for name in sys.argv[1:] or ["ba100k", "planted1m"]:
         print(f"{name} mvc={r.cover_size} resident {1e3*(t1-t):.3f} ms  host {1e3*(t2-t1):.3f} ms "
               f"phases={ {k: round(v*1e3, 3) for k, v in r.stats.phase_seconds.items()} } "
               f"nodes={r.stats.tree_nodes_visited}", flush=True)
+    pl = vc.root_reduce(g, ordered=False, lazy_greedy=True)
+    print(f"{name} lazy root_reduce: forced={pl.forced_count} n'={pl.graph.num_vertices} "
+          f"spec_need={pl.spec_need} kernel={pl.kernel}", flush=True)
     t = time.perf_counter()
     pre = vc.root_reduce(g)
     print(f"{name} ordered root_reduce {1e3*(time.perf_counter()-t):.3f} ms seconds={pre.seconds}",
