@@ -225,15 +225,15 @@ def cpu_baseline_sample():
                       f"(oracle/vc_oracle.c), {dt:.1f} s"}
 
 
-def load_traffic():
-    """dram bytes per root-kernel launch from the committed ncu --set full capture."""
-    p = os.path.join(ROOT, "profiles", "r02_root_grid_ncu.json")
+def load_capture():
+    """The committed ncu --set full capture of the root kernel (one planted1m
+    launch): dram bytes per launch, L2 traffic and atomic rates."""
+    p = os.path.join(ROOT, "profiles", "r02_root_front_ncu.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        return d.get("dram_bytes_per_launch"), os.path.relpath(p, ROOT)
+            return json.load(f), os.path.relpath(p, ROOT)
     except (OSError, ValueError):
-        return None, None
+        return {}, None
 
 
 def other_configs(vc, torch, reps=5):
@@ -339,6 +339,7 @@ def run_b200(args):
     l0 = _lib.launch_count()
     total_ms, nodes = 0.0, 0
     kern_ms, kern_launches, kern_scans, kind = 0.0, 0, 0, None
+    kern_sweeps, kern_bars, kern_walked = 0, 0, 0
     clk.mark_start()
     for _ in range(args.steps):
         flush.zero_()  # L2 flush between timed steps (outside the events)
@@ -353,6 +354,9 @@ def run_b200(args):
         kern_ms += r.root_kernel.get("ms", 0.0)
         kern_launches += r.root_kernel.get("launches", 0)
         kern_scans += r.root_kernel.get("scans", 0)
+        kern_sweeps += r.root_kernel.get("sweeps", 0)
+        kern_bars += r.root_kernel.get("barriers", 0)
+        kern_walked += r.root_kernel.get("walked", 0)
         kind = r.root_kernel.get("kind")
     clk.mark_end()
     launches = _lib.launch_count() - l0
@@ -401,13 +405,15 @@ def run_b200(args):
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks.get("hbm_gbs") else \
         "fallback (B200_PROFILING.md)"
     # algorithmic bytes of one root-fixpoint launch ("Kernels"):
-    # the CSR read once (int32 offsets + neighbours), the int32 degree array
-    # written once and read once per grid-wide scan
-    per_launch_scans = kern_scans / max(kern_launches, 1)
-    alg_bytes = 4 * (n + 1) + 8 * m + 4 * n * (per_launch_scans + 1)
-    launch_ms = kern_ms / max(kern_launches, 1)
+    # what any fixpoint must touch -- the CSR read once (int32 offsets +
+    # neighbours) and the int32 degree array written and read once
+    L = max(kern_launches, 1)
+    per_launch_scans = kern_scans / L
+    alg_bytes = 4 * (n + 1) + 8 * m + 8 * n
+    launch_ms = kern_ms / L
     achieved = alg_bytes / (launch_ms * 1e-3) / 1e9 if launch_ms else 0.0
-    traffic, traffic_src = load_traffic()
+    cap, traffic_src = load_capture()
+    traffic = cap.get("dram_bytes_per_launch")
     tts = total_ms / args.steps * 1e-3
     line = {
         "metric": METRIC,
@@ -433,12 +439,23 @@ def run_b200(args):
                 "input": "pinned host numpy arrays (int64 offsets, int32 neighbours)"},
         "gpu_launches": launches,
         "roofline": {
-            "bound": "hbm", "kernel": f"k_root_grid (root fixpoint, kind={kind})",
+            "bound": "hbm", "kernel": f"k_root_front (root fixpoint, kind={kind})",
             "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-            "algorithmic_bytes_per_launch": alg_bytes, "scans_per_launch": per_launch_scans,
+            "algorithmic_bytes_per_launch": alg_bytes, "full_passes_per_launch": per_launch_scans,
             "launch_ms": launch_ms, "launches_per_step": kern_launches / args.steps,
             "kernel_share_of_step": kern_ms / total_ms if total_ms else None,
+            # what binds it: sequential sweeps (the reference's sweep order)
+            # separated by grid barriers, each a few L2 round trips deep
+            "l2_from_capture": {k: cap.get(k) for k in (
+                "l2_bytes", "l2_gbs", "l2_sector_throughput_pct_of_peak", "l2_atomic_requests",
+                "l2_atomic_requests_per_s", "l2_atomic_unit_active_pct_of_peak",
+                "issue_active_pct", "top_stalls_per_issue")} if cap else None,
+            "latency": {"sweeps_per_launch": kern_sweeps / L,
+                        "grid_barriers_per_launch": kern_bars / L,
+                        "adjacency_entries_walked_per_launch": kern_walked / L,
+                        "us_per_barrier_interval": (launch_ms * 1e3 / (kern_bars / L)
+                                                    if kern_bars else None)},
         },
         "clocks": clk.summary(),
     }

@@ -85,9 +85,10 @@ typedef struct {
   int64_t kernel_launches;
   int64_t kernel_scans;
   int64_t kernel_kind;
-  /* frontier kernel (kind 4): sweeps and adjacency entries walked */
+  /* frontier kernel (kind 4): sweeps, adjacency entries walked, grid barriers */
   int64_t kernel_sweeps;
   int64_t kernel_walked;
+  int64_t kernel_barriers;
   /* VCG_ROOT_LAZY_GREEDY: the smallest greedy_original under which the
    * speculative-budget rules equal the reference's (-1: no speculation) */
   int64_t spec_need;

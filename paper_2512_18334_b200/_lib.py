@@ -30,7 +30,7 @@ class Preprocessed_t(C.Structure):
         ("greedy_original", I64), ("greedy_reduced", I64), ("max_degree_reduced", I64),
         ("rule_counts", I64 * 4), ("seconds", C.c_double * 3),
         ("kernel_ms", C.c_double), ("kernel_launches", I64), ("kernel_scans", I64),
-        ("kernel_kind", I64), ("kernel_sweeps", I64), ("kernel_walked", I64),
+        ("kernel_kind", I64), ("kernel_sweeps", I64), ("kernel_walked", I64), ("kernel_barriers", I64),
         ("spec_need", I64),
     ]
 

@@ -899,7 +899,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
       }
       CK(cudaGetLastError());
       CK(cudaEventRecord(rk1, cudaStreamPerThread));
-      CK(cudaMemcpy(ret, dret.p, fast ? 144 : use_front ? 200 : use_grid ? 88 : 80,
+      CK(cudaMemcpy(ret, dret.p, fast ? 144 : use_front ? 208 : use_grid ? 88 : 80,
                     cudaMemcpyDeviceToHost));
       {
         float kms = 0.f;
@@ -910,6 +910,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
         if (use_front) {
           info->kernel_sweeps += ret[11];
           info->kernel_walked += ret[13];
+          info->kernel_barriers += ret[25];
         }
       }
       if (fast && trace_on())

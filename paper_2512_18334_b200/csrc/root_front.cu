@@ -71,7 +71,7 @@ struct FrontCtl {
   int ropen[3];                               // triangle claim rounds, by claim tag mod 3
   int err, hd_applied, wlo, whi;  // wlo = max(INT_MAX - lowest live), whi = max(highest live + 1)
   unsigned long long edges, walked, items;
-  unsigned bar;                               // grid_barrier word
+  unsigned bar, nbar;                         // grid_barrier word, barriers passed
   unsigned long long tph[8];                  // phase times (ns, thread 0): A, B, C, barriers
   St st;                                      // block 0 -> grid after a solo segment
   int partial[kRootGridMaxBlocks];
@@ -99,6 +99,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
     const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
     __threadfence();
     const unsigned old = atomicAdd(bar, inc);
+    if (blockIdx.x == 0) bar[1] += 1;  // barriers passed (FrontCtl::nbar)
     unsigned ns = 32;
     while (((old ^ *(volatile unsigned*)bar) & 0x80000000u) == 0) {
       __nanosleep(ns);
@@ -780,6 +781,7 @@ __global__ void __launch_bounds__(kRootGridThreads, 1)
     ret[14] = (long long)*(volatile unsigned long long*)&G->items;
     for (int k = 0; k < 4; ++k) ret[15 + k] = (long long)tcat[k];
     for (int k = 0; k < 6; ++k) ret[19 + k] = (long long)G->tph[k];
+    ret[25] = (long long)*(volatile unsigned*)&G->nbar;
   }
 }
 

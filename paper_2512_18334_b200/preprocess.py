@@ -122,7 +122,7 @@ def root_reduce(g: StaticGraph, enabled: bool = True, crown: bool = True,
                  "compaction": info.seconds[2]},
         kernel={"ms": info.kernel_ms, "launches": int(info.kernel_launches),
                 "scans": int(info.kernel_scans), "sweeps": int(info.kernel_sweeps),
-                "walked": int(info.kernel_walked),
+                "walked": int(info.kernel_walked), "barriers": int(info.kernel_barriers),
                 "kind": ("none", "block_smem", "block_hbm", "grid",
                          "frontier")[int(info.kernel_kind)]},
         spec_need=int(info.spec_need) if lazy_greedy else -1,
