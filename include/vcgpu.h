@@ -19,9 +19,10 @@
  *   vcg_search                             <- engine.py:160 _Engine.run (the
  *                                            threaded search behind solve(),
  *                                            engine.py:561)
- *   vcg_node_op                            <- kernels/__init__.py:36-47, the
+ *   vcg_node_op                            <- kernels/__init__.py:33-44, the
  *                                            per-node kernel API (pure.py /
  *                                            _native.pyx), one node per call
+ *   vcg_brute_force_mvc                    <- oracle.py:28 brute_force_mvc
  */
 #ifndef VCGPU_H
 #define VCGPU_H
@@ -157,6 +158,14 @@ typedef struct {
                                  takes 1/gpu_share of the resident block slots.  Calls
                                  from different host threads run concurrently (each
                                  thread has its own stream and pooled buffers). */
+  int32_t* registry_out;      /* nullable: receives the registry after the search,
+                                 entry i at [12 i, 12 i + 12): best key (2 best +
+                                 !achieved), live count, link (parent / ancestor, -1 at
+                                 the root), kind (0 child, 1 parent), sum, sum_achieved,
+                                 initial_sum, folded_total, first_child, nchild,
+                                 discovery_done, child_folded (registry.py:24-88) */
+  int64_t registry_cap;       /* entries registry_out holds; a larger registry is not
+                                 copied (registry_entries still reports its size) */
 } vcg_search_config;
 
 typedef struct {
@@ -230,12 +239,24 @@ int vcg_expand(const vcg_graph* g, const vcg_expand_config* cfg, vcg_expand_resu
  * op: 0 degree_one_pass, 1 degree_two_triangle_pass, 2 high_degree_pass,
  *     3 reduce_fixpoint, 4 recompute_bounds, 5 select_max_degree,
  *     6 count_live, 7 remove_vertex, 8 remove_neighbors,
- *     9 component of vertex `v` (bfs_component result set)
+ *     9 component of vertex `v` (bfs_component result set, index order),
+ *     10 bfs_component (pure.py:258): out[0,n) = visited (in/out), out[n,2n) =
+ *        the BFS queue, budget = stamp, v = source,
+ *     11 next_live_unvisited (pure.py:297): out[0,n) = visited, budget =
+ *        stamp, lo = start,
+ *     12 greedy_cover (pure.py:306): picks to out[pos..], ret = {size, pos}
  * deg: host uint32[n] in/out.  out: host int32 (capacity 4n+4) in/out.
  * ret: host int64[8], op-specific (same tuples as the reference). */
 int vcg_node_op(int op, int width, int64_t n, const int64_t* offsets, const int32_t* neighbors,
                 uint32_t* deg, int64_t lo, int64_t hi, int64_t budget, int64_t v, int32_t* out,
                 int64_t pos, int64_t* ret);
+
+/* Exhaustive minimum vertex cover of a small graph (n <= 26), every vertex
+ * subset checked on the device: *size = the minimum, witness (capacity n,
+ * nullable) = the lexicographically smallest minimum cover in increasing
+ * order (oracle.py:28 brute_force_mvc; n > 26 fails with VCG_EINVAL). */
+int vcg_brute_force_mvc(int64_t n, const int64_t* offsets, const int32_t* neighbors,
+                        int64_t* size, int32_t* witness);
 
 const char* vcg_last_error(void);
 /* Number of kernels this library has launched so far (process-wide). */

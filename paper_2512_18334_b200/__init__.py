@@ -7,6 +7,7 @@ sm_100a CUDA kernels behind the C-ABI in ``include/vcgpu.h``.
 """
 
 from .engine import SolveResult, SolverConfig, Stats, solve, solve_batch
+from .exhaustive import brute_force_mvc
 from .graph import StaticGraph, build_csr, induced_subgraph
 from .preprocess import Preprocessed, greedy_bound, root_reduce, select_width
 
@@ -20,6 +21,7 @@ __all__ = [
     "SolverConfig",
     "StaticGraph",
     "Stats",
+    "brute_force_mvc",
     "build_csr",
     "greedy_bound",
     "induced_subgraph",

@@ -43,7 +43,7 @@ class SearchConfig_t(C.Structure):
         ("workers", C.c_int), ("threads", C.c_int), ("worklist_threshold", I64),
         ("timeout", C.c_double), ("check_registry", C.c_int), ("record_cover", C.c_int),
         ("cover_out", C.c_void_p), ("root_deg", C.c_void_p), ("warp_limit", C.c_int),
-        ("gpu_share", C.c_int),
+        ("gpu_share", C.c_int), ("registry_out", C.c_void_p), ("registry_cap", I64),
     ]
 
 
@@ -79,7 +79,7 @@ EXPORTS = (
     "vcg_graph_create", "vcg_graph_create_borrowed", "vcg_graph_destroy", "vcg_graph_num_vertices", "vcg_graph_num_edges",
     "vcg_graph_download", "vcg_induced_subgraph", "vcg_greedy_bound", "vcg_root_reduce",
     "vcg_search", "vcg_node_op", "vcg_last_error", "vcg_device_count", "vcg_launch_count",
-    "vcg_set_device", "vcg_get_device", "vcg_expand", "vcg_shutdown",
+    "vcg_set_device", "vcg_get_device", "vcg_expand", "vcg_shutdown", "vcg_brute_force_mvc",
 )
 
 
@@ -116,6 +116,7 @@ def _load():
     lib.vcg_search.argtypes = [P, C.POINTER(SearchConfig_t), C.POINTER(SearchResult_t), P]
     lib.vcg_expand.argtypes = [P, C.POINTER(ExpandConfig_t), C.POINTER(ExpandResult_t), P, P, I64]
     lib.vcg_node_op.argtypes = [C.c_int, C.c_int, I64, P, P, P, I64, I64, I64, I64, P, I64, P]
+    lib.vcg_brute_force_mvc.argtypes = [I64, P, P, C.POINTER(I64), P]
     lib.vcg_shutdown.restype = None
     return lib
 

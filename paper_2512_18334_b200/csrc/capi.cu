@@ -97,6 +97,9 @@ extern "C" void vcg_shutdown(void) {
 }
 
 extern "C" const char* vcg_last_error(void) { return g_err.c_str(); }
+// error reporting for the library's other translation units
+int vcg_fail_external(int code, const char* msg) { return fail(code, msg); }
+void vcg_note_launch(int k) { g_launches += (unsigned long long)k; }
 
 extern "C" int vcg_device_count(void) {
   int c = 0;
@@ -527,6 +530,164 @@ static long long ws_total(int n) {
   return ws_bytes<T>(n);
 }
 
+// pure.py:258 bfs_component, one block: the component of a live source in
+// the reference's BFS queue order.  Level by level: every unvisited live
+// neighbour u of the level is claimed by its first discoverer (the lowest
+// queue position, atomicMin on tmin[u]); each level vertex then appends the
+// neighbours it won in adjacency order, at offsets from an exclusive scan over
+// the level in queue order -- exactly the order the sequential queue builds.
+// visited: int32[n] (stamp marks members), queue: int32[n].  Returns
+// {size, degree_sum, min_degree, max_degree, min_vertex, max_vertex}.
+template <typename T>
+__device__ void bfs_component_block(const NodeWs<T>& w, int32_t* visited, int stamp,
+                                    int32_t* queue, int src, long long* r) {
+  if (threadIdx.x == 0) {
+    visited[src] = stamp;
+    queue[0] = src;
+  }
+  __syncthreads();
+  int h = 0, t = 1;
+  while (h < t) {
+    for (int i = h + (int)threadIdx.x; i < t; i += blockDim.x) {
+      const int v = queue[i];
+      for (int j = w.off[v]; j < w.off[v + 1]; ++j) {
+        const int u = w.nbr[j];
+        if (w.deg[u] > 0 && visited[u] != stamp) atomicMin(&w.tmin[u], i);
+      }
+    }
+    __syncthreads();
+    int b, e;
+    my_chunk(h, t - 1, &b, &e);
+    int cnt = 0;
+    for (int i = b; i < e; ++i) {
+      const int v = queue[i];
+      for (int j = w.off[v]; j < w.off[v + 1]; ++j) {
+        const int u = w.nbr[j];
+        cnt += (w.deg[u] > 0 && visited[u] != stamp && w.tmin[u] == i);
+      }
+    }
+    int total;
+    int o = t + block_exscan(cnt, w.bs, &total);
+    for (int i = b; i < e; ++i) {
+      const int v = queue[i];
+      for (int j = w.off[v]; j < w.off[v + 1]; ++j) {
+        const int u = w.nbr[j];
+        if (w.deg[u] > 0 && visited[u] != stamp && w.tmin[u] == i) queue[o++] = u;
+      }
+    }
+    __syncthreads();
+    for (int k = t + (int)threadIdx.x; k < t + total; k += blockDim.x) {
+      const int u = queue[k];
+      visited[u] = stamp;
+      w.tmin[u] = kInf;
+    }
+    __syncthreads();
+    h = t;
+    t += total;
+  }
+  int dsum = 0, mn = kInf, mx = 0, vmn = kInf, vmx = -1;
+  for (int k = threadIdx.x; k < t; k += blockDim.x) {
+    const int x = queue[k], d = w.deg[x];
+    dsum += d;
+    mn = min(mn, d);
+    mx = max(mx, d);
+    vmn = min(vmn, x);
+    vmx = max(vmx, x);
+  }
+  int vals[5] = {dsum, mn, mx, vmn, vmx};
+  const int op[5] = {0, 1, 2, 1, 2};
+  block_reduce<5>(vals, op, w.bs);
+  r[0] = t;
+  for (int k = 0; k < 5; ++k) r[k + 1] = vals[k];
+}
+
+// pure.py:297 next_live_unvisited: first live vertex of [start, hi] without
+// the stamp, or -1
+template <typename T>
+__device__ int next_live_unvisited_block(const NodeWs<T>& w, const int32_t* visited, int stamp,
+                                         int start, int hi) {
+  int best = kInf;
+  for (int v = start + (int)threadIdx.x; v <= hi; v += blockDim.x)
+    if (w.deg[v] > 0 && visited[v] != stamp) {
+      best = v;
+      break;
+    }
+  best = block_min(best, w.bs);
+  return best == kInf ? -1 : best;
+}
+
+// pure.py:306 greedy_cover on the device, one block: repeatedly a live vertex
+// of maximum degree, lowest index first.  Exact level-order restatement: with
+// current maximum degree d, the sequential picks at level d are the
+// lexicographically-first maximal independent set of the degree-d vertices
+// (taking one lowers its degree-d neighbours below d, nothing rises to d), in
+// increasing index order; the MIS is resolved in rounds (a candidate joins
+// once every lower-index candidate neighbour is out, leaves once a neighbour
+// joined).  Picks appended to out[pos..]; deg destroyed.  Returns {size, pos}.
+template <typename T>
+__device__ void greedy_cover_block(const NodeWs<T>& w, int lo, int hi, int32_t* out, int pos,
+                                   long long* r) {
+  int size = 0;
+  int* st = w.ic;  // 0 not a candidate, 1 undecided, 2 out, 3 in
+  for (int v = threadIdx.x; v < w.n; v += blockDim.x) st[v] = 0;
+  __syncthreads();
+  while (lo <= hi) {
+    int dm = 0;
+    for (int v = lo + (int)threadIdx.x; v <= hi; v += blockDim.x) dm = max(dm, (int)w.deg[v]);
+    dm = block_max(dm, w.bs);
+    if (dm == 0) break;
+    for (int v = lo + (int)threadIdx.x; v <= hi; v += blockDim.x) st[v] = w.deg[v] == dm ? 1 : 0;
+    __syncthreads();
+    while (true) {
+      int open = 0;
+      for (int v = lo + (int)threadIdx.x; v <= hi; v += blockDim.x) {
+        if (st[v] != 1) continue;
+        bool out_ = false, wait = false;
+        for (int j = w.off[v]; j < w.off[v + 1]; ++j) {
+          const int u = w.nbr[j];
+          const int su = ((volatile int*)st)[u];
+          if (su == 3) out_ = true;
+          else if (su == 1 && u < v) wait = true;
+        }
+        w.ia[v] = out_ ? 2 : wait ? 1 : 3;
+        open |= wait && !out_;
+      }
+      __syncthreads();
+      for (int v = lo + (int)threadIdx.x; v <= hi; v += blockDim.x)
+        if (st[v] == 1) st[v] = w.ia[v];
+      if (!__syncthreads_or(open)) break;
+    }
+    // the picks in index order, then their removal
+    int b, e;
+    my_chunk(lo, hi, &b, &e);
+    int cnt = 0;
+    for (int v = b; v < e; ++v) cnt += st[v] == 3;
+    int total;
+    int o = pos + block_exscan(cnt, w.bs, &total);
+    for (int v = b; v < e; ++v)
+      if (st[v] == 3) out[o++] = v;
+    __syncthreads();
+    for (int k = pos + (int)threadIdx.x; k < pos + total; k += blockDim.x) {
+      const int v = out[k];
+      for (int j = w.off[v]; j < w.off[v + 1]; ++j) {
+        const int u = w.nbr[j];
+        if (ldv(w.deg, u) > 0 && st[u] != 3) deg_dec(w.deg, u);
+      }
+    }
+    __syncthreads();
+    for (int k = pos + (int)threadIdx.x; k < pos + total; k += blockDim.x) w.deg[out[k]] = 0;
+    for (int v = lo + (int)threadIdx.x; v <= hi; v += blockDim.x) st[v] = 0;
+    __syncthreads();
+    pos += total;
+    size += total;
+    recompute_bounds(w, &lo, &hi);
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < w.n; v += blockDim.x) st[v] = 0;
+  r[0] = size;
+  r[1] = pos;
+}
+
 // single-block kernel running one per-node operation on a global workspace
 template <typename T>
 __global__ void k_node_op(int op, int n, const int32_t* off, const int32_t* nbr, T* deg_io,
@@ -613,6 +774,13 @@ __global__ void k_node_op(int op, int n, const int32_t* off, const int32_t* nbr,
       for (int x = lo; x <= hi; ++x)
         if (w.deg[x] > 0 && w.par[x] == root) out[k++] = x;
     }
+  } else if (op == 10) {
+    // out[0, n) = visited (in/out), out[n, 2n) = queue; stamp = budget
+    bfs_component_block(w, out, budget, out + n, v, r);
+  } else if (op == 11) {
+    r[0] = next_live_unvisited_block(w, out, budget, lo, hi);
+  } else if (op == 12) {
+    greedy_cover_block(w, lo, hi, out, pos, r);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) deg_io[i] = w.deg[i];
@@ -655,7 +823,7 @@ extern "C" int vcg_node_op(int op, int width, int64_t n, const int64_t* offsets,
                            const int32_t* neighbors, uint32_t* deg, int64_t lo, int64_t hi,
                            int64_t budget, int64_t v, int32_t* out, int64_t pos, int64_t* ret) {
   if (int r = need_device()) return r;
-  if (n <= 0 || op < 0 || op > 9) return fail(VCG_EINVAL, "bad node op arguments");
+  if (n <= 0 || op < 0 || op > 12) return fail(VCG_EINVAL, "bad node op arguments");
   if (width == 8) return node_op_t<uint8_t>(op, n, offsets, neighbors, deg, lo, hi, budget, v, out, pos, ret);
   if (width == 16) return node_op_t<uint16_t>(op, n, offsets, neighbors, deg, lo, hi, budget, v, out, pos, ret);
   if (width == 32) return node_op_t<uint32_t>(op, n, offsets, neighbors, deg, lo, hi, budget, v, out, pos, ret);
@@ -1662,6 +1830,13 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
       for (int v = 0; v < n; ++v)
         if (cover[v >> 5] >> (v & 31) & 1u) cfg->cover_out[k++] = v;
       res->cover_size = k;
+    }
+  }
+  if (cfg->registry_out && count > 0 && count <= cfg->registry_cap) {
+    std::vector<int> f(count);
+    for (int k = 0; k < 12; ++k) {
+      CK(cudaMemcpy(f.data(), rb + (size_t)k * reg_cap, (size_t)count * 4, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < count; ++i) cfg->registry_out[(size_t)i * 12 + k] = f[i];
     }
   }
   if (cfg->check_registry && count > 0) {

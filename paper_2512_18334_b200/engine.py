@@ -10,8 +10,9 @@ Differences from the reference, by design:
 * ``workers`` counts thread blocks; 0 (the default) fills every resident
   block slot of the GPU.  ``deterministic=True`` runs one block and replays
   the reference's single-worker schedule exactly (same statistics).
-* The registry lives in HBM; ``SolveResult.registry`` is a summary object
-  exposing the reference's diagnostics (quiescence / conservation).
+* The registry lives in HBM; ``SolveResult.registry`` is a view of it
+  (``Registry``: entries, ``entry(idx)``, the reference's per-entry
+  quiescence / conservation diagnostics), copied back in the parity modes.
 """
 
 from __future__ import annotations
@@ -114,23 +115,96 @@ class Stats:
         }
 
 
-class RegistrySummary:
-    """Post-solve view of the device registry (registry.py:198-224 diagnostics)."""
+@dataclass
+class ChildEntry:
+    """registry.py:24 ChildEntry, as read back from the device registry."""
 
-    def __init__(self, entries: int, violations: int | None):
-        self.entries = entries
-        self._violations = violations
+    best: int
+    achieved: bool
+    live_nodes: int
+    parent: int | None
+
+
+@dataclass
+class ParentEntry:
+    """registry.py:43 ParentEntry, as read back from the device registry."""
+
+    sum: int
+    sum_achieved: bool
+    live_comps: int
+    ancestor: int
+    initial_sum: int
+    folded_total: int
+    children: list[int]
+    discovery_done: bool
+
+
+class Registry:
+    """Post-solve view of the device branch registry (registry.py:79-224):
+    ``entries`` in allocation order, ``entry(idx)``, and the reference's
+    per-entry quiescence / conservation diagnostics.
+
+    The entries are copied back from HBM when the solve asked for them
+    (``check_registry=True`` or ``deterministic=True``); otherwise only the
+    entry count is known and the entry accessors raise."""
+
+    def __init__(self, count: int, raw: np.ndarray | None = None):
+        self.count = count
+        self.entries: list | None = None
+        if raw is not None:
+            self.entries = [self._decode(raw[i]) for i in range(count)]
+
+    @staticmethod
+    def _decode(f) -> ChildEntry | ParentEntry:
+        key, live, link, kind = int(f[0]), int(f[1]), int(f[2]), int(f[3])
+        if kind == 0:
+            return ChildEntry(best=key >> 1, achieved=not (key & 1), live_nodes=live,
+                              parent=None if link < 0 else link)
+        return ParentEntry(sum=int(f[4]), sum_achieved=bool(f[5]), live_comps=live,
+                           ancestor=link, initial_sum=int(f[6]), folded_total=int(f[7]),
+                           children=list(range(int(f[8]), int(f[8]) + int(f[9]))),
+                           discovery_done=bool(f[10]))
 
     def __len__(self) -> int:
+        return self.count
+
+    def _need(self):
+        if self.entries is None:
+            raise RuntimeError("solve with check_registry=True (or deterministic=True) to read "
+                               "the registry entries back from the device")
         return self.entries
 
-    def quiescence_violations(self) -> list[str]:
-        if self._violations is None:
-            raise RuntimeError("solve with check_registry=True to audit the registry")
-        return [f"{self._violations} registry entries violate quiescence/conservation"] \
-            if self._violations else []
+    def entry(self, idx: int):
+        return self._need()[idx]
 
-    conservation_violations = quiescence_violations
+    def quiescence_violations(self) -> list[str]:
+        """registry.py:198 -- entries still holding live counts."""
+        out = []
+        for i, e in enumerate(self._need()):
+            if isinstance(e, ChildEntry):
+                if e.live_nodes != 0:
+                    out.append(f"child entry {i}: live_nodes == {e.live_nodes}")
+            elif e.live_comps != 0:
+                out.append(f"parent entry {i}: live_comps == {e.live_comps}")
+        return out
+
+    def conservation_violations(self) -> list[str]:
+        """registry.py:211 -- parents whose sum disagrees with initial +
+        folded + children bests."""
+        entries = self._need()
+        out = []
+        for i, e in enumerate(entries):
+            if isinstance(e, ParentEntry):
+                kids = [entries[c].best for c in e.children]
+                expected = e.initial_sum + e.folded_total + sum(kids)
+                if e.sum != expected:
+                    out.append(f"parent entry {i}: sum {e.sum} != {expected} "
+                               f"(initial {e.initial_sum} + folded {e.folded_total} "
+                               f"+ children {kids})")
+        return out
+
+
+RegistrySummary = Registry  # round-1 name
 
 
 @dataclass
@@ -144,7 +218,7 @@ class SolveResult:
     stats: Stats
     mode: str
     k: int | None = None
-    registry: RegistrySummary | None = None
+    registry: Registry | None = None
     root_index: int | None = None
     forced_ids: np.ndarray | None = None  # int32 root-forced ids (``forced`` as a list)
     warp_tasks: int = 0     # warp-tier tasks solved
@@ -199,6 +273,13 @@ def run_search(rg: StaticGraph, cfg: SolverConfig, width: int, best_init: int,
         sc.cover_out = cover.ctypes.data
     if config_hook is not None:
         config_hook(sc)  # e.g. seed the search with a subtree root (distributed.py)
+    reg_raw = None
+    if cfg.check_registry or cfg.deterministic:
+        # the registry view (registry.py) is read back for the parity modes
+        cap = 1 << 20 if cfg.check_registry else 1 << 16  # calloc'd: untouched pages are free
+        reg_raw = np.zeros((cap, 12), dtype=np.int32)
+        sc.registry_out = reg_raw.ctypes.data
+        sc.registry_cap = cap
     res = _lib.SearchResult_t()
     hist = np.zeros(rg.num_vertices + 2, dtype=np.int64)
     _lib.check(_lib.lib.vcg_search(rg.device().handle, C.byref(sc), C.byref(res),
@@ -207,6 +288,9 @@ def run_search(rg: StaticGraph, cfg: SolverConfig, width: int, best_init: int,
         raise _lib.GpuError(f"search kernel reported device error {res.error}")
     h = {int(i): int(c) for i, c in enumerate(hist) if c}
     local = cover[: res.cover_size].tolist() if record and res.cover_size >= 0 else None
+    count = int(res.registry_entries)
+    res.registry_view = Registry(count, reg_raw if reg_raw is not None and count <= len(reg_raw)
+                                 else None)
     return res, h, local
 
 
@@ -350,8 +434,7 @@ def _solve(g: StaticGraph, cfg: SolverConfig, lazy: bool):
     stats.max_stack_depth = int(res.max_stack_depth)
     stats.worklist_pushes = int(res.worklist_pushes)
     stats.worklist_pops = int(res.worklist_pops)
-    result.registry = RegistrySummary(int(res.registry_entries),
-                                      int(res.registry_violations) if cfg.check_registry else None)
+    result.registry = res.registry_view
     result.root_index = 0
 
     best = int(res.best)

@@ -111,6 +111,7 @@ def kernel_cases(count=150):
             q = np.zeros(n, dtype=np.int32)
             r = pure.bfs_component(deg, off, nbr, vis, 1, q, src)
             res["bfs_component"] = {"ret": list(r), "members": sorted(q[: r[0]].tolist()),
+                                    "queue": q[: r[0]].tolist(),
                                     "next": pure.next_live_unvisited(deg, vis, 1, 0, n - 1)}
         d = deg.copy()
         o = np.zeros(n + 1, dtype=np.int32)
@@ -231,6 +232,70 @@ def workload_cases():
     return out
 
 
+# -- acceptance families (tests/test_acceptance.py:150-284) ------------------
+
+def registry_dump(reg):
+    """Every registry entry's fields (registry.py:24-88), in allocation order."""
+    from vcsolver.registry import ParentEntry
+    if reg is None:
+        return None
+    out = []
+    for e in reg.entries:
+        if isinstance(e, ParentEntry):
+            out.append({"kind": "parent", "sum": e.sum, "sum_achieved": e.sum_achieved,
+                        "live_comps": e.live_comps, "ancestor": e.ancestor,
+                        "initial_sum": e.initial_sum, "folded_total": e.folded_total,
+                        "children": list(e.children), "discovery_done": e.discovery_done})
+        else:
+            out.append({"kind": "child", "best": e.best, "achieved": e.achieved,
+                        "live_nodes": e.live_nodes, "parent": e.parent})
+    return out
+
+
+def acceptance_cases():
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    import test_acceptance as ta
+    from helpers import PETERSEN_EDGES, clique_edges, cycle_edges, disjoint_union
+    out = {"nested": [], "forests": [], "cliques": [], "cycles": [], "petersen_pair": None}
+
+    def det_run(g):
+        r = solve(g, SolverConfig(deterministic=True))
+        return {"cover_size": r.cover_size, "stats": stats_of(r),
+                "registry": registry_dump(r.registry),
+                "nesting_depth": (ta.registry_nesting_depth(r.registry)
+                                  if r.registry is not None else 0)}
+
+    rng = random.Random(424)  # test_c06_nested_cascades
+    for trial in range(50):
+        g = ta.nested_chain(rng)
+        size, wit = brute_force_mvc(g)
+        out["nested"].append({"name": f"nested_{trial}", "n": g.num_vertices,
+                              "edges": edges_of(g), "brute": [size, list(wit)],
+                              "det": det_run(g)})
+    for i in range(60):  # test_c07 forests
+        rng = random.Random(500_000 + i)
+        f = ta._random_forest(rng, rng.randint(1, 24))
+        pre = root_reduce(f)
+        size, wit = brute_force_mvc(f)
+        out["forests"].append({"name": f"forest_{i}", "n": f.num_vertices, "edges": edges_of(f),
+                               "forced": list(pre.forced), "rule_counts": dict(pre.rule_counts),
+                               "brute": [size, list(wit)]})
+    for n in range(2, 13):  # test_c08
+        g = ta.make_graph(n, clique_edges(n))
+        out["cliques"].append({"n": n, "edges": edges_of(g), "det": det_run(g),
+                               "mvc": solve(g, SolverConfig()).cover_size})
+    for n in range(3, 13):
+        g = ta.make_graph(n, cycle_edges(n))
+        out["cycles"].append({"n": n, "edges": edges_of(g), "det": det_run(g),
+                              "mvc": solve(g, SolverConfig()).cover_size})
+    pair = disjoint_union((10, PETERSEN_EDGES), (10, PETERSEN_EDGES))  # test_c05
+    r = solve(pair, SolverConfig(deterministic=True, use_root_reduce=False))
+    out["petersen_pair"] = {"n": pair.num_vertices, "edges": edges_of(pair),
+                            "cover_size": r.cover_size, "stats": stats_of(r),
+                            "registry": registry_dump(r.registry)}
+    return out
+
+
 def main():
     fixtures = {
         "kernels.json": kernel_cases,
@@ -238,6 +303,7 @@ def main():
         "root_reduce.json": root_cases,
         "solve.json": solve_cases,
         "workloads.json": workload_cases,
+        "acceptance.json": acceptance_cases,
     }
     only = sys.argv[1:]
     for fname, fn in fixtures.items():
@@ -246,7 +312,7 @@ def main():
         data = fn()
         with open(os.path.join(HERE, fname), "w") as f:
             json.dump(data, f, separators=(",", ":"))
-        print("wrote", fname, len(data))
+        print("wrote", fname, len(data) if isinstance(data, list) else sorted(data))
 
 
 if __name__ == "__main__":

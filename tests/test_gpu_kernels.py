@@ -68,6 +68,19 @@ def test_point_kernels_bit_exact():
             r, members = K.component(deg, off, nbr, case["src"])
             assert list(r) == exp["bfs_component"]["ret"]
             assert members == exp["bfs_component"]["members"]
+            # kernels/__init__.py:42-43: BFS queue order, visited stamps
+            vis = np.zeros(n, dtype=np.int32)
+            q = np.zeros(n, dtype=np.int32)
+            r = K.bfs_component(deg, off, nbr, vis, 1, q, case["src"])
+            assert list(r) == exp["bfs_component"]["ret"]
+            assert q[: r[0]].tolist() == exp["bfs_component"]["queue"]
+            assert sorted(np.nonzero(vis == 1)[0].tolist()) == exp["bfs_component"]["members"]
+            assert K.next_live_unvisited(deg, vis, 1, 0, n - 1) == exp["bfs_component"]["next"]
+        d = deg.copy()
+        o = np.zeros(n + 1, dtype=np.int32)
+        r = K.greedy_cover(d, off, nbr, 0, n - 1, o, 0)
+        assert list(r) == exp["greedy_cover"]["ret"]
+        assert o[: r[1]].tolist() == exp["greedy_cover"]["out"]
 
 
 def test_negative_budget_high_degree_closed_form():

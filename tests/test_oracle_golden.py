@@ -63,6 +63,7 @@ def test_point_kernels_match_reference():
             r = oracle.bfs_component(deg, off, nbr, vis, 1, q, case["src"])
             assert list(r) == exp["bfs_component"]["ret"]
             assert sorted(q[: r[0]].tolist()) == exp["bfs_component"]["members"]
+            assert q[: r[0]].tolist() == exp["bfs_component"]["queue"]
             assert oracle.next_live_unvisited(deg, vis, 1, 0, n - 1) == exp["bfs_component"]["next"]
         d = deg.copy()
         o = np.zeros(n + 1, dtype=np.int32)
