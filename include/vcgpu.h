@@ -166,6 +166,9 @@ typedef struct {
                                  discovery_done, child_folded (registry.py:24-88) */
   int64_t registry_cap;       /* entries registry_out holds; a larger registry is not
                                  copied (registry_entries still reports its size) */
+  struct vcg_exchange* exchange; /* nullable: in-flight bound / stop exchange with other
+                                 searches (vcg_exchange_*); the kernel polls it and
+                                 publishes its root scope's achieved best into it */
 } vcg_search_config;
 
 typedef struct {
@@ -205,6 +208,26 @@ typedef struct {
                                  step, first warp task start, last warp task end;
                                  then tree nodes and vertices of the longest warp task */
 } vcg_search_result;
+
+/* In-flight exchange between one running search and the rest of a
+ * distributed solve (engine.py:453-495 semantics across processes / GPUs).
+ * Three device words on the creating thread's current device: an external
+ * bound for the search's root scope (a cover of that size exists elsewhere:
+ * the root key is lowered to it, not achieved; <= 0 stops the search), an
+ * external stop flag (PVC answered elsewhere), and the search's own best
+ * achieved root cover, lowered by the kernel as it finds covers.  post / peek
+ * are DMA copies on the calling thread's stream: another host thread may call
+ * them while the search kernel runs (copy engines, no SM needed).  Replaces
+ * the shared state of engine.py:200 _Engine (threads over one process). */
+typedef struct vcg_exchange vcg_exchange;
+int vcg_exchange_create(vcg_exchange** out);
+int vcg_exchange_destroy(vcg_exchange* x);
+/* reset: no external bound, no stop, no local best */
+int vcg_exchange_reset(vcg_exchange* x);
+/* bound < 0: leave the bound unchanged */
+int vcg_exchange_post(vcg_exchange* x, int64_t bound, int stop);
+/* the search's best achieved root cover so far (INT32_MAX: none) */
+int vcg_exchange_peek(vcg_exchange* x, int64_t* local_best);
 
 /* Run the persistent search kernel.  hist_out (nullable, capacity n+2)
  * receives the components-per-branch histogram indexed by component count. */

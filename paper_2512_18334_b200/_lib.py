@@ -44,6 +44,7 @@ class SearchConfig_t(C.Structure):
         ("timeout", C.c_double), ("check_registry", C.c_int), ("record_cover", C.c_int),
         ("cover_out", C.c_void_p), ("root_deg", C.c_void_p), ("warp_limit", C.c_int),
         ("gpu_share", C.c_int), ("registry_out", C.c_void_p), ("registry_cap", I64),
+        ("exchange", C.c_void_p),
     ]
 
 
@@ -80,6 +81,8 @@ EXPORTS = (
     "vcg_graph_download", "vcg_induced_subgraph", "vcg_greedy_bound", "vcg_root_reduce",
     "vcg_search", "vcg_node_op", "vcg_last_error", "vcg_device_count", "vcg_launch_count",
     "vcg_set_device", "vcg_get_device", "vcg_expand", "vcg_shutdown", "vcg_brute_force_mvc",
+    "vcg_exchange_create", "vcg_exchange_destroy", "vcg_exchange_reset", "vcg_exchange_post",
+    "vcg_exchange_peek",
 )
 
 
@@ -117,6 +120,11 @@ def _load():
     lib.vcg_expand.argtypes = [P, C.POINTER(ExpandConfig_t), C.POINTER(ExpandResult_t), P, P, I64]
     lib.vcg_node_op.argtypes = [C.c_int, C.c_int, I64, P, P, P, I64, I64, I64, I64, P, I64, P]
     lib.vcg_brute_force_mvc.argtypes = [I64, P, P, C.POINTER(I64), P]
+    lib.vcg_exchange_create.argtypes = [C.POINTER(P)]
+    lib.vcg_exchange_destroy.argtypes = [P]
+    lib.vcg_exchange_reset.argtypes = [P]
+    lib.vcg_exchange_post.argtypes = [P, I64, C.c_int]
+    lib.vcg_exchange_peek.argtypes = [P, C.POINTER(I64)]
     lib.vcg_shutdown.restype = None
     return lib
 

@@ -1685,6 +1685,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   static thread_local int* hb_host = nullptr;
   static thread_local long long hb_cap = 0;
   const char* hb_env = getenv("VCG_HEARTBEAT");
+  P.xch = cfg->exchange ? cfg->exchange->d : nullptr;
   P.hb = nullptr;
   if (hb_env) {
     const long long need = (long long)blocks * kMaxWarps;
@@ -1857,6 +1858,64 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
     }
     res->registry_violations = bad;
   }
+  return 0;
+}
+
+// ---------------------------------------------------------------- exchange --
+
+struct vcg_exchange {
+  int dev = 0;
+  int32_t* d = nullptr;  // [0] external bound, [1] external stop, [2] local best, [3] pad
+};
+
+extern "C" int vcg_exchange_create(vcg_exchange** out) {
+  if (int r = need_device()) return r;
+  if (!out) return fail(VCG_EINVAL, "bad arguments");
+  auto* x = new vcg_exchange();
+  CK(cudaGetDevice(&x->dev));
+  if (cudaMalloc(&x->d, 16) != cudaSuccess) {
+    delete x;
+    return fail(VCG_ERESOURCE, "exchange: cudaMalloc failed");
+  }
+  *out = x;
+  return vcg_exchange_reset(x);
+}
+
+extern "C" int vcg_exchange_destroy(vcg_exchange* x) {
+  if (!x) return 0;
+  if (!g_shutdown.load()) cudaFree(x->d);
+  delete x;
+  return 0;
+}
+
+extern "C" int vcg_exchange_reset(vcg_exchange* x) {
+  if (!x) return fail(VCG_EINVAL, "bad arguments");
+  const int32_t init[4] = {kInf, 0, kInf, 0};
+  CK(cudaMemcpyAsync(x->d, init, 16, cudaMemcpyHostToDevice, cudaStreamPerThread));
+  CK(cudaStreamSynchronize(cudaStreamPerThread));
+  return 0;
+}
+
+extern "C" int vcg_exchange_post(vcg_exchange* x, int64_t bound, int stop) {
+  if (!x) return fail(VCG_EINVAL, "bad arguments");
+  if (bound >= 0) {
+    const int32_t b = (int32_t)std::min<int64_t>(bound, kInf);
+    CK(cudaMemcpyAsync(x->d, &b, 4, cudaMemcpyHostToDevice, cudaStreamPerThread));
+  }
+  if (stop) {
+    const int32_t one = 1;
+    CK(cudaMemcpyAsync(x->d + 1, &one, 4, cudaMemcpyHostToDevice, cudaStreamPerThread));
+  }
+  CK(cudaStreamSynchronize(cudaStreamPerThread));
+  return 0;
+}
+
+extern "C" int vcg_exchange_peek(vcg_exchange* x, int64_t* local_best) {
+  if (!x || !local_best) return fail(VCG_EINVAL, "bad arguments");
+  int32_t v = kInf;
+  CK(cudaMemcpyAsync(&v, x->d + 2, 4, cudaMemcpyDeviceToHost, cudaStreamPerThread));
+  CK(cudaStreamSynchronize(cudaStreamPerThread));
+  *local_best = v;
   return 0;
 }
 

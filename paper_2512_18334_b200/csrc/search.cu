@@ -772,6 +772,7 @@ __global__ void __launch_bounds__(VCG_SEARCH_MAXT, VCG_SEARCH_MINB) search_kerne
   bool cont = false;
   unsigned backoff = 32;
   unsigned iter = 0;
+  unsigned xpoll = 0;
   while (true) {
     VCG_HB(&bs, 50);
     // stop / deadline poll: before every pop, and every 4th node of an
@@ -785,6 +786,17 @@ __global__ void __launch_bounds__(VCG_SEARCH_MAXT, VCG_SEARCH_MINB) search_kerne
           atomicExch(&P.ctl->timed_out, 1);
           atomicExch(&P.ctl->stop, 1);
           stop = 1;
+        }
+        // in-flight exchange (vcg_exchange): a cover found elsewhere bounds
+        // the root scope (not achieved here); an external stop ends the search
+        if (!stop && P.xch && (xpoll++ & 15) == 0) {
+          const int xb = __ldcg(&P.xch[0]), xs = __ldcg(&P.xch[1]);
+          if (xs || xb <= 0) {
+            atomicExch(&P.ctl->stop, 1);
+            stop = 1;
+          } else if (xb < kInf) {
+            atomicMin(&P.reg.key[P.root_index], 2 * xb + 1);
+          }
         }
         st.flag = stop;
       }

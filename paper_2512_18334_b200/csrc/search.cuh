@@ -130,7 +130,15 @@ struct SearchParams {
   int bws_alias;          // warp workspaces alias the node workspace's int scratch
   long long bws_off;      // else: their offset in dynamic shared memory
   int* hb;                // debug heartbeat rows [gridDim.x][kMaxWarps] (host-mapped), or null
+  // vcg_exchange words: [0] external root bound (kInf: none), [1] external
+  // stop, [2] this search's best achieved root cover (kInf: none); or null
+  int* xch;
 };
+
+// an achieved root-scope cover of `value` vertices: publish it to the exchange
+__device__ __forceinline__ void xch_publish(const SearchParams& P, int idx, int value) {
+  if (P.xch && idx == P.root_index) atomicMin(&P.xch[2], value);
+}
 
 template <typename T>
 __host__ __device__ inline long long deg_bytes(int n) {
@@ -317,6 +325,7 @@ __device__ inline void pvc_propagate(const SearchParams& P, int idx) {
     total += ld_relaxed(&R.sum[p]);
     int anc = R.link[p];
     atomicMin(&R.key[anc], (int)(total * 2));
+    xch_publish(P, anc, (int)total);
     note_witness(P, anc, (int)total, kComposite | (unsigned)p);
     idx = anc;
   }
@@ -325,7 +334,10 @@ __device__ inline void pvc_propagate(const SearchParams& P, int idx) {
 // engine.py:453 _submit
 __device__ inline void reg_submit(const SearchParams& P, int idx, int value, bool achieved,
                                   unsigned long long wid) {
-  if (achieved) note_witness(P, idx, value, wid);
+  if (achieved) {
+    note_witness(P, idx, value, wid);
+    xch_publish(P, idx, value);
+  }
   atomicMin(&P.reg.key[idx], value * 2 + (achieved ? 0 : 1));
   if (!P.pvc) return;
   if (idx != P.root_index) pvc_propagate(P, idx);

@@ -1,30 +1,42 @@
-"""Multi-GPU solve of ONE instance: root-subtree partitioning across ranks.
+"""Multi-GPU solve of ONE instance: root subtrees self-scheduled across ranks,
+with the best bound and termination exchanged while the searches run.
 
-One process per GPU (torch.distributed, NCCL over NVLink on a GPU node).
-Every rank runs the deterministic root pipeline (``root_reduce``) and the
-same breadth-first expansion of the root's search tree (``vcg_expand``, one
-device block, the reference's node semantics), which yields open subtrees
-that partition the remaining search:
+One process per GPU (torch.distributed; NCCL or gloo for the final
+reductions).  Every rank runs the same deterministic root pipeline
+(``root_reduce``) and the same breadth-first expansion of the root's search
+tree (``vcg_expand``, one device block, the reference's node semantics),
+which yields open subtrees that partition the remaining search:
 
     MVC = min(best, min_i(S_i + MVC(subtree_i)))
 
-Subtrees are dealt round-robin (subtree i -> rank i mod world).  Each rank
-solves its subtree of the round with the persistent search kernel, bounded
-by the current global best minus S_i, then the ranks all-reduce (MIN) the
-best bound -- the bound exchange that lets every rank prune with the best
-cover found anywhere -- and, for PVC, stop as soon as any rank reached k
-(termination propagation).  A subtree whose residual graph is disconnected
-is solved by the component-aware search itself.
+Load balance (engine.py:245-273 take/steal, :413 offload -- here across
+processes): subtrees are not dealt statically; an idle rank takes the next
+one from a shared ticket counter (an atomic ``add`` on the process group's
+c10d store), so a rank stuck in a deep subtree never holds up the others and
+the ranks finish within one subtree of each other.
 
-Reference behaviour replaced: engine.py:200 ``_Engine.run`` (threads over one
-shared worklist); the answer and the result format are those of
-``engine.solve`` (engine.py:561).
+Bound and termination propagation (engine.py:453-495 across processes):
+the global best cover size lives in the store (compare-and-set minimum).
+While a rank's search kernel runs, a host thread on that rank polls the
+kernel's own best achieved root cover through a ``vcg_exchange`` (device
+words read and written by DMA on the copy engines, so the persistent kernel
+keeps every SM), offers it to the store, and posts the store's best back as
+the subtree's external bound (a cover of that size exists elsewhere; the
+kernel lowers its root key to it, not achieved).  PVC: the first rank that
+reaches k sets the store's stop flag, which the other ranks post to their
+kernels and which stops the ticket loop everywhere.
+
+A subtree whose residual graph is disconnected is solved by the
+component-aware search itself.  Reference behaviour replaced: engine.py:200
+``_Engine.run`` (threads over one shared worklist); the answer and the
+result format are those of ``engine.solve`` (engine.py:561).
 """
 
 from __future__ import annotations
 
 import ctypes as C
-import math
+import itertools
+import threading
 import time
 from dataclasses import dataclass
 
@@ -41,8 +53,111 @@ class Subtrees:
     nodes: int           # tree nodes the expansion processed
 
 
+@dataclass
+class SubtreeResult:
+    best: int | None     # subtree cover size below the bound, if one was found
+    nodes: int
+    found: bool          # PVC: the subtree reached its budget
+    hist: dict
+    timed_out: bool
+
+
+# ------------------------------------------------------------ coordination --
+
+_CALLS = itertools.count()
+
+
+class Coordinator:
+    """Global best, PVC stop and the subtree ticket counter of one distributed
+    solve: the process group's c10d store when there is one (atomic ``add``,
+    ``compare_set``), else process-local state."""
+
+    def __init__(self, store=None, prefix: str = "vcg/"):
+        self.store = store
+        self.p = prefix
+        self._lock = threading.Lock()
+        self._best = None
+        self._ticket = 0
+        self._found = False
+
+    def ticket(self) -> int:
+        if self.store is not None:
+            return int(self.store.add(self.p + "ticket", 1)) - 1
+        with self._lock:
+            t = self._ticket
+            self._ticket += 1
+            return t
+
+    def offer(self, v: int) -> None:
+        """best = min(best, v)."""
+        v = int(v)
+        if self.store is None:
+            with self._lock:
+                if self._best is None or v < self._best:
+                    self._best = v
+            return
+        key, want = self.p + "best", str(v).encode()
+        cur = self.store.compare_set(key, "", want)  # sets an absent key
+        while cur != want and int(cur) > v:
+            cur = self.store.compare_set(key, cur, want)
+
+    def best(self) -> int:
+        if self.store is None:
+            return self._best
+        return int(self.store.get(self.p + "best"))
+
+    def set_found(self) -> None:
+        if self.store is None:
+            self._found = True
+        else:
+            self.store.set(self.p + "found", "1")
+
+    def found(self) -> bool:
+        if self.store is None:
+            return self._found
+        return self.store.check([self.p + "found"])
+
+
+def _dist():
+    try:
+        import torch.distributed as dist
+    except ImportError:  # pragma: no cover
+        return None
+    return dist if dist.is_available() and dist.is_initialized() else None
+
+
+def _allreduce(values, op, group=None):
+    """All-reduce a small int64 vector (MIN, MAX or SUM) across the group."""
+    dist = _dist()
+    if dist is None:
+        return list(values)
+    import torch
+
+    backend = dist.get_backend(group)
+    device = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else "cpu"
+    t = torch.tensor(list(values), dtype=torch.int64, device=device)
+    ops = {"min": dist.ReduceOp.MIN, "max": dist.ReduceOp.MAX, "sum": dist.ReduceOp.SUM}
+    dist.all_reduce(t, op=ops[op], group=group)
+    return [int(x) for x in t.cpu().tolist()]
+
+
+def _coordinator(group):
+    dist = _dist()
+    call = next(_CALLS)  # every rank makes the same sequence of calls
+    if dist is None or dist.get_world_size(group) == 1:
+        return Coordinator()
+    from torch.distributed import distributed_c10d as c10d
+
+    return Coordinator(c10d._get_default_store(), prefix=f"vcg/solve{call}/")
+
+
+# ----------------------------------------------------------------- backend --
+
 class GpuBackend:
     """The product path: root pipeline, expansion and subtree search on the GPU."""
+
+    def __init__(self):
+        self._xch = {}
 
     def root_reduce(self, g, cfg):
         from .preprocess import root_reduce
@@ -50,7 +165,7 @@ class GpuBackend:
         bound = cfg.k if cfg.mode == "pvc" else None
         return root_reduce(g, enabled=cfg.use_root_reduce, crown=cfg.use_crown, bound=bound,
                            width_override=cfg.width, need_greedy_original=bound is None,
-                      ordered=False)
+                           ordered=False)
 
     def expand(self, rg, cfg, best_init, target) -> Subtrees:
         from . import _lib
@@ -66,60 +181,82 @@ class GpuBackend:
         k = int(er.count)
         return Subtrees(sub_S[:k].copy(), sub_deg[:k].copy(), int(er.best), int(er.nodes))
 
-    def search_subtree(self, rg, cfg, width, root_deg, bound, k_red):
-        """Search one subtree for a cover < bound: (best or None, nodes, found, hist)."""
+    def _exchange(self):
+        from . import _lib
+
+        dev = _lib.get_device()
+        x = self._xch.get(dev)
+        if x is None:
+            h = C.c_void_p()
+            _lib.check(_lib.lib.vcg_exchange_create(C.byref(h)))
+            x = self._xch[dev] = h
+        return x
+
+    def search_subtree(self, rg, cfg, width, root_deg, bound, k_red, coord, S_i,
+                       timeout=None) -> SubtreeResult:
+        """Search one subtree for a cover < bound, exchanging bounds with the
+        other ranks through ``coord`` while the kernel runs."""
+        from dataclasses import replace
+
+        from . import _lib
         from .engine import run_search
 
         deg = np.ascontiguousarray(root_deg, dtype=np.int32)
+        x = self._exchange()
+        _lib.check(_lib.lib.vcg_exchange_reset(x))
+        _lib.check(_lib.lib.vcg_exchange_post(x, int(bound), int(coord.found())))
+        dev = _lib.get_device()
+        done = threading.Event()
 
-        def seed_root(sc):
+        def exchanger():  # the host side of the in-flight exchange
+            _lib.set_device(dev)
+            lb = C.c_int64()
+            while not done.wait(0.0005):
+                _lib.check(_lib.lib.vcg_exchange_peek(x, C.byref(lb)))
+                if lb.value < (1 << 31) - 1:
+                    coord.offer(S_i + lb.value)
+                _lib.check(_lib.lib.vcg_exchange_post(x, coord.best() - S_i, int(coord.found())))
+
+        def hook(sc):
             sc.root_deg = deg.ctypes.data
+            sc.exchange = x
 
-        res, hist, _ = run_search(rg, cfg, width, bound, False, k_red, config_hook=seed_root)
-        improved = int(res.best) < bound
-        return (int(res.best) if improved else None), int(res.tree_nodes_visited), \
-            bool(res.found), hist
+        sub_cfg = replace(cfg, timeout=timeout)
+        t = threading.Thread(target=exchanger, daemon=True)
+        t.start()
+        try:
+            res, hist, _ = run_search(rg, sub_cfg, width, bound, False, k_red, config_hook=hook)
+        finally:
+            done.set()
+            t.join()
+        improved = int(res.best) < bound and bool(res.best_achieved)
+        return SubtreeResult(int(res.best) if improved else None, int(res.tree_nodes_visited),
+                             bool(res.found), hist, bool(res.timed_out))
 
 
-def _dist():
-    try:
-        import torch.distributed as dist
-    except ImportError:  # pragma: no cover
-        return None
-    return dist if dist.is_available() and dist.is_initialized() else None
-
-
-def _allreduce(values, op, group=None):
-    """All-reduce a small int64 vector (MIN or SUM) across the group."""
-    dist = _dist()
-    if dist is None:
-        return list(values)
-    import torch
-
-    backend = dist.get_backend(group)
-    device = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else "cpu"
-    t = torch.tensor(list(values), dtype=torch.int64, device=device)
-    dist.all_reduce(t, op={"min": dist.ReduceOp.MIN, "sum": dist.ReduceOp.SUM}[op], group=group)
-    return [int(x) for x in t.cpu().tolist()]
-
+# ------------------------------------------------------------------- solve --
 
 def solve_distributed(g, config: SolverConfig | None = None, group=None,
                       subtrees_per_rank: int = 8, backend=None) -> SolveResult:
     """engine.py:561 solve, one instance across every rank of ``group``."""
     cfg = config if config is not None else SolverConfig()
     cfg.validate()
+    if cfg.record_cover:
+        raise ValueError("record_cover is not supported by solve_distributed; use solve()")
     be = backend if backend is not None else GpuBackend()
     dist = _dist()
     rank = dist.get_rank(group) if dist else 0
     world = dist.get_world_size(group) if dist else 1
+    coord = _coordinator(group)
+    t_start = time.perf_counter()
+    deadline = None if cfg.timeout is None else t_start + cfg.timeout
 
     stats = Stats()
     stats.rule_counts = dict.fromkeys(RULE_KEYS, 0)
     stats.root_vertices_before = g.num_vertices
     stats.phase_seconds = {"root_reduce": 0.0, "search": 0.0, "reconstruct": 0.0}
-    t0 = time.perf_counter()
     pre = be.root_reduce(g, cfg)
-    stats.phase_seconds["root_reduce"] = time.perf_counter() - t0
+    stats.phase_seconds["root_reduce"] = time.perf_counter() - t_start
     for key, val in pre.rule_counts.items():
         stats.rule_counts[key] = stats.rule_counts.get(key, 0) + val
     stats.root_vertices_after = pre.graph.num_vertices
@@ -145,43 +282,69 @@ def solve_distributed(g, config: SolverConfig | None = None, group=None,
 
     t1 = time.perf_counter()
     sub = be.expand(rg, cfg, best_init, max(1, subtrees_per_rank * world))
-    best = min(best_init, sub.best)
+    best0 = min(best_init, sub.best)
+    # a subtree without edges is a leaf cover of S_i vertices, not a search
+    edge_free = sub.deg.sum(axis=1) == 0 if len(sub.S) else np.zeros(0, dtype=bool)
+    if edge_free.any():
+        best0 = min(best0, int(sub.S[edge_free].min()))
+    coord.offer(best0)
+    if k_red is not None and best0 <= k_red:
+        coord.set_found()
+    order = np.nonzero(~edge_free)[0]
     nodes = sub.nodes if rank == 0 else 0
-    found = k_red is not None and best <= k_red
-    count = len(sub.S)
     hist: dict[int, int] = {}
-    for r in range(math.ceil(count / world) if not found else 0):
-        i = r * world + rank
-        local = best
-        lfound = 0
-        if i < count:
-            bound = best - int(sub.S[i])
-            if bound >= 1:
-                kr = None if k_red is None else k_red - int(sub.S[i])
-                got, nd, f, h = be.search_subtree(rg, cfg, pre.width, sub.deg[i], bound, kr)
-                nodes += nd
-                for key, c in h.items():
-                    hist[key] = hist.get(key, 0) + c
-                if got is not None:
-                    local = min(local, int(sub.S[i]) + got)
-                lfound = int(f)
-        best, = _allreduce([local], "min", group)
-        if k_red is not None:
-            anyf, = _allreduce([lfound], "sum", group)
-            if anyf or best <= k_red:
-                found = True
+    timed_out = False
+    while not coord.found():
+        t = coord.ticket()
+        if t >= len(order):
+            break
+        remaining = None
+        if deadline is not None:
+            remaining = deadline - time.perf_counter()
+            if remaining <= 0:
+                timed_out = True
                 break
+        i = int(order[t])
+        S_i = int(sub.S[i])
+        bound = coord.best() - S_i
+        if bound < 1:  # a subtree with edges needs >= 1 more vertex: pruned
+            continue
+        kr = None if k_red is None else k_red - S_i
+        r = be.search_subtree(rg, cfg, pre.width, sub.deg[i], bound, kr, coord, S_i,
+                              timeout=remaining)
+        nodes += r.nodes
+        for key, c in r.hist.items():
+            hist[key] = hist.get(key, 0) + c
+        if r.best is not None:
+            coord.offer(S_i + r.best)
+        if r.found or (k_red is not None and coord.best() <= k_red):
+            coord.set_found()
+        timed_out = timed_out or r.timed_out
     stats.phase_seconds["search"] = time.perf_counter() - t1
+    if dist is not None:
+        dist.barrier(group=group)
+    best = coord.best()
     nodes, = _allreduce([nodes], "sum", group)
+    timed_out = bool(_allreduce([int(timed_out)], "max", group)[0])
+    found = coord.found() or (k_red is not None and best <= k_red)
+    if dist is not None and world > 1:
+        parts = [None] * world
+        dist.all_gather_object(parts, hist, group=group)
+        hist = {}
+        for h in parts:
+            for key, c in h.items():
+                hist[key] = hist.get(key, 0) + c
     stats.tree_nodes_visited = nodes
     stats.components_per_branch = hist
     if cfg.mode == "mvc":
         result.found = True
         result.cover_size = pre.forced_count + best
+        result.exact = not timed_out
     else:
-        result.found = found or best <= k_red
-        result.cover_size = pre.forced_count + best if result.found else None
+        result.found = found
+        result.exact = found or not timed_out
+        result.cover_size = pre.forced_count + best if found else None
     return result
 
 
-__all__ = ["solve_distributed", "GpuBackend", "Subtrees"]
+__all__ = ["solve_distributed", "GpuBackend", "Subtrees", "SubtreeResult", "Coordinator"]

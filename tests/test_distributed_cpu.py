@@ -2,8 +2,9 @@
 
 The GPU pieces (root pipeline, expansion, subtree search) are replaced by an
 oracle-backed backend with the same contract, so what is tested here is the
-partitioning itself: identical expansion on every rank, round-robin
-subtrees, MIN all-reduce of the bound, PVC termination propagation, and the
+partitioning itself: identical expansion on every rank, subtrees taken from
+the c10d store's ticket counter, the global best kept as a compare-and-set
+minimum in the store, PVC termination through the store's stop flag, and the
 combination MVC = min(best, min_i S_i + MVC(subtree_i))."""
 
 from __future__ import annotations
@@ -86,7 +87,9 @@ class OracleBackend:
                         np.array([f[4] for f in opened], dtype=np.int32).reshape(len(opened), n),
                         int(best), nodes)
 
-    def search_subtree(self, rg, cfg, width, root_deg, bound, k_red):
+    def search_subtree(self, rg, cfg, width, root_deg, bound, k_red, coord, S_i, timeout=None):
+        from paper_2512_18334_b200.distributed import SubtreeResult
+
         off, nbr = rg.offsets, rg.neighbors
         alive = np.asarray(root_deg) > 0
         heads = np.repeat(np.arange(rg.num_vertices), np.diff(off))
@@ -94,7 +97,7 @@ class OracleBackend:
         n2, o2, b2 = csr(rg.num_vertices, np.stack([heads[keep], nbr[keep]], 1))
         mvc = oracle.solve(n2, o2, b2, deterministic=True)["cover_size"]
         found = k_red is not None and mvc <= k_red
-        return (mvc if mvc < bound else None), 1, found, {}
+        return SubtreeResult(mvc if mvc < bound else None, 1, found, {}, False)
 
 
 def _graph(case):
@@ -157,3 +160,41 @@ def test_single_process_partition_matches_reference():
         want = case["runs"]["det"]["cover_size"]
         r = solve_distributed(g, SolverConfig(), subtrees_per_rank=4, backend=OracleBackend())
         assert r.cover_size == want, case["name"]
+
+
+def _ticket_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2512_18334_b200.distributed import _coordinator
+
+    coord = _coordinator(None)
+    coord.offer(1000 + rank)
+    mine = []
+    while True:
+        t = coord.ticket()
+        if t >= 200:
+            break
+        mine.append(t)
+        coord.offer(900 - t)
+    dist.barrier()
+    q.put((rank, mine, coord.best(), coord.found()))
+    dist.destroy_process_group()
+
+
+def test_store_coordinator_two_ranks():
+    """Tickets are handed out exactly once across ranks; the store's best is
+    the minimum every rank offered."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ticket_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r, (m, b, f)) for r, m, b, f in (q.get(timeout=300) for _ in procs))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    taken = res[0][0] + res[1][0]
+    assert sorted(taken) == list(range(200))
+    assert res[0][1] == res[1][1] == 900 - 199
+    assert res[0][2] is False

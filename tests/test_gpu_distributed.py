@@ -1,6 +1,7 @@
-"""The distributed solver's GPU backend on one GPU (world 1): device
-expansion of the root's search tree + subtree searches seeded from it must
-give the reference's answers."""
+"""The distributed solver's GPU backend on one GPU: world 1 (device expansion
+of the root's search tree + subtree searches seeded from it), the in-flight
+vcg_exchange of one search, and world 2 (two processes sharing cuda:0) --
+the reference's answers throughout."""
 
 from __future__ import annotations
 
@@ -42,3 +43,100 @@ def test_subtree_partition_workloads(name):
     for k, e in exp["pvc"].items():
         r = solve_distributed(g, vc.SolverConfig(mode="pvc", k=int(k)), subtrees_per_rank=8)
         assert r.found == e["found"], k
+
+
+def test_exchange_bound_stop_and_publish():
+    """vcg_exchange on one search: the kernel publishes its best achieved root
+    cover; an external bound at the optimum leaves nothing better to find; an
+    external stop ends the search."""
+    import ctypes as C
+
+    import paper_2512_18334_b200 as vc
+    from paper_2512_18334_b200 import _lib, synth
+    from paper_2512_18334_b200.engine import run_search
+
+    exp = golden("workloads.json")["rgg2000"]
+    n, off, nbr = synth.WORKLOADS["rgg2000"]()
+    g = vc.StaticGraph(n, off, nbr)
+    pre = vc.root_reduce(g, ordered=False)
+    rg, opt_red = pre.graph, exp["mvc"] - pre.forced_count
+    x = C.c_void_p()
+    _lib.check(_lib.lib.vcg_exchange_create(C.byref(x)))
+    lb = C.c_int64()
+    try:
+        def hook(sc):
+            sc.exchange = x
+
+        cfg = vc.SolverConfig()
+        _lib.check(_lib.lib.vcg_exchange_reset(x))
+        res, _, _ = run_search(rg, cfg, pre.width, pre.greedy_reduced, True, None,
+                               config_hook=hook)
+        _lib.check(_lib.lib.vcg_exchange_peek(x, C.byref(lb)))
+        assert int(res.best) == opt_red and lb.value == opt_red
+        full_nodes = int(res.tree_nodes_visited)
+        # a cover of opt size exists elsewhere: nothing better here
+        _lib.check(_lib.lib.vcg_exchange_reset(x))
+        _lib.check(_lib.lib.vcg_exchange_post(x, opt_red, 0))
+        res, _, _ = run_search(rg, cfg, pre.width, pre.greedy_reduced, True, None,
+                               config_hook=hook)
+        assert int(res.best) == opt_red
+        assert int(res.tree_nodes_visited) <= full_nodes
+        # external stop: the kernel ends without an answer
+        _lib.check(_lib.lib.vcg_exchange_reset(x))
+        _lib.check(_lib.lib.vcg_exchange_post(x, -1, 1))
+        res, _, _ = run_search(rg, cfg, pre.width, pre.greedy_reduced, True, None,
+                               config_hook=hook)
+        assert int(res.tree_nodes_visited) < full_nodes
+    finally:
+        _lib.lib.vcg_exchange_destroy(x)
+
+
+def _gpu_worker(rank, world, port, cases, q):
+    import os
+
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), VCG_WATCHDOG_S="120")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2512_18334_b200 as vc
+    from paper_2512_18334_b200.distributed import solve_distributed
+
+    out = []
+    for name, n, edges, opt, pvc in cases:
+        n, off, nbr = csr(n, edges)
+        g = vc.StaticGraph(n, off, nbr)
+        r = solve_distributed(g, vc.SolverConfig(), subtrees_per_rank=3)
+        ks = {int(k): solve_distributed(g, vc.SolverConfig(mode="pvc", k=int(k)),
+                                        subtrees_per_rank=3).found for k in pvc}
+        out.append((name, r.cover_size, r.exact, ks))
+    q.put((rank, out))
+    dist.destroy_process_group()
+
+
+def test_two_ranks_share_one_gpu():
+    """The GPU backend at world size 2 (two processes on cuda:0 over gloo):
+    subtrees from the store's ticket counter, bounds and PVC stops through the
+    store and each rank's vcg_exchange -- the reference's answers on every rank."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cases = [(c["name"], c["n"], c["edges"], c["runs"]["det"]["cover_size"],
+              {k: e["found"] for k, e in c["pvc"].items()})
+             for c in golden("solve.json")[::9] if c["n"] > 0]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, cases, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=900) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert res[0] == res[1]
+    for (name, _, _, opt, pvc), (name2, mvc, exact, ks) in zip(cases, res[0]):
+        assert name == name2 and mvc == opt and exact, name
+        assert ks == {int(k): f for k, f in pvc.items()}, name
