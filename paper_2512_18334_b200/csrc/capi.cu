@@ -1541,7 +1541,8 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
     return VCG_ERESOURCE;
   if (C.stacks.ensure((size_t)(stack_cap * slot * blocks)) || C.qseq.ensure((size_t)qcap * 8) ||
       C.qdata.ensure((size_t)(qcap * slot)) || C.qctl.ensure(64) ||
-      C.reg.ensure((size_t)reg_cap * (4 * 13 + 8) + 64) || C.ctl.ensure(sizeof(Ctl)) ||
+      C.reg.ensure((size_t)reg_cap * (4 * 13 + 8) + 64 + 8 * kFreeClasses) ||
+      C.ctl.ensure(sizeof(Ctl)) ||
       C.hist.ensure((size_t)(n + 2) * 8) ||
       (!in_smem && C.gws.ensure((size_t)(wsb * blocks))))
     return VCG_ERESOURCE;
@@ -1582,7 +1583,12 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   R.count = rb + 13 * reg_cap;
   R.wkey = (unsigned long long*)(rb + 13 * reg_cap + 16);  // 64-byte aligned
   R.cap = reg_cap;
+  R.fheads = R.wkey + reg_cap;
   const int record = cfg->record_cover != 0;
+  // registry reclamation: parallel mode, unless the entries are read back
+  // (record-cover witnesses, audits, the registry view) -- VCG_NO_RECLAIM=1 off
+  R.reclaim = !record && !cfg->deterministic && !cfg->check_registry && !cfg->registry_out &&
+              !getenv("VCG_NO_RECLAIM");
   const int nw = (n + 31) / 32;
   int wcap = 0;
   if (record) {

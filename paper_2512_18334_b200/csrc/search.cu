@@ -162,14 +162,22 @@ struct Worker {
     if (threadIdx.x == 0) {
       int g = -1;
       const long long words = (long long)offw + m2c;
-      const long long b = atomicAdd(P.arena_top, (int)words);
-      if (b + words <= (long long)P.arena_cap) {
-        g = atomicAdd(P.sg_count, 1);
-        if (g >= P.sg_cap) {
-          g = -1;
-        } else {
-          P.sg_base[g] = (int)b;
-          P.sg_n[g] = size;
+      long long b = -1;
+      // the arena is bump-allocated for the whole search; once it is full
+      // (or the subgraph table is), components stay in the parent's graph.
+      // Check before claiming: a counter advanced by every failed claim of a
+      // long search would overflow int and alias live subgraphs.
+      if (ld_relaxed(P.arena_top) + words <= (long long)P.arena_cap &&
+          ld_relaxed(P.sg_count) < P.sg_cap) {
+        b = atomicAdd(P.arena_top, (int)words);
+        if (b + words <= (long long)P.arena_cap) {
+          g = atomicAdd(P.sg_count, 1);
+          if (g >= P.sg_cap) {
+            g = -1;
+          } else {
+            P.sg_base[g] = (int)b;
+            P.sg_n[g] = size;
+          }
         }
       }
       st->v = g;
@@ -412,8 +420,8 @@ struct Worker {
       const Registry& R = P.reg;
       const int scope = h.scope;
       lb.inc(P, scope);  // slot for the parent entry's finalisation
-      int base = atomicAdd(R.count, 1 + G);
-      if (base + 1 + G > R.cap) {
+      int base = reg_alloc(R, 1 + G);
+      if (base < 0) {
         atomicExch(&P.ctl->error, 1);
         atomicExch(&P.ctl->stop, 1);
         base = -1;
@@ -935,6 +943,7 @@ __global__ void search_init_kernel(SearchParams P, int root_key, unsigned long l
       *P.wcount = 0;
     }
     *R.count = 1;
+    for (int c = 0; c < kFreeClasses; ++c) R.fheads[c] = 0xffffffffull;
     *P.q.head = 0ull;
     *P.q.tail = 0ull;
     *P.q.count = 0ull;

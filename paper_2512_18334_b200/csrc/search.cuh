@@ -43,7 +43,52 @@ struct Registry {
   int* pwrec;         // record-cover: parent entry's arena record (path + special covers)
   int* count;         // arena size (device counter)
   int cap;
+  // Reclamation (parallel mode without record-cover / audits): a split's
+  // group (parent + its child entries, contiguous) is dead once the parent's
+  // cascade has submitted to its ancestor -- every reader holds a live node
+  // below it until then -- so it goes on a free stack for groups of its size
+  // class (power of two).  Tagged Treiber stacks, next pointer in the free
+  // group's link field.  Without reclamation groups are bump-allocated.
+  unsigned long long* fheads;  // [kFreeClasses]: tag << 32 | top group (0xffffffff: empty)
+  int reclaim;
 };
+
+constexpr int kFreeClasses = 32;
+
+__device__ __forceinline__ int reg_class(int sz) { return sz <= 1 ? 0 : 32 - __clz(sz - 1); }
+
+// base of a group of sz entries, or -1 when the arena is exhausted
+__device__ inline int reg_alloc(const Registry& R, int sz) {
+  if (R.reclaim) {
+    const int c = reg_class(sz);
+    unsigned long long* h = &R.fheads[c];
+    while (true) {
+      const unsigned long long old = ld_acquire_u64(h);
+      const unsigned top = (unsigned)old;
+      if (top == 0xffffffffu) break;
+      const unsigned nxt = (unsigned)ld_relaxed(&R.link[top]);
+      const unsigned long long nw = (((old >> 32) + 1ull) << 32) | nxt;
+      if (atomicCAS(h, old, nw) == old) return (int)top;
+    }
+    sz = 1 << c;
+  }
+  const int base = atomicAdd(R.count, sz);
+  return base + sz > R.cap ? -1 : base;
+}
+
+// the group of parent entry p is dead: recycle it
+__device__ inline void reg_free_group(const Registry& R, int p) {
+  if (!R.reclaim) return;
+  const int c = reg_class(1 + R.nchild[p]);
+  unsigned long long* h = &R.fheads[c];
+  while (true) {
+    const unsigned long long old = ld_relaxed_u64(h);
+    R.link[p] = (int)(unsigned)old;
+    __threadfence();
+    const unsigned long long nw = (((old >> 32) + 1ull) << 32) | (unsigned)p;
+    if (atomicCAS(h, old, nw) == old) return;
+  }
+}
 
 struct Ctl {
   int stop, found, timed_out, error;
@@ -371,6 +416,7 @@ __device__ inline void reg_cascade(const SearchParams& P, int idx) {
       int ach = ld_relaxed(&R.sum_ach[idx]);
       int anc = R.link[idx];
       reg_submit(P, anc, total, ach != 0, kComposite | (unsigned)idx);
+      reg_free_group(R, idx);
       if (atomicSub(&R.live[anc], 1) != 1) return;
       idx = anc;
     }

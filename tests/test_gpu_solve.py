@@ -229,3 +229,28 @@ def test_solve_batch_matches_sequential():
     graphs = [_graph(c) for c in cases]
     rs = vc.solve_batch(graphs, [vc.SolverConfig() for _ in cases])
     assert [r.cover_size for r in rs] == [c["runs"]["det"]["cover_size"] for c in cases]
+
+
+def test_registry_reclamation_answers_and_reuse():
+    """Parallel solves recycle dead split groups (registry reclamation, off in
+    the parity / audit modes): answers unchanged, and a split-heavy search
+    runs with fewer entries than it made splits."""
+    import paper_2512_18334_b200 as vc
+    from paper_2512_18334_b200 import synth
+
+    for case in golden("solve.json")[::3]:
+        g = _graph(case)
+        r = vc.solve(g, vc.SolverConfig())
+        assert r.cover_size == case["runs"]["det"]["cover_size"], case["name"]
+    exp = golden("workloads.json")["rgg2000"]
+    n, off, nbr = synth.WORKLOADS["rgg2000"]()
+    g = vc.StaticGraph(n, off, nbr)
+    for _ in range(3):
+        r = vc.solve(g, vc.SolverConfig())
+        assert r.cover_size == exp["mvc"]
+        assert len(r.registry) < r.stats.component_branches  # groups were reused
+    # split-heavy and long (bounded): no arena / registry exhaustion
+    n, off, nbr = synth.gnp(250, 0.06, 1)
+    r = vc.solve(vc.StaticGraph(n, off, nbr), vc.SolverConfig(timeout=4.0))
+    assert r.stats.component_branches > len(r.registry)
+    assert r.cover_size is not None
