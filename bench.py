@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-other-configs", action="store_true")
+    ap.add_argument("--no-strong", action="store_true")
     return ap.parse_args()
 
 
@@ -291,6 +292,54 @@ def other_configs(vc, torch, reps=5):
     return out
 
 
+STRONG = {"n": 180, "p": 0.08, "seed": 1, "mvc": 136, "subtrees": 128}
+
+
+def strong_scaling(vc, torch, world, ndev, barrier, steps=2):
+    """ONE hard instance across all ranks (distributed.solve_distributed:
+    subtrees from the store's ticket counter, in-flight bound exchange):
+    time-to-solution and search-tree nodes/s at this N.  The instance is the
+    configs[4] family (dense-ish Erdos-Renyi) at the size whose exact MVC one
+    GPU proves in seconds; its optimum is pinned by the C oracle
+    (tests/golden/strong.json)."""
+    from paper_2512_18334_b200.distributed import solve_distributed
+
+    synth = load_synth()
+    per = -(-STRONG["subtrees"] // world)  # the same total partition at every N
+    n, off, nbr = synth.gnp(STRONG["n"], STRONG["p"], STRONG["seed"])
+    g = vc.StaticGraph(n, off, nbr)
+
+    def one():
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = solve_distributed(g, vc.SolverConfig(), subtrees_per_rank=per)
+        e1.record()
+        torch.cuda.synchronize()
+        if r.cover_size != STRONG["mvc"] or not r.exact:
+            raise RuntimeError(f"strong instance: MVC {r.cover_size}, expected {STRONG['mvc']}")
+        return e0.elapsed_time(e1), r.stats.tree_nodes_visited
+
+    one()  # warm-up
+    ms, nodes = 0.0, 0
+    for _ in range(steps):
+        t, nd = one()
+        ms += t
+        nodes += nd
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device="cuda" if world <= ndev else "cpu")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt[0])
+    tts = ms / steps * 1e-3
+    return {"workload": f"MVC on G(n={STRONG['n']}, p={STRONG['p']}), seed {STRONG['seed']} "
+                        f"(configs[4] family, exact): one instance across all {world} GPU(s)",
+            "n_gpus": world, "scaling": "strong", "steps": steps, "warmup": 1,
+            "time_to_solution_s": tts, "nodes_per_s": nodes / (ms * 1e-3),
+            "tree_nodes_per_solve": nodes / steps, "mvc": STRONG["mvc"],
+            "subtrees": STRONG["subtrees"], "subtrees_per_rank": per,
+            "timing": "CUDA events around solve_distributed, max over ranks"}
+
+
 def run_b200(args):
     import numpy as np
     import torch
@@ -382,6 +431,8 @@ def run_b200(args):
     # reduced CSR (int32) and the result structs
     d2h = 4 * pre_forced + 8 * rn + 4 * (rn + 1) + 8 * rm + 512
 
+    strong = None if args.no_strong else strong_scaling(vc, torch, world, ndev, barrier)
+
     t = torch.tensor([total_ms, e2e_ms, nodes], dtype=torch.float64,
                      device="cuda" if world <= ndev else "cpu")
     if world > 1:
@@ -459,6 +510,8 @@ def run_b200(args):
         },
         "clocks": clk.summary(),
     }
+    if strong is not None:
+        line["strong_scaling"] = strong
     if not args.no_other_configs:
         line["other_configs"] = other_configs(vc, torch)
     if not args.no_cpu_baseline:
