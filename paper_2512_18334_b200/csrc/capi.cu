@@ -1541,7 +1541,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
     return VCG_ERESOURCE;
   if (C.stacks.ensure((size_t)(stack_cap * slot * blocks)) || C.qseq.ensure((size_t)qcap * 8) ||
       C.qdata.ensure((size_t)(qcap * slot)) || C.qctl.ensure(64) ||
-      C.reg.ensure((size_t)reg_cap * (4 * 13 + 8) + 64 + 8 * kFreeClasses) ||
+      C.reg.ensure((size_t)reg_cap * (4 * 13 + 8) + 64 + 8 * kFreeClasses * kFreeShards) ||
       C.ctl.ensure(sizeof(Ctl)) ||
       C.hist.ensure((size_t)(n + 2) * 8) ||
       (!in_smem && C.gws.ensure((size_t)(wsb * blocks))))
@@ -1589,6 +1589,8 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   // (record-cover witnesses, audits, the registry view) -- VCG_NO_RECLAIM=1 off
   R.reclaim = !record && !cfg->deterministic && !cfg->check_registry && !cfg->registry_out &&
               !getenv("VCG_NO_RECLAIM");
+  // recycling starts at half the arena (VCG_RECLAIM_AT: entries, tests use 0)
+  R.reclaim_at = getenv("VCG_RECLAIM_AT") ? atoi(getenv("VCG_RECLAIM_AT")) : reg_cap / 2;
   const int nw = (n + 31) / 32;
   int wcap = 0;
   if (record) {

@@ -943,7 +943,7 @@ __global__ void search_init_kernel(SearchParams P, int root_key, unsigned long l
       *P.wcount = 0;
     }
     *R.count = 1;
-    for (int c = 0; c < kFreeClasses; ++c) R.fheads[c] = 0xffffffffull;
+    for (int c = 0; c < kFreeClasses * kFreeShards; ++c) R.fheads[c] = 0xffffffffull;
     *P.q.head = 0ull;
     *P.q.tail = 0ull;
     *P.q.count = 0ull;

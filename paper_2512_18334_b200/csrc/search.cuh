@@ -49,28 +49,41 @@ struct Registry {
   // below it until then -- so it goes on a free stack for groups of its size
   // class (power of two).  Tagged Treiber stacks, next pointer in the free
   // group's link field.  Without reclamation groups are bump-allocated.
-  unsigned long long* fheads;  // [kFreeClasses]: tag << 32 | top group (0xffffffff: empty)
+  // Recycling starts once the arena is half used (short searches never pay
+  // for it) and the stacks are sharded by block to spread the CAS traffic.
+  unsigned long long* fheads;  // [kFreeClasses][kFreeShards]: tag << 32 | top (0xffffffff: empty)
   int reclaim;
+  int reclaim_at;  // arena entries in use from which groups are recycled
 };
 
 constexpr int kFreeClasses = 32;
+constexpr int kFreeShards = 16;
 
 __device__ __forceinline__ int reg_class(int sz) { return sz <= 1 ? 0 : 32 - __clz(sz - 1); }
+
+__device__ __forceinline__ bool reg_recycling(const Registry& R) {
+  return R.reclaim && ld_relaxed(R.count) >= R.reclaim_at;
+}
 
 // base of a group of sz entries, or -1 when the arena is exhausted
 __device__ inline int reg_alloc(const Registry& R, int sz) {
   if (R.reclaim) {
     const int c = reg_class(sz);
-    unsigned long long* h = &R.fheads[c];
-    while (true) {
-      const unsigned long long old = ld_acquire_u64(h);
-      const unsigned top = (unsigned)old;
-      if (top == 0xffffffffu) break;
-      const unsigned nxt = (unsigned)ld_relaxed(&R.link[top]);
-      const unsigned long long nw = (((old >> 32) + 1ull) << 32) | nxt;
-      if (atomicCAS(h, old, nw) == old) return (int)top;
+    if (reg_recycling(R)) {
+      for (int k = 0; k < kFreeShards; ++k) {
+        unsigned long long* h =
+            &R.fheads[c * kFreeShards + (blockIdx.x + k) % kFreeShards];
+        while (true) {
+          const unsigned long long old = ld_acquire_u64(h);
+          const unsigned top = (unsigned)old;
+          if (top == 0xffffffffu) break;
+          const unsigned nxt = (unsigned)ld_relaxed(&R.link[top]);
+          const unsigned long long nw = (((old >> 32) + 1ull) << 32) | nxt;
+          if (atomicCAS(h, old, nw) == old) return (int)top;
+        }
+      }
     }
-    sz = 1 << c;
+    sz = 1 << c;  // a recyclable group occupies its whole size class
   }
   const int base = atomicAdd(R.count, sz);
   return base + sz > R.cap ? -1 : base;
@@ -78,9 +91,9 @@ __device__ inline int reg_alloc(const Registry& R, int sz) {
 
 // the group of parent entry p is dead: recycle it
 __device__ inline void reg_free_group(const Registry& R, int p) {
-  if (!R.reclaim) return;
+  if (!reg_recycling(R)) return;
   const int c = reg_class(1 + R.nchild[p]);
-  unsigned long long* h = &R.fheads[c];
+  unsigned long long* h = &R.fheads[c * kFreeShards + blockIdx.x % kFreeShards];
   while (true) {
     const unsigned long long old = ld_relaxed_u64(h);
     R.link[p] = (int)(unsigned)old;

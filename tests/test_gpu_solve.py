@@ -231,12 +231,15 @@ def test_solve_batch_matches_sequential():
     assert [r.cover_size for r in rs] == [c["runs"]["det"]["cover_size"] for c in cases]
 
 
-def test_registry_reclamation_answers_and_reuse():
+def test_registry_reclamation_answers_and_reuse(monkeypatch):
     """Parallel solves recycle dead split groups (registry reclamation, off in
-    the parity / audit modes): answers unchanged, and a split-heavy search
-    runs with fewer entries than it made splits."""
+    the parity / audit modes; recycling from the first split here, from half
+    the arena by default): answers unchanged, and a split-heavy search runs
+    with fewer entries than it made splits."""
     import paper_2512_18334_b200 as vc
     from paper_2512_18334_b200 import synth
+
+    monkeypatch.setenv("VCG_RECLAIM_AT", "0")
 
     for case in golden("solve.json")[::3]:
         g = _graph(case)
