@@ -150,10 +150,12 @@ typedef struct {
   const int32_t* root_deg;    /* NULL: search the whole graph.  Else the residual
                                  degree array (n entries) of a subtree root, e.g. one
                                  produced by vcg_expand; covers are counted from it */
-  int warp_limit;             /* warp tier: subproblems with <= warp_limit (<= 64) live
+  int warp_limit;             /* warp tier: subproblems with <= warp_limit (<= 128) live
                                  vertices are solved by one warp as bitmask tasks;
-                                 0 = off.  Ignored (off) in deterministic, record-cover,
-                                 no-components and no-pruning runs. */
+                                 0 = off, < 0 = auto (128 when the graph's average
+                                 degree is >= 8, else 64).  Ignored (off) in
+                                 deterministic, record-cover, no-components and
+                                 no-pruning runs. */
   int gpu_share;              /* concurrent searches sharing the device (>= 1): each
                                  takes 1/gpu_share of the resident block slots.  Calls
                                  from different host threads run concurrently (each

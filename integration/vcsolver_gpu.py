@@ -158,7 +158,7 @@ def solve(g, config=None):
                           load_balance=int(get("load_balance", True)),
                           workers=int(get("workers", 0) if not get("deterministic", False)
                                       else 1),
-                          timeout=float(get("timeout", None) or 0.0), warp_limit=64,
+                          timeout=float(get("timeout", None) or 0.0), warp_limit=-1,
                           gpu_share=1)
         res = SearchResult()
         hist = np.zeros(int(info.n_reduced) + 2, dtype=np.int64)

@@ -1436,7 +1436,13 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   const long long smem_limit = (long long)smem_optin - 8192;  // static smem headroom
   const int smem_fits = wsb <= smem_limit && !getenv("VCG_WS_GLOBAL");
   const long long csrb = csr_smem_bytes(n, g->m2);
-  int warp_limit0 = std::min(std::max(cfg->warp_limit, 0), kWMax);
+  // warp tier limit; < 0 = auto: 128-vertex tasks on dense reduced graphs
+  // (average degree >= 8: G(180, 0.08) 7.7 s -> 1.05 s), 64 on sparse ones,
+  // whose component splits already fit 64 and whose long 128-vertex tasks
+  // would serialise (rgg2000 PVC 1.2 -> 8.9 ms)
+  int warp_limit0 = cfg->warp_limit;
+  if (warp_limit0 < 0) warp_limit0 = g->m2 >= 8LL * g->n ? kWMax : 64;
+  warp_limit0 = std::min(warp_limit0, kWMax);
   if (cfg->deterministic || cfg->record_cover || !cfg->use_components || cfg->disable_pruning ||
       !cfg->load_balance)
     warp_limit0 = 0;
@@ -1457,11 +1463,12 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
     // warp tier: per-warp workspaces alias the node workspace's int scratch
     // (ia .. par, 7 arrays; the tier runs only while the block holds no node)
     // when that is large enough, else they follow in dynamic shared memory
-    pl->warp_limit = th > 512 ? 0 : warp_limit0;
+    pl->warp_limit = th > 32 * kWTierWarps ? 0 : warp_limit0;
     pl->bws_alias = 0;
     pl->bws_off = 0;
     if (pl->warp_limit) {
-      const long long need = (long long)(th / 32) * (long long)sizeof(WarpWs);
+      const long long need = (long long)(th / 32) *
+                             (long long)(warp_limit0 > 64 ? sizeof(WarpWs2) : sizeof(WarpWs1));
       const long long ni = ((long long)std::max(n, 1) + 3) & ~3LL;
       if (ws_smem && 7 * ni * 4 >= need) {
         pl->bws_alias = 1;

@@ -72,7 +72,7 @@ struct Worker {
   // ------------------------------------------------------- warp tasks --
   // One warp (all lanes) packs the live vertices of the current node in
   // [lo, hi] that belong to component `root` (root < 0: all of them) --
-  // `size` of them, <= 64 -- into a warp-tier task: local ids follow the
+  // `size` of them, <= kWMax -- into a warp-tier task: local ids follow the
   // reduced graph's order (so lowest-index tie-breaks are unchanged), rows
   // are adjacency bitmasks.  Returns false when the task ring is full.
   __device__ bool emit_task(int root, int size, int lo, int hi, int scope, int S, int depth,
@@ -105,18 +105,27 @@ struct Worker {
     }
     __syncwarp();
     unsigned long long* adj = (unsigned long long*)(slot + kWHdrBytes);
+    const int W = wrows(size);  // 64-bit words per row
     for (int i = lane; i < size; i += 32) {
       const int v = gv[i];
-      unsigned long long mk = 0;
+      unsigned long long mk0 = 0, mk1 = 0;
       for (int k = w.off[v]; k < w.off[v + 1]; ++k) {
         const int x = w.nbr[k];
-        if (w.deg[x] > 0) mk |= 1ull << w.ia[x];
+        if (w.deg[x] > 0) {
+          const int b = w.ia[x];
+          if (b < 64) mk0 |= 1ull << b;
+          else mk1 |= 1ull << (b - 64);
+        }
       }
-      __stcg(adj + i, mk);
+      __stcg(adj + W * i, mk0);
+      if (W > 1) __stcg(adj + W * i + 1, mk1);
     }
     if (lane == 0) {
       __stcg((int4*)slot, make_int4(S, scope, size | (counted << 16), depth));
-      __stcg((unsigned long long*)(slot + 16), size == 64 ? ~0ull : ((1ull << size) - 1));
+      const unsigned long long lo = size >= 64 ? ~0ull : ((1ull << size) - 1);
+      const unsigned long long hi =
+          size >= 128 ? ~0ull : size > 64 ? ((1ull << (size - 64)) - 1) : 0ull;
+      __stcg((ulonglong2*)(slot + 16), make_ulonglong2(lo, hi));
     }
     __syncwarp();
     if (lane == 0) q_publish_push(P.bq, pos);
@@ -723,7 +732,7 @@ __global__ void __launch_bounds__(VCG_SEARCH_MAXT, VCG_SEARCH_MINB) search_kerne
   extern __shared__ __align__(16) unsigned char dsmem[];
   __shared__ BlockScratch bs;
   __shared__ BlockState st;
-  __shared__ int wgl[16][kWMax];
+  __shared__ int wgl[kWTierWarps][kWMax];  // the warp tier runs in blocks of <= 256 threads
   __shared__ int wbusy;
   char* base = kSmem ? (char*)dsmem : P.gws + (long long)blockIdx.x * P.gws_bytes;
   NodeWs<T> ws = carve_ws<T>(base, P.n, &bs, P.off, P.nbr);
@@ -766,9 +775,9 @@ __global__ void __launch_bounds__(VCG_SEARCH_MAXT, VCG_SEARCH_MINB) search_kerne
   wk.gl = wgl;
   wk.soff = csr_soff;
   wk.snbr = csr_snbr;
-  WarpWs* wws = nullptr;
+  void* wws = nullptr;
   if (P.warp_limit)
-    wws = (WarpWs*)((kSmem && P.bws_alias) ? (char*)ws.ia : (char*)dsmem + P.bws_off);
+    wws = (kSmem && P.bws_alias) ? (void*)ws.ia : (void*)((char*)dsmem + P.bws_off);
   WStats wst;
   memset(&wst, 0, sizeof(wst));
   if (threadIdx.x == 0) wbusy = 0;
@@ -834,7 +843,8 @@ __global__ void __launch_bounds__(VCG_SEARCH_MAXT, VCG_SEARCH_MINB) search_kerne
             __syncthreads();
             wk.tick(PH_IDLE);
             VCG_HB(&bs, 60);
-            const bool ran = warp_epoch(P, wws, &wbusy, wst);
+            const bool ran = P.warp_limit > 64 ? warp_epoch<2>(P, wws, &wbusy, wst)
+                                                : warp_epoch<1>(P, wws, &wbusy, wst);
             VCG_HB(&bs, 61);
             if (threadIdx.x == 0) {
               const long long now = clock64();

@@ -1,4 +1,4 @@
-// Warp tier of the search: a subproblem with at most 64 live vertices is
+// Warp tier of the search: a subproblem with at most 128 live vertices is
 // solved by ONE warp as bitmask branch-and-reduce.
 //
 // Why: on the component-splitting workloads (configs[1], the RGG) the search
@@ -6,10 +6,13 @@
 // spans ~540 vertices of the reduced graph (87% of the nodes have <= 32 live
 // vertices, 97.6% <= 64).  A whole thread block sweeping a 1 KB degree
 // record per node is the wrong granularity for them.  Here a task is the
-// induced subgraph itself -- 64 adjacency bitmasks (512 B) held in
-// registers, two rows per lane -- and a search node is a 64-bit live mask
-// plus a cover count, so a node costs a few hundred warp instructions and no
-// block barrier, HBM record or registry atomic.
+// induced subgraph itself -- up to 128 adjacency bitmasks held in registers,
+// one to four rows per lane -- and a search node is a live mask plus a
+// cover count, so a node costs a few hundred warp instructions and no block
+// barrier, HBM record or registry atomic.  Masks are 32, 64 or 128 bits wide
+// by task size: dense instances (configs[4]) have most of their search
+// nodes at 65-128 live vertices, which the 128-bit tier takes off the block
+// tier.
 //
 // Semantics (reference engine.py:277 _process_node, kernels/pure.py rules,
 // engine.py:334 _try_component_split) are preserved as sets, not as
@@ -40,22 +43,23 @@ namespace vcg {
 #define WPROF(...)
 #endif
 
-constexpr int kWMax = 64;      // vertices per warp task
-constexpr int kWStack = 72;    // DFS stack entries per warp (depth <= 64)
-constexpr int kWFrames = 24;   // nested component frames (each >= 6 vertices)
-constexpr int kWPend = 32;     // pending component masks over all frames
+constexpr int kWMax = 128;            // vertices per warp task
+constexpr int kWFrames = 24;          // nested component frames (each >= 6 vertices)
+constexpr int kWTierWarps = 8;        // warps of a block that runs the warp tier (<= 256 threads)
+constexpr int kWPend = 32;            // pending component masks over all frames
 
-// warp-task record: 32 B header + adjacency rows (n used of 64)
+// warp-task record: 32 B header + adjacency rows of n vertices, each row
+// wrows(n) 64-bit words (1 for n <= 64, 2 up to 128)
 struct WTaskHdr {
   int S;      // cover size of the task's root within its registry scope
   int scope;  // registry entry the task reports to (it holds one live unit)
   int n;      // vertices | (root already counted as a tree node) << 16
   int depth;
-  unsigned long long live;  // live vertices of the task's root node
-  unsigned long long pad;
+  unsigned long long live, live_hi;  // live vertices of the task's root node (128 bits)
 };
 constexpr long long kWHdrBytes = 32;
-constexpr long long kWSlotBytes = kWHdrBytes + 8 * kWMax;
+constexpr long long kWSlotBytes = kWHdrBytes + 16 * kWMax;
+__host__ __device__ __forceinline__ int wrows(int n) { return n > 64 ? 2 : 1; }
 // a task polls every 4 nodes and may shed work after 4 (capi.cu; VCG_WCHECK /
 // VCG_WEXPORT override): on rgg2000 PVC(opt-1) 1.40 -> 1.28 ms vs every 16 / after 64
 
@@ -68,13 +72,22 @@ struct WFrame {
   int pad0, pad1;
 };
 
-struct WarpWs {
-  unsigned long long adj[kWMax];
-  unsigned long long stL[kWStack];
-  unsigned long long pend[kWPend];
-  int stS[kWStack];
+// per-warp shared-memory workspace for tasks of up to 64 * WW vertices;
+// masks are stored as WW 64-bit words (the 64-vertex layout keeps the
+// round-1 footprint, so the launch plan of sparse workloads is unchanged)
+template <int WW>
+struct WarpWsT {
+  static constexpr int kW = WW;
+  static constexpr int kMax = 64 * WW;
+  static constexpr int kStack = kMax + 8;  // DFS depth <= kMax
+  unsigned long long adj[WW * kMax];
+  unsigned long long stL[WW * kStack];
+  unsigned long long pend[WW * kWPend];
+  int stS[kStack];
   WFrame fr[kWFrames];
 };
+using WarpWs1 = WarpWsT<1>;
+using WarpWs2 = WarpWsT<2>;
 
 struct WStats {
   unsigned long long tasks, nodes, splits, cyc, maxcyc, max_nodes, max_n;
@@ -83,49 +96,125 @@ struct WStats {
   unsigned long long rules[6];
 };
 
+// ------------------------------------------------------------ masks --
+// Three task widths: <= 32 vertices on 32-bit masks (one vertex per lane),
+// <= 64 on 64-bit masks (two per lane), <= 128 on 128-bit masks (four per
+// lane).  Lane l owns vertices l + 32 r; the ballot of every lane's r-th
+// vertex is bits [32 r, 32 r + 32) of a mask, so a collective over the
+// warp's vertices is R ballots / OR-reductions, no cross-lane shuffles.
+struct W128 {
+  unsigned long long lo, hi;
+};
+__device__ __forceinline__ W128 operator&(W128 a, W128 b) { return {a.lo & b.lo, a.hi & b.hi}; }
+__device__ __forceinline__ W128 operator|(W128 a, W128 b) { return {a.lo | b.lo, a.hi | b.hi}; }
+__device__ __forceinline__ W128 operator~(W128 a) { return {~a.lo, ~a.hi}; }
+__device__ __forceinline__ W128& operator&=(W128& a, W128 b) { a = a & b; return a; }
+__device__ __forceinline__ W128& operator|=(W128& a, W128 b) { a = a | b; return a; }
+__device__ __forceinline__ bool operator==(W128 a, W128 b) { return a.lo == b.lo && a.hi == b.hi; }
+__device__ __forceinline__ bool operator!=(W128 a, W128 b) { return !(a == b); }
+
+template <typename M> struct WT;
+template <> struct WT<unsigned> { static constexpr int R = 1; };
+template <> struct WT<unsigned long long> { static constexpr int R = 2; };
+template <> struct WT<W128> { static constexpr int R = 4; };
+
+__device__ __forceinline__ bool nz(unsigned x) { return x != 0u; }
+__device__ __forceinline__ bool nz(unsigned long long x) { return x != 0ull; }
+__device__ __forceinline__ bool nz(W128 x) { return (x.lo | x.hi) != 0ull; }
+
 __device__ __forceinline__ unsigned long long wor64(unsigned long long x) {
   const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)x);
   const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(x >> 32));
   return ((unsigned long long)hi << 32) | lo;
 }
-
-__device__ __forceinline__ unsigned long long ballot64(bool a, bool b) {
-  return (unsigned long long)__ballot_sync(0xffffffffu, a) |
-         ((unsigned long long)__ballot_sync(0xffffffffu, b) << 32);
-}
-
-// Mask helpers for both task widths: tasks of <= 32 vertices run on 32-bit
-// masks (one vertex per lane: one ballot / reduction per collective, no
-// 64-bit emulation), larger ones on 64-bit masks (two vertices per lane).
 __device__ __forceinline__ unsigned wor(unsigned x) { return __reduce_or_sync(0xffffffffu, x); }
 __device__ __forceinline__ unsigned long long wor(unsigned long long x) { return wor64(x); }
+__device__ __forceinline__ W128 wor(W128 x) { return {wor64(x.lo), wor64(x.hi)}; }
 __device__ __forceinline__ int wpopc(unsigned x) { return __popc(x); }
 __device__ __forceinline__ int wpopc(unsigned long long x) { return __popcll(x); }
+__device__ __forceinline__ int wpopc(W128 x) { return __popcll(x.lo) + __popcll(x.hi); }
 __device__ __forceinline__ int wlsb(unsigned x) { return __ffs((int)x) - 1; }
 __device__ __forceinline__ int wlsb(unsigned long long x) { return __ffsll((long long)x) - 1; }
+__device__ __forceinline__ int wlsb(W128 x) {
+  return x.lo ? __ffsll((long long)x.lo) - 1 : (x.hi ? 63 + __ffsll((long long)x.hi) : -1);
+}
 __device__ __forceinline__ int wmsb(unsigned x) { return 31 - __clz((int)x); }
 __device__ __forceinline__ int wmsb(unsigned long long x) { return 63 - __clzll((long long)x); }
+__device__ __forceinline__ int wmsb(W128 x) {
+  return x.hi ? 127 - __clzll((long long)x.hi) : 63 - __clzll((long long)x.lo);
+}
+__device__ __forceinline__ unsigned wclr(unsigned x) { return x & (x - 1u); }
+__device__ __forceinline__ unsigned long long wclr(unsigned long long x) { return x & (x - 1ull); }
+__device__ __forceinline__ W128 wclr(W128 x) {
+  return x.lo ? W128{x.lo & (x.lo - 1ull), x.hi} : W128{0ull, x.hi & (x.hi - 1ull)};
+}
 template <typename M>
-__device__ __forceinline__ M wbit(int i) { return (M)1 << i; }
+__device__ __forceinline__ M wbit(int i);
+template <>
+__device__ __forceinline__ unsigned wbit<unsigned>(int i) { return 1u << i; }
+template <>
+__device__ __forceinline__ unsigned long long wbit<unsigned long long>(int i) { return 1ull << i; }
+template <>
+__device__ __forceinline__ W128 wbit<W128>(int i) {
+  return i < 64 ? W128{1ull << i, 0ull} : W128{0ull, 1ull << (i - 64)};
+}
 // vertex v live in L (v >= the mask width: never)
 __device__ __forceinline__ bool whas(unsigned L, int v) { return v < 32 && ((L >> v) & 1u); }
-__device__ __forceinline__ bool whas(unsigned long long L, int v) { return (L >> v) & 1ull; }
+__device__ __forceinline__ bool whas(unsigned long long L, int v) { return v < 64 && ((L >> v) & 1ull); }
+__device__ __forceinline__ bool whas(W128 L, int v) {
+  return v < 64 ? ((L.lo >> v) & 1ull) : (v < 128 && ((L.hi >> (v - 64)) & 1ull));
+}
+// mask from per-lane predicates p[r] on the lane's r-th vertex
 template <typename M>
-__device__ __forceinline__ M wballot(bool a, bool b);
+__device__ __forceinline__ M wballot(const bool (&p)[WT<M>::R]);
 template <>
-__device__ __forceinline__ unsigned wballot<unsigned>(bool a, bool) {
-  return __ballot_sync(0xffffffffu, a);
+__device__ __forceinline__ unsigned wballot<unsigned>(const bool (&p)[1]) {
+  return __ballot_sync(0xffffffffu, p[0]);
 }
 template <>
-__device__ __forceinline__ unsigned long long wballot<unsigned long long>(bool a, bool b) {
-  return ballot64(a, b);
+__device__ __forceinline__ unsigned long long wballot<unsigned long long>(const bool (&p)[2]) {
+  return (unsigned long long)__ballot_sync(0xffffffffu, p[0]) |
+         ((unsigned long long)__ballot_sync(0xffffffffu, p[1]) << 32);
+}
+template <>
+__device__ __forceinline__ W128 wballot<W128>(const bool (&p)[4]) {
+  return {(unsigned long long)__ballot_sync(0xffffffffu, p[0]) |
+              ((unsigned long long)__ballot_sync(0xffffffffu, p[1]) << 32),
+          (unsigned long long)__ballot_sync(0xffffffffu, p[2]) |
+              ((unsigned long long)__ballot_sync(0xffffffffu, p[3]) << 32)};
+}
+// masks in the workspace: two 64-bit words each
+template <typename M>
+__device__ __forceinline__ M wload(const unsigned long long* p);
+template <>
+__device__ __forceinline__ unsigned wload<unsigned>(const unsigned long long* p) { return (unsigned)p[0]; }
+template <>
+__device__ __forceinline__ unsigned long long wload<unsigned long long>(const unsigned long long* p) {
+  return p[0];
+}
+template <>
+__device__ __forceinline__ W128 wload<W128>(const unsigned long long* p) { return {p[0], p[1]}; }
+template <int WW>
+__device__ __forceinline__ void wstore(unsigned long long* p, unsigned x) {
+  p[0] = x;
+  if (WW > 1) p[1] = 0ull;
+}
+template <int WW>
+__device__ __forceinline__ void wstore(unsigned long long* p, unsigned long long x) {
+  p[0] = x;
+  if (WW > 1) p[1] = 0ull;
+}
+template <int WW>
+__device__ __forceinline__ void wstore(unsigned long long* p, W128 x) {
+  p[0] = x.lo;
+  if (WW > 1) p[1] = x.hi;
 }
 
-// Per-lane view of the task graph: this lane owns vertices lane and lane+32.
+// Per-lane view of the task graph: this lane owns vertices lane + 32 r.
 template <typename M>
 struct WLane {
-  M a0, a1;  // adjacency rows of the two vertices (32-bit tasks: a1 = 0, v1 = 64)
-  int v0, v1;
+  M a[WT<M>::R];    // adjacency rows of the lane's vertices (0 beyond n)
+  int v[WT<M>::R];
 };
 
 // Connected component of the live mask L containing r (frontier BFS, one
@@ -133,10 +222,11 @@ struct WLane {
 template <typename M>
 __device__ __forceinline__ M w_component(const WLane<M>& q, M L, int r) {
   M comp = wbit<M>(r), fr = comp;
-  while (fr) {
-    M c = 0;
-    if (whas(fr, q.v0)) c |= q.a0;
-    if (whas(fr, q.v1)) c |= q.a1;
+  while (nz(fr)) {
+    M c{};
+#pragma unroll
+    for (int j = 0; j < WT<M>::R; ++j)
+      if (whas(fr, q.v[j])) c |= q.a[j];
     fr = wor(c) & L & ~comp;
     comp |= fr;
   }
@@ -144,32 +234,37 @@ __device__ __forceinline__ M w_component(const WLane<M>& q, M L, int r) {
 }
 
 // Rules to a joint fixpoint on (L, S) under the bound `best` (pure.py:188
-// reduce_fixpoint: degree-one, degree-two triangle, high degree).  Leaves d0
-// / d1 = current degrees of the lane's vertices.  Returns the edge count,
-// or -1 when S reached the bound (prune).
-template <typename M>
-__device__ __forceinline__ int w_fixpoint(const WarpWs& ws, const WLane<M>& q, M& L, int& S,
-                                          int best, int& d0, int& d1, WStats& st) {
+// reduce_fixpoint: degree-one, degree-two triangle, high degree).  Leaves d
+// = current degrees of the lane's vertices.  Returns the edge count, or -1
+// when S reached the bound (prune).
+template <typename M, typename WS>
+__device__ __forceinline__ int w_fixpoint(const WS& ws, const WLane<M>& q, M& L, int& S,
+                                          int best, int (&d)[WT<M>::R], WStats& st) {
+  constexpr int R = WT<M>::R;
   while (true) {
     WPROF(++st.c_iter);
-    d0 = whas(L, q.v0) ? wpopc(q.a0 & L) : 0;
-    d1 = whas(L, q.v1) ? wpopc(q.a1 & L) : 0;
-    L = wballot<M>(d0 > 0, d1 > 0);  // isolated vertices leave the graph
-    const int k = best - S - 1;    // vertices an improving cover may still take
+    bool p[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      d[j] = whas(L, q.v[j]) ? wpopc(q.a[j] & L) : 0;
+      p[j] = d[j] > 0;
+    }
+    L = wballot<M>(p);  // isolated vertices leave the graph
+    const int k = best - S - 1;  // vertices an improving cover may still take
     if (k < 0) return -1;
     // degree one (pure.py:82): the neighbour of a pendant vertex is forced;
     // of an isolated edge only the higher end (the in-order sweep's choice)
-    const M p1 = wballot<M>(d0 == 1, d1 == 1);
-    if (p1) {
-      M c = 0;
-      if (d0 == 1) {
-        const int u = wlsb(q.a0 & L);
-        if (!(((p1 >> u) & 1) && u < q.v0)) c |= wbit<M>(u);
-      }
-      if (d1 == 1) {
-        const int u = wlsb(q.a1 & L);
-        if (!(((p1 >> u) & 1) && u < q.v1)) c |= wbit<M>(u);
-      }
+#pragma unroll
+    for (int j = 0; j < R; ++j) p[j] = d[j] == 1;
+    const M p1 = wballot<M>(p);
+    if (nz(p1)) {
+      M c{};
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        if (d[j] == 1) {
+          const int u = wlsb(q.a[j] & L);
+          if (!(whas(p1, u) && u < q.v[j])) c |= wbit<M>(u);
+        }
       const M F = wor(c);
       L &= ~F;
       S += wpopc(F);
@@ -178,51 +273,44 @@ __device__ __forceinline__ int w_fixpoint(const WarpWs& ws, const WLane<M>& q, M
     }
     // degree-two triangle (pure.py:113): in index order with revalidation.
     // Validity (the two neighbours adjacent) is decided by every lane for
-    // its own vertices, fetching the neighbour's row from its owner lane;
-    // the in-order walk then only visits valid candidates, and a later
+    // its own vertices from the neighbour's row in the workspace; the
+    // in-order walk then only visits valid candidates, and a later
     // candidate stays applicable iff it and its two neighbours are still
     // live (a removal only deletes vertices, so its degree cannot stay 2
     // otherwise).
     {
-      int ab0 = -1, ab1 = -1;
-      bool t0 = false, t1 = false;
-      {
-        const M n0 = q.a0 & L, n1 = q.a1 & L;
-        const int a0 = wlsb(n0), b0 = wmsb(n0);
-        const int a1 = wlsb(n1), b1 = wmsb(n1);
-        // row of a0 / a1 from their owner lanes (all lanes shuffle)
-        const M r0lo = __shfl_sync(0xffffffffu, q.a0, a0 & 31);
-        const M r0hi = __shfl_sync(0xffffffffu, q.a1, a0 & 31);
-        const M r1lo = __shfl_sync(0xffffffffu, q.a0, a1 & 31);
-        const M r1hi = __shfl_sync(0xffffffffu, q.a1, a1 & 31);
-        if (d0 == 2) {
-          const M ra = a0 < 32 ? r0lo : r0hi;
-          t0 = (ra >> b0) & 1;
-          ab0 = a0 | (b0 << 8);
-        }
-        if (d1 == 2) {
-          const M ra = a1 < 32 ? r1lo : r1hi;
-          t1 = (ra >> b1) & 1;
-          ab1 = a1 | (b1 << 8);
+      int ab[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        p[j] = false;
+        ab[j] = -1;
+        if (d[j] == 2) {
+          const M nb = q.a[j] & L;
+          const int x = wlsb(nb), y = wmsb(nb);
+          p[j] = whas(wload<M>(&ws.adj[WS::kW * x]), y);
+          ab[j] = x | (y << 8);
         }
       }
-      M T = wballot<M>(t0, t1);
-      if (T) {
-        M R = 0;  // vertices removed by this sweep
+      M T = wballot<M>(p);
+      if (nz(T)) {
+        M Rm{};  // vertices removed by this sweep
         int applied = 0;
-        while (T) {
+        while (nz(T)) {
           const int v = wlsb(T);
-          T &= T - 1;
-          const int ab = __shfl_sync(0xffffffffu, v < 32 ? ab0 : ab1, v & 31);
-          const M tri = wbit<M>(v) | wbit<M>(ab & 255) | wbit<M>(ab >> 8);
-          if (tri & R) continue;
-          R |= tri & ~wbit<M>(v);
-          R |= wbit<M>(v);  // v leaves too (isolated once its neighbours are in)
+          T = wclr(T);
+          int mine = ab[0];
+#pragma unroll
+          for (int j = 1; j < R; ++j)
+            if ((v >> 5) == j) mine = ab[j];
+          const int abv = __shfl_sync(0xffffffffu, mine, v & 31);
+          // v leaves too (isolated once its neighbours are in)
+          const M tri = wbit<M>(v) | wbit<M>(abv & 255) | wbit<M>(abv >> 8);
+          if (nz(tri & Rm)) continue;
+          Rm |= tri;
           ++applied;
         }
-        const M nb = R;  // includes the candidates themselves
         // cover gains exactly the two neighbours per applied triangle
-        L &= ~nb;
+        L &= ~Rm;
         S += 2 * applied;
         st.rules[1] += applied;
         continue;
@@ -230,8 +318,10 @@ __device__ __forceinline__ int w_fixpoint(const WarpWs& ws, const WLane<M>& q, M
     }
     // high degree (pure.py:158): a vertex of degree > k is in every cover
     // that still improves the bound
-    const M H = wballot<M>(d0 > k, d1 > k);
-    if (H) {
+#pragma unroll
+    for (int j = 0; j < R; ++j) p[j] = d[j] > k;
+    const M H = wballot<M>(p);
+    if (nz(H)) {
       L &= ~H;
       S += wpopc(H);
       st.rules[2] += wpopc(H);
@@ -239,13 +329,17 @@ __device__ __forceinline__ int w_fixpoint(const WarpWs& ws, const WLane<M>& q, M
     }
     break;
   }
-  return __reduce_add_sync(0xffffffffu, d0 + d1) >> 1;
+  int sum = 0;
+#pragma unroll
+  for (int j = 0; j < R; ++j) sum += d[j];
+  return __reduce_add_sync(0xffffffffu, sum) >> 1;
 }
 
-// Push (adjacency of this task, live mask L) as a new task on the same
-// scope with cover offset th.S + Sl.  false: ring full.
-__device__ inline bool warp_export(const SearchParams& P, const WarpWs& ws, const WTaskHdr& th,
-                                   int n, unsigned long long L, int Sl) {
+// Push (adjacency of this task, live mask L = two words at Lw) as a new task
+// on the same scope with cover offset th.S + Sl.  false: ring full.
+template <typename WS>
+__device__ inline bool warp_export(const SearchParams& P, const WS& ws, const WTaskHdr& th,
+                                   int n, const unsigned long long* Lw, int Sl) {
   const int lane = threadIdx.x & 31;
   long long pos = -1;
   if (lane == 0) pos = q_reserve_push(P.bq, P.bq.cap);
@@ -253,10 +347,11 @@ __device__ inline bool warp_export(const SearchParams& P, const WarpWs& ws, cons
   if (pos < 0) return false;
   char* slot = P.bq.data + (pos % P.bq.cap) * kWSlotBytes;
   unsigned long long* dst = (unsigned long long*)(slot + kWHdrBytes);
-  for (int i = lane; i < n; i += 32) __stcg(dst + i, ws.adj[i]);
+  const int W = wrows(n);
+  for (int i = lane; i < n * W; i += 32) __stcg(dst + i, ws.adj[WS::kW * (i / W) + i % W]);
   if (lane == 0) {
     __stcg((int4*)slot, make_int4(th.S + Sl, th.scope, n, th.depth + 1));
-    __stcg((unsigned long long*)(slot + 16), L);
+    __stcg((ulonglong2*)(slot + 16), make_ulonglong2(Lw[0], WS::kW > 1 ? Lw[1] : 0ull));
     atomicAdd(&P.reg.live[th.scope], 1);  // before the task can finish it
   }
   __syncwarp();
@@ -266,17 +361,19 @@ __device__ inline bool warp_export(const SearchParams& P, const WarpWs& ws, cons
 
 // Solve one task to completion (or until the stop flag).  All 32 lanes run
 // it with warp-uniform state; returns false when abandoned on stop.
-template <typename M>
-__device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const WTaskHdr th,
+template <typename M, typename WS>
+__device__ inline bool warp_solve_task(const SearchParams& P, WS& ws, const WTaskHdr th,
                                        WStats& st) {
+  constexpr int K = WS::kW;
+  constexpr int R = WT<M>::R;
   const int lane = threadIdx.x & 31;
   const int n = th.n & 0xffff;
-  constexpr bool kTwo = sizeof(M) == 8;
   WLane<M> q;
-  q.v0 = lane;
-  q.v1 = kTwo ? lane + 32 : 64;  // 64: never live (whas)
-  q.a0 = q.v0 < n ? (M)ws.adj[q.v0] : (M)0;
-  q.a1 = kTwo && q.v1 < n ? (M)ws.adj[q.v1] : (M)0;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    q.v[j] = lane + 32 * j;
+    q.a[j] = q.v[j] < n ? wload<M>(&ws.adj[K * q.v[j]]) : M{};
+  }
   bool skip_count = (th.n >> 16) & 1;
 
   int sb = 0;
@@ -287,7 +384,11 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
   ws.fr[0].base = 0;
   ws.fr[0].pend_b = ws.fr[0].pend_e = 0;
   int nf = 1, sp = 0;
-  M L = (M)th.live;
+  M L;
+  {
+    const unsigned long long lv[2] = {th.live, th.live_hi};
+    L = wload<M>(lv);
+  }
   int S = 0;
   bool have = ws.fr[0].best > 0;
   unsigned tick = 0;
@@ -297,7 +398,7 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
       const int f = nf - 1;
       if (sp > ws.fr[f].base) {
         --sp;
-        L = (M)ws.stL[sp];
+        L = wload<M>(&ws.stL[K * sp]);
         S = ws.stS[sp];
         have = true;
       } else if (f == 0) {
@@ -311,7 +412,7 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
         }
         F.running += F.best;
         if (F.pend_e > F.pend_b) {
-          const M c = (M)ws.pend[--F.pend_e];
+          const M c = wload<M>(&ws.pend[K * --F.pend_e]);
           const int bound = ws.fr[f - 1].best - F.running - (F.pend_e - F.pend_b);
           const int size = wpopc(c);
           if (bound <= 0) {
@@ -372,15 +473,15 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
       const int top0 = nf > 1 ? ws.fr[1].base : sp;
       if (__shfl_sync(0xffffffffu, shed, 0) && top0 > ws.fr[0].base) {
         const int b = ws.fr[0].base;
-        if (warp_export(P, ws, th, n, ws.stL[b], ws.stS[b])) ws.fr[0].base = b + 1;
+        if (warp_export(P, ws, th, n, &ws.stL[K * b], ws.stS[b])) ws.fr[0].base = b + 1;
       }
     }
     if (skip_count) skip_count = false;
     else ++st.nodes;
     WFrame& F = ws.fr[f];
-    int d0, d1;
+    int d[R];
     WPROF(long long c0 = clock64());
-    const int E = w_fixpoint(ws, q, L, S, F.best, d0, d1, st);
+    const int E = w_fixpoint(ws, q, L, S, F.best, d, st);
     WPROF(long long c1 = clock64(); st.c_fix += (unsigned long long)(c1 - c0));
     have = false;
     if (E < 0) continue;
@@ -410,20 +511,28 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
       while (true) {
         ++ncomp;
         const int size = wpopc(comp);
-        const bool in0 = whas(comp, q.v0), in1 = whas(comp, q.v1);
-        if (!wballot<M>(in0 && d0 != size - 1, in1 && d1 != size - 1)) {
+        bool p[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) p[j] = whas(comp, q.v[j]) && d[j] != size - 1;
+        bool cyc = false;
+        if (!nz(wballot<M>(p))) {
           special += size - 1;  // clique: all but one vertex
           st.rules[4] += 1;
-        } else if (size >= 3 && !wballot<M>(in0 && d0 != 2, in1 && d1 != 2)) {
-          special += (size + 1) / 2;  // chordless cycle
-          st.rules[5] += 1;
         } else {
-          if (pbase + ng < kWPend) ws.pend[pbase + ng] = comp;
-          else overflow = true;
-          ++ng;
+#pragma unroll
+          for (int j = 0; j < R; ++j) p[j] = whas(comp, q.v[j]) && d[j] != 2;
+          cyc = size >= 3 && !nz(wballot<M>(p));
+          if (cyc) {
+            special += (size + 1) / 2;  // chordless cycle
+            st.rules[5] += 1;
+          } else {
+            if (pbase + ng < kWPend) wstore<K>(&ws.pend[K * (pbase + ng)], comp);
+            else overflow = true;
+            ++ng;
+          }
         }
         rest &= ~comp;
-        if (!rest) break;
+        if (!nz(rest)) break;
         comp = w_component(q, rest, wlsb(rest));
       }
       if (lane == 0) atomicAdd(&P.hist[ncomp < P.n + 1 ? ncomp : P.n + 1], 1ull);
@@ -439,7 +548,7 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
       }
       if (base_S + ng >= F.best) continue;  // every general component needs >= 1
       if (ng == 1) {
-        L = (M)ws.pend[pbase];
+        L = wload<M>(&ws.pend[K * pbase]);
         S = base_S;
         have = true;
         continue;
@@ -453,11 +562,13 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
       }
       // new frame: solve pend[pbase] now, the rest afterwards (popped from
       // the end, so store them reversed to keep discovery order)
-      const M first = (M)ws.pend[pbase];
+      const M first = wload<M>(&ws.pend[K * pbase]);
       for (int i = 1, j = ng - 1; i < j; ++i, --j) {
-        const unsigned long long t = ws.pend[pbase + i];
-        ws.pend[pbase + i] = ws.pend[pbase + j];
-        ws.pend[pbase + j] = t;
+        for (int w = 0; w < K; ++w) {
+          const unsigned long long t = ws.pend[K * (pbase + i) + w];
+          ws.pend[K * (pbase + i) + w] = ws.pend[K * (pbase + j) + w];
+          ws.pend[K * (pbase + j) + w] = t;
+        }
       }
       WFrame& G = ws.fr[nf++];
       G.running = base_S;
@@ -480,23 +591,27 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
     }
     // ------------------------------------------------------- branch --
     // pure.py:241 select_max_degree (lowest index on ties)
-    unsigned k0 = d0 > 0 ? ((unsigned)d0 << 7) | (127u - q.v0) : 0u;
-    unsigned k1 = d1 > 0 ? ((unsigned)d1 << 7) | (127u - q.v1) : 0u;
-    const unsigned key = __reduce_max_sync(0xffffffffu, k0 > k1 ? k0 : k1);
+    unsigned kmax = 0u;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const unsigned kj = d[j] > 0 ? ((unsigned)d[j] << 7) | (127u - (unsigned)q.v[j]) : 0u;
+      kmax = kj > kmax ? kj : kmax;
+    }
+    const unsigned key = __reduce_max_sync(0xffffffffu, kmax);
     const int v = 127 - (int)(key & 127u);
-    const M nv = (M)ws.adj[v] & L;
+    const M nv = wload<M>(&ws.adj[K * v]) & L;
     // engine.py:319: exclude child (v out, N(v) in) to the stack, include
     // child (v in) continues here
     const int Sx = S + wpopc(nv);
     if (Sx < F.best) {
-      if (sp >= kWStack) {
+      if (sp >= WS::kStack) {
         if (lane == 0) {
           atomicExch(&P.ctl->error, 8);
           atomicExch(&P.ctl->stop, 1);
         }
         return false;
       }
-      ws.stL[sp] = L & ~(nv | wbit<M>(v));
+      wstore<K>(&ws.stL[K * sp], L & ~(nv | wbit<M>(v)));
       ws.stS[sp] = Sx;
       ++sp;
     }
@@ -512,9 +627,11 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WarpWs& ws, const 
 // the ring is empty and no warp of its block is still busy (new tasks can
 // only come from busy blocks), or as soon as node-level work is queued (the
 // block is needed there), or on stop.  Returns whether the block ran a task.
-__device__ inline bool warp_epoch(const SearchParams& P, WarpWs* wws, int* busy, WStats& st) {
+template <int WW>
+__device__ inline bool warp_epoch(const SearchParams& P, void* wws_raw, int* busy, WStats& st) {
+  using WS = WarpWsT<WW>;
   const int lane = threadIdx.x & 31;
-  WarpWs& ws = wws[threadIdx.x >> 5];
+  WS& ws = ((WS*)wws_raw)[threadIdx.x >> 5];
   bool any = false;
   unsigned backoff = 64;
   while (true) {
@@ -546,17 +663,26 @@ __device__ inline bool warp_epoch(const SearchParams& P, WarpWs* wws, int* busy,
     any = true;
     const char* slot = P.bq.data + (pos % P.bq.cap) * kWSlotBytes;
     const int4 h = __ldcg((const int4*)slot);
-    const WTaskHdr th{h.x, h.y, h.z, h.w, __ldcg((const unsigned long long*)(slot + 16)), 0ull};
+    const ulonglong2 lv = __ldcg((const ulonglong2*)(slot + 16));
+    const WTaskHdr th{h.x, h.y, h.z, h.w, lv.x, lv.y};
     const int n = th.n & 0xffff;
     const unsigned long long* src = (const unsigned long long*)(slot + kWHdrBytes);
-    for (int i = lane; i < n; i += 32) ws.adj[i] = __ldcg(src + i);
+    if (wrows(n) == WW) {
+      for (int i = lane; i < WW * n; i += 32) ws.adj[i] = __ldcg(src + i);
+    } else {  // a 64-vertex task in the 128-vertex layout
+      for (int i = lane; i < n; i += 32) {
+        ws.adj[WW * i] = __ldcg(src + i);
+        ws.adj[WW * i + 1] = 0ull;
+      }
+    }
     __syncwarp();
     if (lane == 0) q_release_pop(P.bq, pos);
     const long long t0 = clock64();
     const unsigned long long nodes0 = st.nodes;
     if (lane == 0) atomicMin(&P.ctl->t_task_first, globaltimer());
     if (n <= 32) warp_solve_task<unsigned>(P, ws, th, st);
-    else warp_solve_task<unsigned long long>(P, ws, th, st);
+    else if (n <= 64 || WW == 1) warp_solve_task<unsigned long long>(P, ws, th, st);
+    else warp_solve_task<W128>(P, ws, th, st);
     __syncwarp();
     if (lane == 0) {
       reg_finish(P, th.scope);  // the task's live unit on its scope

@@ -56,10 +56,11 @@ class SolverConfig:
     worklist_threshold: int | None = None
     threads: int = 0  # block size; 0 = chosen from the reduced graph size
     check_registry: bool = False
-    # warp tier: subproblems with <= warp_limit live vertices (max 64) are
-    # solved by one warp each as bitmask tasks; 0 = off.  Parallel mode only
+    # warp tier: subproblems with <= warp_limit live vertices (max 128) are
+    # solved by one warp each as bitmask tasks; 0 = off, -1 = auto (128 on
+    # dense reduced graphs, 64 on sparse ones).  Parallel mode only
     # (deterministic / record_cover runs keep the reference's node schedule).
-    warp_limit: int = 64
+    warp_limit: int = -1
     # concurrent searches sharing the GPU (solve_batch sets it): each takes
     # 1/gpu_share of the resident block slots
     gpu_share: int = 1
@@ -77,8 +78,8 @@ class SolverConfig:
             raise ValueError("timeout must be positive")
         if self.worklist_threshold is not None and self.worklist_threshold < 1:
             raise ValueError("worklist threshold must be >= 1")
-        if not 0 <= self.warp_limit <= 64:
-            raise ValueError("warp_limit must be in [0, 64]")
+        if not -1 <= self.warp_limit <= 128:
+            raise ValueError("warp_limit must be in [-1, 128]")
         if self.gpu_share < 1:
             raise ValueError("gpu_share must be >= 1")
 

@@ -50,9 +50,9 @@ def test_product_never_imports_oracle():
 def test_warp_limit_validation():
     import paper_2512_18334_b200 as vc
 
-    vc.SolverConfig(warp_limit=0).validate()
-    vc.SolverConfig(warp_limit=64).validate()
-    for bad in (-1, 65):
+    for ok in (-1, 0, 64, 128):
+        vc.SolverConfig(warp_limit=ok).validate()
+    for bad in (-2, 129):
         with pytest.raises(ValueError):
             vc.SolverConfig(warp_limit=bad).validate()
 
