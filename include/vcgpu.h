@@ -152,8 +152,8 @@ typedef struct {
                                  produced by vcg_expand; covers are counted from it */
   int warp_limit;             /* warp tier: subproblems with <= warp_limit (<= 128) live
                                  vertices are solved by one warp as bitmask tasks;
-                                 0 = off, < 0 = auto (128 when the graph's average
-                                 degree is >= 8, else 64).  Ignored (off) in
+                                 0 = off, < 0 = auto (128 when the graph has <= 256
+                                 vertices of average degree >= 8, else 64).  Ignored (off) in
                                  deterministic, record-cover, no-components and
                                  no-pruning runs. */
   int gpu_share;              /* concurrent searches sharing the device (>= 1): each

@@ -1436,12 +1436,15 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   const long long smem_limit = (long long)smem_optin - 8192;  // static smem headroom
   const int smem_fits = wsb <= smem_limit && !getenv("VCG_WS_GLOBAL");
   const long long csrb = csr_smem_bytes(n, g->m2);
-  // warp tier limit; < 0 = auto: 128-vertex tasks on dense reduced graphs
-  // (average degree >= 8: G(180, 0.08) 7.7 s -> 1.05 s), 64 on sparse ones,
-  // whose component splits already fit 64 and whose long 128-vertex tasks
-  // would serialise (rgg2000 PVC 1.2 -> 8.9 ms)
+  // warp tier limit; < 0 = auto: 128-vertex tasks on small dense reduced
+  // graphs (average degree >= 8, n <= 256: G(180, 0.08) 7.7 s -> 0.9 s),
+  // 64 otherwise -- sparse graphs' component splits already fit 64 and
+  // their long 128-vertex tasks would serialise (rgg2000 PVC 1.2 -> 8.9 ms),
+  // and on larger dense graphs the search rarely gets down to 128 live
+  // vertices while the 128-bit workspaces halve the resident blocks
+  // (G(400, 0.1): 15.6 -> 8.7 M nodes/s)
   int warp_limit0 = cfg->warp_limit;
-  if (warp_limit0 < 0) warp_limit0 = g->m2 >= 8LL * g->n ? kWMax : 64;
+  if (warp_limit0 < 0) warp_limit0 = g->m2 >= 8LL * g->n && g->n <= 2 * kWMax ? kWMax : 64;
   warp_limit0 = std::min(warp_limit0, kWMax);
   if (cfg->deterministic || cfg->record_cover || !cfg->use_components || cfg->disable_pruning ||
       !cfg->load_balance)

@@ -58,7 +58,7 @@ class SolverConfig:
     check_registry: bool = False
     # warp tier: subproblems with <= warp_limit live vertices (max 128) are
     # solved by one warp each as bitmask tasks; 0 = off, -1 = auto (128 on
-    # dense reduced graphs, 64 on sparse ones).  Parallel mode only
+    # small dense reduced graphs, else 64).  Parallel mode only
     # (deterministic / record_cover runs keep the reference's node schedule).
     warp_limit: int = -1
     # concurrent searches sharing the GPU (solve_batch sets it): each takes
