@@ -237,6 +237,21 @@ def load_capture():
         return {}, None
 
 
+def atomic_frac(cap):
+    """L2 atomic requests/s of the captured launch against the measured L2
+    atomic peak (profiles/r02_l2_atomic_peak.json: distinct-address ATOM,
+    tools/l2_atomic_peak.cu on this pool's B200)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_l2_atomic_peak.json")) as f:
+            peak = json.load(f)["ATOM distinct"]["G_atomics_per_s"] * 1e9
+    except (OSError, ValueError, KeyError):
+        return None
+    rate = cap.get("l2_atomic_requests_per_s") if cap else None
+    return {"achieved_per_s": rate, "peak_per_s": peak,
+            "frac": rate / peak if rate else None,
+            "peak_source": "profiles/r02_l2_atomic_peak.json (ATOM, distinct addresses)"}
+
+
 def other_configs(vc, torch, reps=5):
     """configs[0]-[2] through the public API, device-timed with CUDA events."""
     synth = load_synth()
@@ -498,6 +513,7 @@ def run_b200(args):
             "kernel_share_of_step": kern_ms / total_ms if total_ms else None,
             # what binds it: sequential sweeps (the reference's sweep order)
             # separated by grid barriers, each a few L2 round trips deep
+            "l2_atomic_frac": atomic_frac(cap),
             "l2_from_capture": {k: cap.get(k) for k in (
                 "l2_bytes", "l2_gbs", "l2_sector_throughput_pct_of_peak", "l2_atomic_requests",
                 "l2_atomic_requests_per_s", "l2_atomic_unit_active_pct_of_peak",

@@ -209,6 +209,8 @@ typedef struct {
   int64_t trace[8];           /* ns after the search kernel started: last node-level
                                  step, first warp task start, last warp task end;
                                  then tree nodes and vertices of the longest warp task */
+  int64_t kernel_t0_ns;       /* device %globaltimer when the search kernel started and */
+  int64_t kernel_t1_ns;       /* when its drain finished (a timeline of concurrent solves) */
 } vcg_search_result;
 
 /* In-flight exchange between one running search and the rest of a

@@ -69,6 +69,7 @@ class SearchResult_t(C.Structure):
         ("fix_cycles", I64 * 4), ("fix_count", I64 * 4),
         ("warp_tasks", I64), ("warp_nodes", I64), ("warp_cycles", I64), ("warp_limit", C.c_int),
         ("warp_epoch_cycles", I64), ("warp_task_max_cycles", I64), ("trace", I64 * 8),
+        ("kernel_t0_ns", I64), ("kernel_t1_ns", I64),
     ]
 
 

@@ -1792,6 +1792,8 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   res->trace[5] = (int64_t)ctl.wc_fix;
   res->trace[6] = (int64_t)ctl.wc_comp;
   res->trace[7] = (int64_t)ctl.wc_split;
+  res->kernel_t0_ns = (int64_t)ctl.t0;
+  res->kernel_t1_ns = (int64_t)ctl.t_end;
 
   for (int i = 0; i < 4; ++i) {
     res->fix_cycles[i] = (int64_t)ctl.rcyc[i];

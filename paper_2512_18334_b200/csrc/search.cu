@@ -917,6 +917,7 @@ __global__ void __launch_bounds__(VCG_SEARCH_MAXT, VCG_SEARCH_MINB) search_kerne
 // (engine.py:216), then publish the result words for one readback
 __global__ void drain_kernel(SearchParams P) {
   if (threadIdx.x != 0) return;
+  P.ctl->t_end = globaltimer();
   while (true) {
     long long pos = q_reserve_pop(P.q);
     if (pos < 0) break;

@@ -120,6 +120,7 @@ struct Ctl {
   // %globaltimer trace (ns): search start, last node-level step, first warp
   // task start, last warp task end
   unsigned long long t0, t_node_last, t_task_first, t_task_last;
+  unsigned long long t_end;  // %globaltimer when the drain kernel published the result
   unsigned long long wc_fix, wc_comp, wc_split;  // warp-task cycles: fixpoint, component test, splits
   unsigned long long wc_iter;                    // warp fixpoint loop iterations
 };

@@ -229,6 +229,7 @@ class SolveResult:
     threads: int = 0        # and threads per block
     phase_cycles: dict = field(default_factory=dict)  # block time by phase (SM cycles)
     root_kernel: dict = field(default_factory=dict)   # root rule kernels (Preprocessed.kernel)
+    kernel_interval_ns: tuple = (0, 0)  # device %globaltimer: search kernel start, drain end
 
     @property
     def forced(self) -> list[int]:
@@ -410,6 +411,7 @@ def _solve(g: StaticGraph, cfg: SolverConfig, lazy: bool):
                                      record=cfg.record_cover)
     stats.phase_seconds["search"] = time.perf_counter() - t1
     result.search_ms = float(res.kernel_ms)
+    result.kernel_interval_ns = (int(res.kernel_t0_ns), int(res.kernel_t1_ns))
     result.blocks = int(res.workers)
     result.threads = int(res.threads)
     result.phase_cycles = dict(zip(_lib.PHASES, (int(x) for x in res.phase_cycles)))
