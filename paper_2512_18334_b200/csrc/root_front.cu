@@ -27,10 +27,11 @@
 // Latency, not bandwidth, bounds a sweep (a few thousand frontier entries on
 // the 100k-vertex config), so every step is shaped for short dependent
 // chains spread over the whole grid:
-//  * every vertex keeps the sum and the sum of squares of its live
-//    neighbours' ids: a degree-1 vertex's neighbour is the sum, a degree-2
-//    vertex's two neighbours solve a + b = S1, a^2 + b^2 = S2 -- one load
-//    instead of a walk over a mostly dead adjacency;
+//  * every vertex with a long adjacency (> kTrack) keeps the sum and the sum
+//    of squares of its live neighbours' ids: a degree-1 vertex's neighbour
+//    is the sum, a degree-2 vertex's two neighbours solve a + b = S1,
+//    a^2 + b^2 = S2 -- one load instead of a walk over a mostly dead
+//    adjacency; short adjacencies are read whole (all loads in flight);
 //  * removals are split into chunks of kChunk adjacency entries, one thread
 //    per chunk, loads of a chunk issued before its atomics;
 //  * a grid barrier that polls with volatile loads and __nanosleep (the
@@ -56,6 +57,7 @@ namespace {
 
 constexpr int kSolo = 0;     // default: frontier size below which block 0 sweeps alone
 constexpr int kChunk = 8;    // adjacency entries per removal work item
+constexpr int kTrack = 12;   // adjacencies longer than this keep live-neighbour id sums
 
 enum Phase { F_D1 = 0, F_TRI = 1, F_HD = 2, F_DONE = 3 };
 
@@ -86,6 +88,7 @@ struct Front {  // device arrays (root_front_bytes)
   int *rem, *cand;
   int2* chunk;                      // removal work items (vertex, first entry)
   uint8_t* forced;
+  uint8_t* trk;                     // adjacency longer than kTrack: sums maintained
 };
 
 // Grid barrier.  cooperative_groups' grid.sync() polls with acquire loads,
@@ -205,6 +208,27 @@ __device__ __forceinline__ void cflush(BlockQ* q, int2* list, int* cnt) {
   if (threadIdx.x == 0) q->ccnt = q->cused = 0;
 }
 
+// the first two live neighbours of an untracked vertex (adjacency <= kTrack):
+// all its entries and their degrees loaded at once, two dependent round trips
+__device__ __forceinline__ void live_short(const Front& F, const int* off, const int* nbr, int v,
+                                           int* a, int* b) {
+  const int s0 = off[v], len = off[v + 1] - s0;
+  int x[kTrack], d[kTrack];
+#pragma unroll
+  for (int j = 0; j < kTrack; ++j) x[j] = j < len ? __ldg(nbr + s0 + j) : -1;
+#pragma unroll
+  for (int j = 0; j < kTrack; ++j) d[j] = x[j] >= 0 ? dget(F.deg, x[j]) : 0;
+  int u = -1, w = -1;
+#pragma unroll
+  for (int j = 0; j < kTrack; ++j)
+    if (d[j] > 0) {
+      if (u < 0) u = x[j];
+      else if (w < 0) w = x[j];
+    }
+  *a = u;
+  *b = w;
+}
+
 // one removal work item: the entries [b, min(b + kChunk, end(u))) of removed
 // vertex u.  Non-member live neighbours lose a degree and u from their sums;
 // 2 -> 1 and 3 -> 2 transitions are pushed to the pending lists.
@@ -222,10 +246,11 @@ __device__ __forceinline__ void rm_chunk(const Front& F, FrontCtl* G, BlockQ* q,
     if (x[j] >= 0) {
       const int r = __ldcg(F.rs + x[j]);
       const int d = dget(F.deg, x[j]);
+      const int tr = __ldg(F.trk + x[j]);
       if (r == s) {
         if (x[j] > u) ++*edges;  // both ends removed together: counted once
       } else if (d > 0) {
-        live[j] = 1;
+        live[j] = 1 + tr;
       }
     }
   }
@@ -236,8 +261,10 @@ __device__ __forceinline__ void rm_chunk(const Front& F, FrontCtl* G, BlockQ* q,
     old[j] = 0;
     if (live[j]) {
       old[j] = atomicSub(F.deg + x[j], 1u);
-      atomicAdd(F.nsum + x[j], 0ull - uu);
-      atomicAdd(F.nsq + x[j], 0ull - uu * uu);
+      if (live[j] > 1) {  // tracked neighbour: u leaves its sums
+        atomicAdd(F.nsum + x[j], 0ull - uu);
+        atomicAdd(F.nsq + x[j], 0ull - uu * uu);
+      }
       ++*edges;
     }
   }
@@ -267,8 +294,8 @@ __device__ __forceinline__ void remove_set(const Ex& E, const Front& F, FrontCtl
   qflush(q, F.l1[p1], &G->cnt1[p1], F.l2[p2], &G->cnt2[p2]);
 }
 
-// live-neighbour sums of every live vertex (thread per vertex, a warp for
-// adjacencies longer than 32)
+// live-neighbour sums of every tracked live vertex (thread per vertex, a
+// warp for adjacencies longer than 32)
 __device__ __forceinline__ void init_sums(const Front& F, const int* off, const int* nbr, int n,
                                           bool all_live) {
   const int lane = threadIdx.x & 31;
@@ -276,7 +303,7 @@ __device__ __forceinline__ void init_sums(const Front& F, const int* off, const 
   for (int base = gt - lane; base < n; base += T) {
     const int v = base + lane;
     bool lng = false;
-    if (v < n && dget(F.deg, v) > 0) {
+    if (v < n && F.trk[v] && dget(F.deg, v) > 0) {
       const int b = off[v], e = off[v + 1];
       if (e - b <= 32) {
         unsigned long long s1 = 0, s2 = 0;
@@ -365,7 +392,9 @@ __device__ __forceinline__ void sweep_d1(const Ex& E, const Front& F, FrontCtl* 
       L[k] = -1;
       continue;
     }
-    const int u = (int)__ldcg(F.nsum + v);
+    int u, u2;
+    if (__ldg(F.trk + v)) u = (int)__ldcg(F.nsum + v);
+    else live_short(F, off, nbr, v, &u, &u2);
     if (u < 0 || dget(F.deg, u) <= 0) {  // inconsistent degree array: report, never loop
       atomicExch(&G->err, 1);
       L[k] = -1;
@@ -451,7 +480,8 @@ __device__ __forceinline__ void sweep_tri(const Ex& E, const Front& F, FrontCtl*
     const int v = L[k];
     if (dget(F.deg, v) != 2) continue;
     int a, b;
-    two_from_sums(F, v, &a, &b);
+    if (__ldg(F.trk + v)) two_from_sums(F, v, &a, &b);
+    else live_short(F, off, nbr, v, &a, &b);
     if (a < 0 || a >= b || dget(F.deg, a) <= 0 || dget(F.deg, b) <= 0) {
       atomicExch(&G->err, 1);
       continue;
@@ -624,7 +654,8 @@ __global__ void __launch_bounds__(kRootGridThreads, 1)
     F.rem = ip + 8 * nn;
     F.cand = ip + 9 * nn;
     F.forced = (uint8_t*)(ip + 10 * nn);
-    F.chunk = (int2*)(F.forced + nn);
+    F.trk = F.forced + nn;
+    F.chunk = (int2*)(F.trk + nn);
   }
   int* hd_out = F.cand;  // the high-degree sweep's ids (cand is free outside triangle sweeps)
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, T = gridDim.x * blockDim.x;
@@ -636,6 +667,7 @@ __global__ void __launch_bounds__(kRootGridThreads, 1)
     F.key[v] = 0ull;
     F.rs[v] = 0;
     F.forced[v] = 0;
+    F.trk[v] = off[v + 1] - off[v] > kTrack;
     if (d == 1) qpush(&q, 0, F.l1[0], &G->cnt1[0], v);
     else if (d == 2) qpush(&q, 1, F.l2[0], &G->cnt2[0], v);
   }
@@ -789,9 +821,9 @@ size_t root_front_ctl_bytes() { return sizeof(FrontCtl); }
 
 size_t root_front_bytes(int n, long long m2) {
   const size_t nn = ((size_t)n + 31) & ~(size_t)31;
-  // key, nsum, nsq, 10 int arrays, forced, then the chunk list: every vertex
+  // key, nsum, nsq, 10 int arrays, forced, trk, then the chunk list: every vertex
   // is removed at most once, so a step's chunks number at most n + m2 / kChunk
-  return 24 * nn + 40 * nn + nn + 8 * ((size_t)n + (size_t)m2 / kChunk + 1) + 256;
+  return 24 * nn + 40 * nn + 2 * nn + 8 * ((size_t)n + (size_t)m2 / kChunk + 1) + 256;
 }
 
 int root_front_blocks() {
