@@ -26,7 +26,7 @@
 using namespace vcg;
 
 namespace vcg {
-template <typename T, bool kSmem>
+template <typename T, bool kSmem, int kWW>
 __global__ void search_kernel(SearchParams P);
 __global__ void drain_kernel(SearchParams P);
 __global__ void search_init_kernel(SearchParams P, int root_key, unsigned long long timeout_ns);
@@ -1444,7 +1444,10 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   // vertices while the 128-bit workspaces halve the resident blocks
   // (G(400, 0.1): 15.6 -> 8.7 M nodes/s)
   int warp_limit0 = cfg->warp_limit;
-  if (warp_limit0 < 0) warp_limit0 = g->m2 >= 8LL * g->n && g->n <= 2 * kWMax ? kWMax : 64;
+  if (warp_limit0 < 0) {
+    const bool dense = g->m2 >= 8LL * g->n;
+    warp_limit0 = dense && g->n <= 256 ? 128 : dense && g->n <= 640 ? 256 : 64;
+  }
   warp_limit0 = std::min(warp_limit0, kWMax);
   if (cfg->deterministic || cfg->record_cover || !cfg->use_components || cfg->disable_pruning ||
       !cfg->load_balance)
@@ -1457,8 +1460,16 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
     long long bws_off;
     size_t dsmem;
   };
+  // kernel variant: workspace placement x widest warp-task mask (64-bit words)
+  auto variant = [](int ws_smem, int wl) -> void (*)(SearchParams) {
+    const int ww = wl > 128 ? 4 : wl > 64 ? 2 : 1;
+    if (ws_smem)
+      return ww == 4 ? search_kernel<T, true, 4>
+             : ww == 2 ? search_kernel<T, true, 2> : search_kernel<T, true, 1>;
+    return ww == 4 ? search_kernel<T, false, 4>
+           : ww == 2 ? search_kernel<T, false, 2> : search_kernel<T, false, 1>;
+  };
   auto plan = [&](int th, int ws_smem, int csr, Plan* pl) -> int {
-    auto kern = ws_smem ? search_kernel<T, true> : search_kernel<T, false>;
     pl->threads = th;
     pl->in_smem = ws_smem;
     pl->csr_smem = ws_smem && csr;
@@ -1470,8 +1481,10 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
     pl->bws_alias = 0;
     pl->bws_off = 0;
     if (pl->warp_limit) {
-      const long long need = (long long)(th / 32) *
-                             (long long)(warp_limit0 > 64 ? sizeof(WarpWs2) : sizeof(WarpWs1));
+      const long long need =
+          (long long)(th / 32) * (long long)(warp_limit0 > 128  ? sizeof(WarpWs4)
+                                             : warp_limit0 > 64 ? sizeof(WarpWs2)
+                                                                : sizeof(WarpWs1));
       const long long ni = ((long long)std::max(n, 1) + 3) & ~3LL;
       if (ws_smem && 7 * ni * 4 >= need) {
         pl->bws_alias = 1;
@@ -1481,6 +1494,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
         else pl->warp_limit = 0;
       }
     }
+    auto kern = variant(ws_smem, pl->warp_limit);
     if (int r = raise_smem_limit((const void*)kern, pl->dsmem)) return r;
     pl->per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->per_sm, kern, th, pl->dsmem));
@@ -1510,7 +1524,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   }
   // the chosen plan is the kernel's final attribute setting
   if (int r = plan(pl.threads, pl.in_smem, pl.csr_smem, &pl)) return r;
-  auto kern = pl.in_smem ? search_kernel<T, true> : search_kernel<T, false>;
+  auto kern = variant(pl.in_smem, pl.warp_limit);
   const int in_smem = pl.in_smem;
   threads = pl.threads;
   const int csr_smem = pl.csr_smem;
@@ -1538,7 +1552,11 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   if (qcap * slot > q_budget) qcap = std::max(4096LL, q_budget / slot);
   const int reg_cap = (int)std::min<long long>(1LL << 23, std::max<long long>(1LL << 16, (long long)n * 1024));
 
-  const long long bcap = warp_limit ? std::max<long long>(65536, 64LL * blocks) : 16;
+  // warp-task ring: slots sized for the run's limit (576 B at 64 vertices,
+  // 8 KB at 256); fewer of the large ones
+  const long long bcap = !warp_limit ? 16
+                         : warp_limit > 128 ? std::max<long long>(16384, 16LL * blocks)
+                                            : std::max<long long>(65536, 64LL * blocks);
   // component subgraph arena: order-preserving compaction of split
   // components (not in record-cover mode, whose witnesses use reduced ids)
   const int compact = !cfg->record_cover && !getenv("VCG_NO_COMPACT");
@@ -1546,7 +1564,8 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   const long long arena_cap = compact ? std::min<long long>(
       (1LL << 28), std::max<long long>(1LL << 22, 64LL * ((long long)n + 1 + g->m2))) : 4;
   if (C.sg.ensure((size_t)sg_cap * 8 + 64) || C.arena.ensure((size_t)arena_cap * 4)) return VCG_ERESOURCE;
-  if (C.bseq.ensure((size_t)bcap * 8) || C.bdata.ensure((size_t)(bcap * kWSlotBytes)) ||
+  const long long bslot = wslot_bytes(std::max(warp_limit, 1));
+  if (C.bseq.ensure((size_t)bcap * 8) || C.bdata.ensure((size_t)(bcap * bslot)) ||
       C.bctl.ensure(64))
     return VCG_ERESOURCE;
   if (C.stacks.ensure((size_t)(stack_cap * slot * blocks)) || C.qseq.ensure((size_t)qcap * 8) ||
@@ -1636,6 +1655,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   P.bq.data = C.bdata.as<char>();
   P.bq.cap = bcap;
   P.warp_limit = warp_limit;
+  P.bq_slot = bslot;
   P.bq_low = std::max(8LL, (long long)blocks * (threads / 32) / 4);
   {
     const char* e1 = getenv("VCG_WCHECK");

@@ -171,6 +171,7 @@ struct SearchParams {
   int wcap;
   // warp tier (warp_solve.cuh): ring of bitmask tasks, per-warp workspaces
   Queue bq;
+  long long bq_slot;      // bytes per warp-task slot (warp_solve.cuh wslot_bytes)
   int warp_limit;         // 0 = off
   long long bq_low;       // a long warp task sheds work while the ring holds fewer
   int w_check_mask;       // a warp task polls stop / bound / ring every (mask + 1) nodes

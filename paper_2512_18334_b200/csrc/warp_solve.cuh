@@ -43,23 +43,26 @@ namespace vcg {
 #define WPROF(...)
 #endif
 
-constexpr int kWMax = 128;            // vertices per warp task
+constexpr int kWMax = 256;            // vertices per warp task
 constexpr int kWFrames = 24;          // nested component frames (each >= 6 vertices)
 constexpr int kWTierWarps = 8;        // warps of a block that runs the warp tier (<= 256 threads)
 constexpr int kWPend = 32;            // pending component masks over all frames
 
-// warp-task record: 32 B header + adjacency rows of n vertices, each row
-// wrows(n) 64-bit words (1 for n <= 64, 2 up to 128)
-struct WTaskHdr {
+// warp-task record: 32 B header, adjacency rows of n vertices (each row
+// wrows(n) 64-bit words: 1 for n <= 64, 2 up to 128, 4 up to 256), then
+// the live mask's words beyond the first two
+struct WTaskHdr {  // (the root's live mask follows at +16 / after the rows: WarpWsT::live0)
   int S;      // cover size of the task's root within its registry scope
   int scope;  // registry entry the task reports to (it holds one live unit)
   int n;      // vertices | (root already counted as a tree node) << 16
   int depth;
-  unsigned long long live, live_hi;  // live vertices of the task's root node (128 bits)
 };
 constexpr long long kWHdrBytes = 32;
-constexpr long long kWSlotBytes = kWHdrBytes + 16 * kWMax;
-__host__ __device__ __forceinline__ int wrows(int n) { return n > 64 ? 2 : 1; }
+__host__ __device__ __forceinline__ int wrows(int n) { return n > 128 ? 4 : n > 64 ? 2 : 1; }
+// bytes of a ring slot for tasks of up to `limit` vertices
+__host__ __device__ __forceinline__ long long wslot_bytes(int limit) {
+  return (kWHdrBytes + 8LL * wrows(limit) * limit + 16 + 15) & ~15LL;  // 16 B aligned
+}
 // a task polls every 4 nodes and may shed work after 4 (capi.cu; VCG_WCHECK /
 // VCG_WEXPORT override): on rgg2000 PVC(opt-1) 1.40 -> 1.28 ms vs every 16 / after 64
 
@@ -85,9 +88,11 @@ struct WarpWsT {
   unsigned long long pend[WW * kWPend];
   int stS[kStack];
   WFrame fr[kWFrames];
+  unsigned long long live0[WW];  // the task root's live mask
 };
 using WarpWs1 = WarpWsT<1>;
 using WarpWs2 = WarpWsT<2>;
+using WarpWs4 = WarpWsT<4>;
 
 struct WStats {
   unsigned long long tasks, nodes, splits, cyc, maxcyc, max_nodes, max_n;
@@ -113,14 +118,37 @@ __device__ __forceinline__ W128& operator|=(W128& a, W128 b) { a = a | b; return
 __device__ __forceinline__ bool operator==(W128 a, W128 b) { return a.lo == b.lo && a.hi == b.hi; }
 __device__ __forceinline__ bool operator!=(W128 a, W128 b) { return !(a == b); }
 
+struct W256 {
+  unsigned long long w[4];
+};
+__device__ __forceinline__ W256 operator&(const W256& a, const W256& b) {
+  return {{a.w[0] & b.w[0], a.w[1] & b.w[1], a.w[2] & b.w[2], a.w[3] & b.w[3]}};
+}
+__device__ __forceinline__ W256 operator|(const W256& a, const W256& b) {
+  return {{a.w[0] | b.w[0], a.w[1] | b.w[1], a.w[2] | b.w[2], a.w[3] | b.w[3]}};
+}
+__device__ __forceinline__ W256 operator~(const W256& a) {
+  return {{~a.w[0], ~a.w[1], ~a.w[2], ~a.w[3]}};
+}
+__device__ __forceinline__ W256& operator&=(W256& a, const W256& b) { a = a & b; return a; }
+__device__ __forceinline__ W256& operator|=(W256& a, const W256& b) { a = a | b; return a; }
+__device__ __forceinline__ bool operator==(const W256& a, const W256& b) {
+  return a.w[0] == b.w[0] && a.w[1] == b.w[1] && a.w[2] == b.w[2] && a.w[3] == b.w[3];
+}
+__device__ __forceinline__ bool operator!=(const W256& a, const W256& b) { return !(a == b); }
+
 template <typename M> struct WT;
 template <> struct WT<unsigned> { static constexpr int R = 1; };
 template <> struct WT<unsigned long long> { static constexpr int R = 2; };
 template <> struct WT<W128> { static constexpr int R = 4; };
+template <> struct WT<W256> { static constexpr int R = 8; };
 
 __device__ __forceinline__ bool nz(unsigned x) { return x != 0u; }
 __device__ __forceinline__ bool nz(unsigned long long x) { return x != 0ull; }
 __device__ __forceinline__ bool nz(W128 x) { return (x.lo | x.hi) != 0ull; }
+__device__ __forceinline__ bool nz(const W256& x) {
+  return (x.w[0] | x.w[1] | x.w[2] | x.w[3]) != 0ull;
+}
 
 __device__ __forceinline__ unsigned long long wor64(unsigned long long x) {
   const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)x);
@@ -130,23 +158,50 @@ __device__ __forceinline__ unsigned long long wor64(unsigned long long x) {
 __device__ __forceinline__ unsigned wor(unsigned x) { return __reduce_or_sync(0xffffffffu, x); }
 __device__ __forceinline__ unsigned long long wor(unsigned long long x) { return wor64(x); }
 __device__ __forceinline__ W128 wor(W128 x) { return {wor64(x.lo), wor64(x.hi)}; }
+__device__ __forceinline__ W256 wor(const W256& x) {
+  return {{wor64(x.w[0]), wor64(x.w[1]), wor64(x.w[2]), wor64(x.w[3])}};
+}
 __device__ __forceinline__ int wpopc(unsigned x) { return __popc(x); }
 __device__ __forceinline__ int wpopc(unsigned long long x) { return __popcll(x); }
 __device__ __forceinline__ int wpopc(W128 x) { return __popcll(x.lo) + __popcll(x.hi); }
+__device__ __forceinline__ int wpopc(const W256& x) {
+  return __popcll(x.w[0]) + __popcll(x.w[1]) + __popcll(x.w[2]) + __popcll(x.w[3]);
+}
 __device__ __forceinline__ int wlsb(unsigned x) { return __ffs((int)x) - 1; }
 __device__ __forceinline__ int wlsb(unsigned long long x) { return __ffsll((long long)x) - 1; }
 __device__ __forceinline__ int wlsb(W128 x) {
   return x.lo ? __ffsll((long long)x.lo) - 1 : (x.hi ? 63 + __ffsll((long long)x.hi) : -1);
+}
+__device__ __forceinline__ int wlsb(const W256& x) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (x.w[i]) return 64 * i + __ffsll((long long)x.w[i]) - 1;
+  return -1;
 }
 __device__ __forceinline__ int wmsb(unsigned x) { return 31 - __clz((int)x); }
 __device__ __forceinline__ int wmsb(unsigned long long x) { return 63 - __clzll((long long)x); }
 __device__ __forceinline__ int wmsb(W128 x) {
   return x.hi ? 127 - __clzll((long long)x.hi) : 63 - __clzll((long long)x.lo);
 }
+__device__ __forceinline__ int wmsb(const W256& x) {
+#pragma unroll
+  for (int i = 3; i >= 0; --i)
+    if (x.w[i]) return 64 * i + 63 - __clzll((long long)x.w[i]);
+  return -1;
+}
 __device__ __forceinline__ unsigned wclr(unsigned x) { return x & (x - 1u); }
 __device__ __forceinline__ unsigned long long wclr(unsigned long long x) { return x & (x - 1ull); }
 __device__ __forceinline__ W128 wclr(W128 x) {
   return x.lo ? W128{x.lo & (x.lo - 1ull), x.hi} : W128{0ull, x.hi & (x.hi - 1ull)};
+}
+__device__ __forceinline__ W256 wclr(W256 x) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (x.w[i]) {
+      x.w[i] &= x.w[i] - 1ull;
+      break;
+    }
+  return x;
 }
 template <typename M>
 __device__ __forceinline__ M wbit(int i);
@@ -158,11 +213,22 @@ template <>
 __device__ __forceinline__ W128 wbit<W128>(int i) {
   return i < 64 ? W128{1ull << i, 0ull} : W128{0ull, 1ull << (i - 64)};
 }
+template <>
+__device__ __forceinline__ W256 wbit<W256>(int i) {
+  const unsigned long long b = 1ull << (i & 63);
+  const int k = i >> 6;  // selects, not an indexed store (which would go to local memory)
+  return {{k == 0 ? b : 0ull, k == 1 ? b : 0ull, k == 2 ? b : 0ull, k == 3 ? b : 0ull}};
+}
 // vertex v live in L (v >= the mask width: never)
 __device__ __forceinline__ bool whas(unsigned L, int v) { return v < 32 && ((L >> v) & 1u); }
 __device__ __forceinline__ bool whas(unsigned long long L, int v) { return v < 64 && ((L >> v) & 1ull); }
 __device__ __forceinline__ bool whas(W128 L, int v) {
   return v < 64 ? ((L.lo >> v) & 1ull) : (v < 128 && ((L.hi >> (v - 64)) & 1ull));
+}
+__device__ __forceinline__ bool whas(const W256& L, int v) {
+  const int k = v >> 6;
+  const unsigned long long w = k == 0 ? L.w[0] : k == 1 ? L.w[1] : k == 2 ? L.w[2] : L.w[3];
+  return v < 256 && ((w >> (v & 63)) & 1ull);
 }
 // mask from per-lane predicates p[r] on the lane's r-th vertex
 template <typename M>
@@ -183,7 +249,16 @@ __device__ __forceinline__ W128 wballot<W128>(const bool (&p)[4]) {
           (unsigned long long)__ballot_sync(0xffffffffu, p[2]) |
               ((unsigned long long)__ballot_sync(0xffffffffu, p[3]) << 32)};
 }
-// masks in the workspace: two 64-bit words each
+template <>
+__device__ __forceinline__ W256 wballot<W256>(const bool (&p)[8]) {
+  W256 r;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    r.w[i] = (unsigned long long)__ballot_sync(0xffffffffu, p[2 * i]) |
+             ((unsigned long long)__ballot_sync(0xffffffffu, p[2 * i + 1]) << 32);
+  return r;
+}
+// masks in the workspace: WW 64-bit words each
 template <typename M>
 __device__ __forceinline__ M wload(const unsigned long long* p);
 template <>
@@ -194,27 +269,51 @@ __device__ __forceinline__ unsigned long long wload<unsigned long long>(const un
 }
 template <>
 __device__ __forceinline__ W128 wload<W128>(const unsigned long long* p) { return {p[0], p[1]}; }
+template <>
+__device__ __forceinline__ W256 wload<W256>(const unsigned long long* p) {
+  return {{p[0], p[1], p[2], p[3]}};
+}
 template <int WW>
 __device__ __forceinline__ void wstore(unsigned long long* p, unsigned x) {
   p[0] = x;
-  if (WW > 1) p[1] = 0ull;
+#pragma unroll
+  for (int i = 1; i < WW; ++i) p[i] = 0ull;
 }
 template <int WW>
 __device__ __forceinline__ void wstore(unsigned long long* p, unsigned long long x) {
   p[0] = x;
-  if (WW > 1) p[1] = 0ull;
+#pragma unroll
+  for (int i = 1; i < WW; ++i) p[i] = 0ull;
 }
 template <int WW>
 __device__ __forceinline__ void wstore(unsigned long long* p, W128 x) {
   p[0] = x.lo;
   if (WW > 1) p[1] = x.hi;
+  if (WW > 2) p[2] = p[3] = 0ull;
+}
+template <int WW>
+__device__ __forceinline__ void wstore(unsigned long long* p, const W256& x) {
+#pragma unroll
+  for (int i = 0; i < WW; ++i) p[i] = x.w[i];
 }
 
 // Per-lane view of the task graph: this lane owns vertices lane + 32 r.
+// Rows of up to 128-bit tasks are held in registers; the 256-bit tier's
+// eight 256-bit rows per lane stay in the workspace and are read on use.
 template <typename M>
 struct WLane {
   M a[WT<M>::R];    // adjacency rows of the lane's vertices (0 beyond n)
   int v[WT<M>::R];
+  __device__ __forceinline__ M row(int j) const { return a[j]; }
+};
+template <>
+struct WLane<W256> {
+  const unsigned long long* adj;  // the workspace rows, 4 words each
+  int n;
+  int v[8];
+  __device__ __forceinline__ W256 row(int j) const {
+    return v[j] < n ? wload<W256>(adj + 4 * v[j]) : W256{{0ull, 0ull, 0ull, 0ull}};
+  }
 };
 
 // Connected component of the live mask L containing r (frontier BFS, one
@@ -226,7 +325,7 @@ __device__ __forceinline__ M w_component(const WLane<M>& q, M L, int r) {
     M c{};
 #pragma unroll
     for (int j = 0; j < WT<M>::R; ++j)
-      if (whas(fr, q.v[j])) c |= q.a[j];
+      if (whas(fr, q.v[j])) c |= q.row(j);
     fr = wor(c) & L & ~comp;
     comp |= fr;
   }
@@ -246,7 +345,7 @@ __device__ __forceinline__ int w_fixpoint(const WS& ws, const WLane<M>& q, M& L,
     bool p[R];
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-      d[j] = whas(L, q.v[j]) ? wpopc(q.a[j] & L) : 0;
+      d[j] = whas(L, q.v[j]) ? wpopc(q.row(j) & L) : 0;
       p[j] = d[j] > 0;
     }
     L = wballot<M>(p);  // isolated vertices leave the graph
@@ -262,7 +361,7 @@ __device__ __forceinline__ int w_fixpoint(const WS& ws, const WLane<M>& q, M& L,
 #pragma unroll
       for (int j = 0; j < R; ++j)
         if (d[j] == 1) {
-          const int u = wlsb(q.a[j] & L);
+          const int u = wlsb(q.row(j) & L);
           if (!(whas(p1, u) && u < q.v[j])) c |= wbit<M>(u);
         }
       const M F = wor(c);
@@ -285,7 +384,7 @@ __device__ __forceinline__ int w_fixpoint(const WS& ws, const WLane<M>& q, M& L,
         p[j] = false;
         ab[j] = -1;
         if (d[j] == 2) {
-          const M nb = q.a[j] & L;
+          const M nb = q.row(j) & L;
           const int x = wlsb(nb), y = wmsb(nb);
           p[j] = whas(wload<M>(&ws.adj[WS::kW * x]), y);
           ab[j] = x | (y << 8);
@@ -345,13 +444,14 @@ __device__ inline bool warp_export(const SearchParams& P, const WS& ws, const WT
   if (lane == 0) pos = q_reserve_push(P.bq, P.bq.cap);
   pos = __shfl_sync(0xffffffffu, pos, 0);
   if (pos < 0) return false;
-  char* slot = P.bq.data + (pos % P.bq.cap) * kWSlotBytes;
+  char* slot = P.bq.data + (pos % P.bq.cap) * P.bq_slot;
   unsigned long long* dst = (unsigned long long*)(slot + kWHdrBytes);
   const int W = wrows(n);
   for (int i = lane; i < n * W; i += 32) __stcg(dst + i, ws.adj[WS::kW * (i / W) + i % W]);
   if (lane == 0) {
     __stcg((int4*)slot, make_int4(th.S + Sl, th.scope, n, th.depth + 1));
     __stcg((ulonglong2*)(slot + 16), make_ulonglong2(Lw[0], WS::kW > 1 ? Lw[1] : 0ull));
+    if (W > 2) __stcg((ulonglong2*)(dst + n * W), make_ulonglong2(Lw[2], Lw[3]));
     atomicAdd(&P.reg.live[th.scope], 1);  // before the task can finish it
   }
   __syncwarp();
@@ -369,10 +469,17 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WS& ws, const WTas
   const int lane = threadIdx.x & 31;
   const int n = th.n & 0xffff;
   WLane<M> q;
+  if constexpr (R == 8) {
+    q.adj = ws.adj;
+    q.n = n;
 #pragma unroll
-  for (int j = 0; j < R; ++j) {
-    q.v[j] = lane + 32 * j;
-    q.a[j] = q.v[j] < n ? wload<M>(&ws.adj[K * q.v[j]]) : M{};
+    for (int j = 0; j < R; ++j) q.v[j] = lane + 32 * j;
+  } else {
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      q.v[j] = lane + 32 * j;
+      q.a[j] = q.v[j] < n ? wload<M>(&ws.adj[K * q.v[j]]) : M{};
+    }
   }
   bool skip_count = (th.n >> 16) & 1;
 
@@ -384,11 +491,7 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WS& ws, const WTas
   ws.fr[0].base = 0;
   ws.fr[0].pend_b = ws.fr[0].pend_e = 0;
   int nf = 1, sp = 0;
-  M L;
-  {
-    const unsigned long long lv[2] = {th.live, th.live_hi};
-    L = wload<M>(lv);
-  }
+  M L = wload<M>(ws.live0);
   int S = 0;
   bool have = ws.fr[0].best > 0;
   unsigned tick = 0;
@@ -594,11 +697,11 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WS& ws, const WTas
     unsigned kmax = 0u;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-      const unsigned kj = d[j] > 0 ? ((unsigned)d[j] << 7) | (127u - (unsigned)q.v[j]) : 0u;
+      const unsigned kj = d[j] > 0 ? ((unsigned)d[j] << 8) | (255u - (unsigned)q.v[j]) : 0u;
       kmax = kj > kmax ? kj : kmax;
     }
     const unsigned key = __reduce_max_sync(0xffffffffu, kmax);
-    const int v = 127 - (int)(key & 127u);
+    const int v = 255 - (int)(key & 255u);
     const M nv = wload<M>(&ws.adj[K * v]) & L;
     // engine.py:319: exclude child (v out, N(v) in) to the stack, include
     // child (v in) continues here
@@ -661,18 +764,28 @@ __device__ inline bool warp_epoch(const SearchParams& P, void* wws_raw, int* bus
     }
     backoff = 64;
     any = true;
-    const char* slot = P.bq.data + (pos % P.bq.cap) * kWSlotBytes;
+    const char* slot = P.bq.data + (pos % P.bq.cap) * P.bq_slot;
     const int4 h = __ldcg((const int4*)slot);
     const ulonglong2 lv = __ldcg((const ulonglong2*)(slot + 16));
-    const WTaskHdr th{h.x, h.y, h.z, h.w, lv.x, lv.y};
+    const WTaskHdr th{h.x, h.y, h.z, h.w};
     const int n = th.n & 0xffff;
+    const int W = wrows(n);
     const unsigned long long* src = (const unsigned long long*)(slot + kWHdrBytes);
-    if (wrows(n) == WW) {
+    if (lane == 0) {
+      ws.live0[0] = lv.x;
+      if (WW > 1) ws.live0[1] = W > 1 ? lv.y : 0ull;
+      if (WW > 2) {
+        const ulonglong2 t = W > 2 ? __ldcg((const ulonglong2*)(src + n * W)) : ulonglong2{0ull, 0ull};
+        ws.live0[2] = t.x;
+        ws.live0[3] = t.y;
+      }
+    }
+    if (W == WW) {
       for (int i = lane; i < WW * n; i += 32) ws.adj[i] = __ldcg(src + i);
-    } else {  // a 64-vertex task in the 128-vertex layout
-      for (int i = lane; i < n; i += 32) {
-        ws.adj[WW * i] = __ldcg(src + i);
-        ws.adj[WW * i + 1] = 0ull;
+    } else {  // a narrower task in a wider layout: zero-extend its rows
+      for (int i = lane; i < WW * n; i += 32) {
+        const int r = i / WW, w = i % WW;
+        ws.adj[i] = w < W ? __ldcg(src + r * W + w) : 0ull;
       }
     }
     __syncwarp();
@@ -682,7 +795,8 @@ __device__ inline bool warp_epoch(const SearchParams& P, void* wws_raw, int* bus
     if (lane == 0) atomicMin(&P.ctl->t_task_first, globaltimer());
     if (n <= 32) warp_solve_task<unsigned>(P, ws, th, st);
     else if (n <= 64 || WW == 1) warp_solve_task<unsigned long long>(P, ws, th, st);
-    else warp_solve_task<W128>(P, ws, th, st);
+    else if (n <= 128 || WW == 2) warp_solve_task<W128>(P, ws, th, st);
+    else warp_solve_task<W256>(P, ws, th, st);
     __syncwarp();
     if (lane == 0) {
       reg_finish(P, th.scope);  // the task's live unit on its scope
@@ -727,7 +841,7 @@ __device__ inline void warp_ring_drain(const SearchParams& P) {
   while (true) {
     const long long pos = q_reserve_pop(P.bq);
     if (pos < 0) break;
-    const int scope = __ldcg((const int*)(P.bq.data + (pos % P.bq.cap) * kWSlotBytes) + 1);
+    const int scope = __ldcg((const int*)(P.bq.data + (pos % P.bq.cap) * P.bq_slot) + 1);
     q_release_pop(P.bq, pos);
     reg_finish(P, scope);
   }

@@ -56,7 +56,7 @@ class SolverConfig:
     worklist_threshold: int | None = None
     threads: int = 0  # block size; 0 = chosen from the reduced graph size
     check_registry: bool = False
-    # warp tier: subproblems with <= warp_limit live vertices (max 128) are
+    # warp tier: subproblems with <= warp_limit live vertices (max 256) are
     # solved by one warp each as bitmask tasks; 0 = off, -1 = auto (128 on
     # small dense reduced graphs, else 64).  Parallel mode only
     # (deterministic / record_cover runs keep the reference's node schedule).
@@ -78,8 +78,8 @@ class SolverConfig:
             raise ValueError("timeout must be positive")
         if self.worklist_threshold is not None and self.worklist_threshold < 1:
             raise ValueError("worklist threshold must be >= 1")
-        if not -1 <= self.warp_limit <= 128:
-            raise ValueError("warp_limit must be in [-1, 128]")
+        if not -1 <= self.warp_limit <= 256:
+            raise ValueError("warp_limit must be in [-1, 256]")
         if self.gpu_share < 1:
             raise ValueError("gpu_share must be >= 1")
 

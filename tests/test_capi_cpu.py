@@ -50,9 +50,9 @@ def test_product_never_imports_oracle():
 def test_warp_limit_validation():
     import paper_2512_18334_b200 as vc
 
-    for ok in (-1, 0, 64, 128):
+    for ok in (-1, 0, 64, 128, 256):
         vc.SolverConfig(warp_limit=ok).validate()
-    for bad in (-2, 129):
+    for bad in (-2, 257):
         with pytest.raises(ValueError):
             vc.SolverConfig(warp_limit=bad).validate()
 

@@ -12,7 +12,7 @@ for name in sys.argv[1:] or ["gnp400", "torus60"]:
     n, off, nbr = synth.WORKLOADS[name]()
     g = vc.StaticGraph(n, off, nbr)
     vc.solve(g, vc.SolverConfig(timeout=0.2))
-    for wl in (64, 128, -1):
+    for wl in (64, 128, 256, -1):
         t = time.perf_counter()
         r = vc.solve(g, vc.SolverConfig(timeout=B, warp_limit=wl))
         dt = time.perf_counter() - t

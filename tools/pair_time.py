@@ -29,8 +29,12 @@ def timed(fn, reps=15):
 
 for k in (opt, opt - 1):
     timed(lambda: vc.solve(g, vc.SolverConfig(mode="pvc", k=k)), 3)
-    print(f"[{os.environ.get('VCG_NO_RECLAIM', 'reclaim')}] k={k}: "
-          f"{timed(lambda: vc.solve(g, vc.SolverConfig(mode='pvc', k=k))):.3f} ms", flush=True)
+    sm = []
+    t = timed(lambda: sm.append(vc.solve(g, vc.SolverConfig(mode='pvc', k=k))))
+    print(f"[{os.environ.get('VCG_NO_RECLAIM', 'reclaim')}] k={k}: {t:.3f} ms  search kernel "
+          f"{statistics.median(r.search_ms for r in sm):.3f} ms  root "
+          f"{statistics.median(r.stats.phase_seconds['root_reduce'] for r in sm)*1e3:.3f} ms "
+          f"nodes {statistics.median(r.stats.tree_nodes_visited for r in sm)}", flush=True)
 cfgs = [vc.SolverConfig(mode="pvc", k=opt), vc.SolverConfig(mode="pvc", k=opt - 1)]
 timed(lambda: vc.solve_batch(g, cfgs), 3)
 print(f"[{os.environ.get('VCG_NO_RECLAIM', 'reclaim')}] pair: {timed(lambda: vc.solve_batch(g, cfgs)):.3f} ms")
