@@ -293,6 +293,20 @@ def other_configs(vc, torch, reps=5):
         for _ in range(reps * 2):
             t, r = timed(lambda: vc.solve(g, vc.SolverConfig(mode="pvc", k=k)))
             single[k].append((t, r.stats.tree_nodes_visited))
+    for key, name, gen in (("configs[4] gnp400", "MVC G(n=400, p=0.1), 2 s budget",
+                            lambda: synth.gnp(400, 0.1, 1)),
+                           ("configs[4] torus60", "MVC torus 60x60, 2 s budget",
+                            lambda: synth.torus(60, 60))):
+        n4, off4, nbr4 = gen()
+        g4 = vc.StaticGraph(n4, off4, nbr4)
+        vc.solve(g4, vc.SolverConfig(timeout=0.2))
+        t, r = timed(lambda: vc.solve(g4, vc.SolverConfig(timeout=2.0)))
+        out[key] = {"workload": name + " (beyond exact search on either side: nodes/s and the "
+                                      "best cover reached)",
+                    "best_cover": r.cover_size, "exact": r.exact,
+                    "tree_nodes": r.stats.tree_nodes_visited,
+                    "nodes_per_s": r.stats.tree_nodes_visited / (t * 1e-3),
+                    "warp_tier_share": r.warp_nodes / max(1, r.stats.tree_nodes_visited)}
     out["configs[1]"] = {
         "workload": "PVC yes/no pair (k=opt, opt-1) on random geometric graph n=2000 r=0.027",
         "opt": opt,
