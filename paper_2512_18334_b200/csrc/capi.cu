@@ -1490,7 +1490,13 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
         pl->bws_alias = 1;
       } else {
         pl->bws_off = ((long long)pl->dsmem + 15) & ~15LL;
-        if (pl->bws_off + need <= smem_limit) pl->dsmem = (size_t)(pl->bws_off + need);
+        // the wide-tier variants carry more static shared memory (the task
+        // packing table): check against the variant's own headroom
+        cudaFuncAttributes fa{};
+        CK(cudaFuncGetAttributes(&fa, (const void*)variant(ws_smem, pl->warp_limit)));
+        const long long lim = std::min<long long>(smem_limit, (long long)smem_optin -
+                                                                  (long long)fa.sharedSizeBytes);
+        if (pl->bws_off + need <= lim) pl->dsmem = (size_t)(pl->bws_off + need);
         else pl->warp_limit = 0;
       }
     }
@@ -1656,6 +1662,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   P.bq.cap = bcap;
   P.warp_limit = warp_limit;
   P.bq_slot = bslot;
+  P.warp_split_export = !getenv("VCG_NO_WSPLIT");
   P.bq_low = std::max(8LL, (long long)blocks * (threads / 32) / 4);
   {
     const char* e1 = getenv("VCG_WCHECK");

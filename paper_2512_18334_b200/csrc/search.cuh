@@ -172,6 +172,7 @@ struct SearchParams {
   // warp tier (warp_solve.cuh): ring of bitmask tasks, per-warp workspaces
   Queue bq;
   long long bq_slot;      // bytes per warp-task slot (warp_solve.cuh wslot_bytes)
+  int warp_split_export;  // wide warp tasks hand frame-0 splits to the registry
   int warp_limit;         // 0 = off
   long long bq_low;       // a long warp task sheds work while the ring holds fewer
   int w_check_mask;       // a warp task polls stop / bound / ring every (mask + 1) nodes

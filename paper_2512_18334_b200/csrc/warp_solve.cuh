@@ -203,6 +203,25 @@ __device__ __forceinline__ W256 wclr(W256 x) {
     }
   return x;
 }
+// set bits of c below position u
+__device__ __forceinline__ int wrank(unsigned c, int u) { return __popc(c & ((1u << u) - 1u)); }
+__device__ __forceinline__ int wrank(unsigned long long c, int u) {
+  return __popcll(c & ((1ull << u) - 1ull));
+}
+__device__ __forceinline__ int wrank(W128 c, int u) {
+  return u < 64 ? __popcll(c.lo & ((1ull << u) - 1ull))
+                : __popcll(c.lo) + __popcll(c.hi & ((1ull << (u - 64)) - 1ull));
+}
+__device__ __forceinline__ int wrank(const W256& c, int u) {
+  int r = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int lo = 64 * i;
+    if (u >= lo + 64) r += __popcll(c.w[i]);
+    else if (u > lo) r += __popcll(c.w[i] & ((1ull << (u - lo)) - 1ull));
+  }
+  return r;
+}
 template <typename M>
 __device__ __forceinline__ M wbit(int i);
 template <>
@@ -459,6 +478,139 @@ __device__ inline bool warp_export(const SearchParams& P, const WS& ws, const WT
   return true;
 }
 
+// Write component c of the current task as a new task at ring ticket pos:
+// its vertices renumbered in increasing order (lowest-index tie-breaks are
+// unchanged), rows restricted to c and compacted, so a small component runs
+// on narrow masks.
+template <typename M, typename WS>
+__device__ inline void warp_emit_component(const SearchParams& P, const WS& ws, M c, int scope,
+                                           int depth, long long pos) {
+  const int lane = threadIdx.x & 31;
+  const int sz = wpopc(c);
+  const int Wn = wrows(sz);
+  char* slot = P.bq.data + (pos % P.bq.cap) * P.bq_slot;
+  unsigned long long* dst = (unsigned long long*)(slot + kWHdrBytes);
+  M rest = c;
+  for (int j = 0; nz(rest); ++j) {  // warp-uniform walk over c; lane j % 32 packs row j
+    const int v = wlsb(rest);
+    rest = wclr(rest);
+    if ((j & 31) != lane) continue;
+    M r = wload<M>(&ws.adj[WS::kW * v]) & c;
+    unsigned long long o0 = 0ull, o1 = 0ull, o2 = 0ull, o3 = 0ull;
+    while (nz(r)) {
+      const int b = wrank(c, wlsb(r));
+      r = wclr(r);
+      const unsigned long long bit = 1ull << (b & 63);
+      const int k = b >> 6;
+      o0 |= k == 0 ? bit : 0ull;
+      o1 |= k == 1 ? bit : 0ull;
+      o2 |= k == 2 ? bit : 0ull;
+      o3 |= k == 3 ? bit : 0ull;
+    }
+    __stcg(dst + Wn * j, o0);
+    if (Wn > 1) __stcg(dst + Wn * j + 1, o1);
+    if (Wn > 2) {
+      __stcg(dst + Wn * j + 2, o2);
+      __stcg(dst + Wn * j + 3, o3);
+    }
+  }
+  if (lane == 0) {
+    __stcg((int4*)slot, make_int4(0, scope, sz, depth));
+    unsigned long long lv[4];
+    for (int j = 0; j < 4; ++j) {
+      const int rr = sz - 64 * j;
+      lv[j] = rr >= 64 ? ~0ull : rr > 0 ? ((1ull << rr) - 1) : 0ull;
+    }
+    __stcg((ulonglong2*)(slot + 16), make_ulonglong2(lv[0], lv[1]));
+    if (Wn > 2) __stcg((ulonglong2*)(dst + sz * Wn), make_ulonglong2(lv[2], lv[3]));
+  }
+  __syncwarp();
+  if (lane == 0) q_publish_push(P.bq, pos);
+}
+
+// A frame-0 node of a wide task that splits into ng >= 2 general components
+// (staged at pend[pbase, pbase + ng)): hand them to the registry like a
+// block-level split (engine.py:334 _try_component_split, search_impl.cuh
+// try_split) -- a parent entry on the task's scope holding the node's cover
+// S_abs plus the folded special components, one child entry and one compacted
+// task per component -- instead of solving them one after another inside this
+// warp.  The components then run on any warp in parallel: a wide task's
+// subtree no longer serialises on the warp that started it.  false: no ring
+// room (the caller solves them in place as nested frames).
+template <typename M, typename WS>
+__device__ inline bool warp_registry_split(const SearchParams& P, WS& ws, const WTaskHdr& th,
+                                           int pbase, int ng, int S_abs, int special,
+                                           int best_abs) {
+  constexpr int K = WS::kW;
+  const int lane = threadIdx.x & 31;
+  const Registry& R = P.reg;
+  // each component may take at most this many vertices for the node to
+  // improve the scope's bound (the others need >= 1 each)
+  const int room = best_abs - S_abs - special - (ng - 1);
+  long long pos = -1;
+  int p = -1;
+  if (lane == 0) {
+    p = reg_alloc(R, 1 + ng);
+    if (p < 0) {
+      atomicExch(&P.ctl->error, 1);
+      atomicExch(&P.ctl->stop, 1);
+    } else {
+      pos = q_reserve_push_n(P.bq, ng, P.bq.cap);
+      if (pos < 0) {
+        R.nchild[p] = ng;  // the free list reads the group size from it
+        reg_free_group(R, p);
+        p = -2;
+      }
+    }
+  }
+  p = __shfl_sync(0xffffffffu, p, 0);
+  pos = __shfl_sync(0xffffffffu, pos, 0);
+  if (p == -2) return false;
+  if (p < 0) return true;  // registry exhausted: the search stops
+  if (lane == 0) {
+    atomicAdd(&R.live[th.scope], 1);  // the parent entry's reference on the scope
+    R.kind[p] = 1;
+    R.sum[p] = S_abs + special;
+    R.sum_ach[p] = 1;
+    R.init_sum[p] = S_abs;
+    R.folded[p] = special;
+    R.live[p] = 1 + ng;
+    R.link[p] = th.scope;
+    R.first_child[p] = p + 1;
+    R.nchild[p] = ng;
+    R.disc_done[p] = 0;
+    R.key[p] = 0;
+    R.child_folded[p] = 0;
+    for (int j = 0; j < ng; ++j) {
+      const int size = wpopc(wload<M>(&ws.pend[K * (pbase + j)]));
+      int init = room < size - 1 ? room : size - 1;
+      if (init < 1) init = 1;
+      const int c = p + 1 + j;
+      R.kind[c] = 0;
+      R.key[c] = init * 2 + (init == size - 1 ? 0 : 1);
+      R.live[c] = 1;
+      R.link[c] = p;
+      R.child_folded[c] = 0;
+      R.disc_done[c] = 0;
+    }
+    __threadfence();
+  }
+  __syncwarp();
+  for (int j = 0; j < ng; ++j) {
+    if (lane == 0) q_wait_free(P.bq, pos + j);
+    __syncwarp();
+    warp_emit_component<M, WS>(P, ws, wload<M>(&ws.pend[K * (pbase + j)]), p + 1 + j,
+                               th.depth + 1, pos + j);
+  }
+  if (lane == 0) {
+    __threadfence();
+    st_release(&R.disc_done[p], 1);
+    if (atomicSub(&R.live[p], 1) == 1) reg_cascade(P, p);
+  }
+  __syncwarp();
+  return true;
+}
+
 // Solve one task to completion (or until the stop flag).  All 32 lanes run
 // it with warp-uniform state; returns false when abandoned on stop.
 template <typename M, typename WS>
@@ -655,6 +807,11 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WS& ws, const WTas
         S = base_S;
         have = true;
         continue;
+      }
+      if constexpr (K > 1) {  // wide-task variants only
+        if (f == 0 && n > 64 && !overflow && P.warp_split_export &&
+            warp_registry_split<M, WS>(P, ws, th, pbase, ng, th.S + S, special, th.S + F.best))
+          continue;  // the components run as tasks of their own
       }
       if (overflow || nf >= kWFrames) {
         if (lane == 0) {

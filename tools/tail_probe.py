@@ -8,11 +8,12 @@ name = sys.argv[1] if len(sys.argv) > 1 else "rgg2000"
 n, off, nbr = synth.WORKLOADS[name]()
 g = vc.StaticGraph(n, off, nbr)
 opt = vc.solve(g, vc.SolverConfig()).cover_size
+wl = int(os.environ.get("WL", "-1"))
 for k in (opt, opt - 1):
     for rep in range(3):
-        r = vc.solve(g, vc.SolverConfig(mode="pvc", k=k))
+        r = vc.solve(g, vc.SolverConfig(mode="pvc", k=k, warp_limit=wl))
         pc = r.phase_cycles
-        print(f"k={k} kern={r.search_ms:.3f} ms nodes={r.stats.tree_nodes_visited} warp_nodes={r.warp_nodes} "
+        print(f"wl={wl} k={k} kern={r.search_ms:.3f} ms nodes={r.stats.tree_nodes_visited} warp_nodes={r.warp_nodes} "
               f"tasks={r.warp_tasks} last_node={pc['t_node_last_ns']/1e6:.3f} ms task_first={pc['t_task_first_ns']/1e6:.3f} "
               f"task_last={pc['t_task_last_ns']/1e6:.3f} ms max_task={pc['warp_task_max_cycles']/1.9e6:.3f} ms "
               f"max_task_nodes={pc['warp_task_max_nodes']} max_task_n={pc['warp_task_max_n']} "
