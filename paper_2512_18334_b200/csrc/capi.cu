@@ -1452,6 +1452,11 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   if (cfg->deterministic || cfg->record_cover || !cfg->use_components || cfg->disable_pruning ||
       !cfg->load_balance)
     warp_limit0 = 0;
+  // when the wide warp tier carries the search, more warps per block beat
+  // the small blocks a small graph's node operations want: 256 threads with
+  // 128-vertex tasks (G(180, 0.08): 0.91 -> 0.68 s), 128 with 256-vertex
+  // tasks (their workspaces are 4x larger; G(400, 0.1) 15.6 -> 38 M nodes/s)
+  if (auto_threads && warp_limit0 > 64) threads = warp_limit0 > 128 ? 128 : 256;
   // launch plan for a block size, workspace placement (shared memory or a
   // per-block slice of HBM) and CSR placement: dynamic shared memory,
   // warp-tier workspace placement and resident blocks per SM
