@@ -266,8 +266,14 @@ def other_configs(vc, torch, reps=5):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1), r
 
-    for key, name, gen in (("configs[0]", "er200 MVC", lambda: synth.er(200, 4.0, 1)),
-                           ("configs[2]", "ba100k MVC", lambda: synth.ba(100_000, 3, 1))):
+    for key, name, gen in (
+            ("configs[0]", "er200 MVC: G(n=200, avg degree 4), seed 1", lambda: synth.er(200, 4.0, 1)),
+            ("configs[2]", "ba100k MVC: synth.ba(100_000, m=3, seed 1) -- Barabasi-Albert with 2 % "
+                           "single-edge arrivals (pure m=3 BA has minimum degree 3 and nothing for "
+                           "the root rules to start from)", lambda: synth.ba(100_000, 3, 1)),
+            ("configs[3] variant", "planted1m MVC with 3x the noise (synth.planted(oo=1.0)): the "
+                                   "root rules leave a residual to search",
+             lambda: synth.planted(1_000_000, 50_000, 1, oo=1.0))):
         n, off, nbr = gen()
         g = vc.StaticGraph(n, off, nbr)
         vc.solve(g)
@@ -296,7 +302,10 @@ def other_configs(vc, torch, reps=5):
     for key, name, gen in (("configs[4] gnp400", "MVC G(n=400, p=0.1), 2 s budget",
                             lambda: synth.gnp(400, 0.1, 1)),
                            ("configs[4] torus60", "MVC torus 60x60, 2 s budget",
-                            lambda: synth.torus(60, 60))):
+                            lambda: synth.torus(60, 60)),
+                           ("configs[2] pure BA", "MVC pure Barabasi-Albert n=100k m=3 "
+                            "(synth.ba(pendant=0)), 2 s budget",
+                            lambda: synth.ba(100_000, 3, 1, pendant=0.0))):
         n4, off4, nbr4 = gen()
         g4 = vc.StaticGraph(n4, off4, nbr4)
         vc.solve(g4, vc.SolverConfig(timeout=0.2))
