@@ -75,15 +75,17 @@ class Coordinator:
     def __init__(self, store=None, prefix: str = "vcg/"):
         self.store = store
         self.p = prefix
+        # one store request at a time per process: the ticket loop and the
+        # exchanger thread share the client connection
         self._lock = threading.Lock()
         self._best = None
         self._ticket = 0
         self._found = False
 
     def ticket(self) -> int:
-        if self.store is not None:
-            return int(self.store.add(self.p + "ticket", 1)) - 1
         with self._lock:
+            if self.store is not None:
+                return int(self.store.add(self.p + "ticket", 1)) - 1
             t = self._ticket
             self._ticket += 1
             return t
@@ -91,31 +93,40 @@ class Coordinator:
     def offer(self, v: int) -> None:
         """best = min(best, v)."""
         v = int(v)
-        if self.store is None:
-            with self._lock:
-                if self._best is None or v < self._best:
-                    self._best = v
-            return
-        key, want = self.p + "best", str(v).encode()
-        cur = self.store.compare_set(key, "", want)  # sets an absent key
-        while cur != want and int(cur) > v:
-            cur = self.store.compare_set(key, cur, want)
+        with self._lock:
+            if self._best is not None and v >= self._best:
+                return  # this process already knows a cover at least as small
+            if self.store is None:
+                self._best = v
+                return
+            key, want = self.p + "best", str(v).encode()
+            cur = self.store.compare_set(key, "", want)  # sets an absent key
+            while cur != want and int(cur) > v:
+                cur = self.store.compare_set(key, cur, want)
+            self._best = min(v, int(cur))
 
     def best(self) -> int:
-        if self.store is None:
-            return self._best
-        return int(self.store.get(self.p + "best"))
+        with self._lock:
+            if self.store is None:
+                return self._best
+            b = int(self.store.get(self.p + "best"))
+            self._best = b if self._best is None else min(self._best, b)
+            return b
 
     def set_found(self) -> None:
-        if self.store is None:
-            self._found = True
-        else:
-            self.store.set(self.p + "found", "1")
+        with self._lock:
+            if self.store is None:
+                self._found = True
+            else:
+                self.store.set(self.p + "found", "1")
+                self._found = True
 
     def found(self) -> bool:
-        if self.store is None:
+        with self._lock:
+            if self.store is None or self._found:
+                return self._found
+            self._found = self.store.check([self.p + "found"])
             return self._found
-        return self.store.check([self.p + "found"])
 
 
 def _dist():
@@ -211,11 +222,15 @@ class GpuBackend:
         def exchanger():  # the host side of the in-flight exchange
             _lib.set_device(dev)
             lb = C.c_int64()
-            while not done.wait(0.0005):
+            posted = (int(bound), 0)
+            while not done.wait(0.001):
                 _lib.check(_lib.lib.vcg_exchange_peek(x, C.byref(lb)))
                 if lb.value < (1 << 31) - 1:
                     coord.offer(S_i + lb.value)
-                _lib.check(_lib.lib.vcg_exchange_post(x, coord.best() - S_i, int(coord.found())))
+                now = (coord.best() - S_i, int(coord.found()))
+                if now != posted:  # post only news (a DMA and a stream sync)
+                    _lib.check(_lib.lib.vcg_exchange_post(x, now[0], now[1]))
+                    posted = now
 
         def hook(sc):
             sc.root_deg = deg.ctypes.data
