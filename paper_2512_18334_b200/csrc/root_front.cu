@@ -86,7 +86,7 @@ struct Front {  // device arrays (root_front_bytes)
   int *ia, *ib, *st, *rs;           // targets, triangle state, removal tag
   int *l1[2], *l2[2];               // frontier lists (pending / snapshot)
   int *rem, *cand;
-  int2* chunk;                      // removal work items (vertex, first entry)
+  int4* chunk;                      // removal work items (vertex, first entry, end, -)
   uint8_t* forced;
   uint8_t* trk;                     // adjacency longer than kTrack: sums maintained
 };
@@ -136,11 +136,12 @@ __device__ __forceinline__ unsigned long long claim_key(int tg, int v) {
 // shared memory: one global atomic per block and phase instead of one per
 // entry (the list counters are the kernel's only hot words).
 constexpr int kQ = 2048;
+constexpr int kQC = 1024;  // staged removal chunks (16 B each)
 struct BlockQ {
   int cnt[2], base[2];
   int buf[2][kQ];
   int ccnt, cbase, cused;  // removal chunks: reserved, published base, staged
-  int2 cbuf[kQ];
+  int4 cbuf[kQC];
 };
 
 __device__ __forceinline__ void qpush(BlockQ* q, int which, int* list, int* gcnt, int v) {
@@ -179,25 +180,28 @@ __device__ __forceinline__ void two_from_sums(const Front& F, int v, int* a, int
 // u joins the removal set of step s: the rem list, and its adjacency as
 // kChunk-entry work items
 __device__ __forceinline__ void add_removed(const Front& F, FrontCtl* G, BlockQ* q,
-                                            const int* off, int s, int u) {
+                                            const int* off, int s, int u, long long* walked) {
   F.rs[u] = s;
   qpush(q, 0, F.rem, &G->nrem[s % 3], u);
   const int b = off[u], e = off[u + 1];
+  *walked += e - b;
   const int nc = (e - b + kChunk - 1) / kChunk;
   if (nc > 0) {
     const int pos = atomicAdd(&q->ccnt, nc);
-    if (pos + nc <= kQ) {
-      for (int c = 0; c < nc; ++c) q->cbuf[pos + c] = make_int2(u, b + c * kChunk);
+    if (pos + nc <= kQC) {
+      for (int c = 0; c < nc; ++c)
+        q->cbuf[pos + c] = make_int4(u, b + c * kChunk, min(e, b + (c + 1) * kChunk), 0);
       atomicMax(&q->cused, pos + nc);
     } else {  // staging full: append directly
       const int at = atomicAdd(&G->nchunk[s % 3], nc);
-      for (int c = 0; c < nc; ++c) F.chunk[at + c] = make_int2(u, b + c * kChunk);
+      for (int c = 0; c < nc; ++c)
+        F.chunk[at + c] = make_int4(u, b + c * kChunk, min(e, b + (c + 1) * kChunk), 0);
     }
   }
 }
 
 // every thread of the block calls: publishes the staged removal chunks
-__device__ __forceinline__ void cflush(BlockQ* q, int2* list, int* cnt) {
+__device__ __forceinline__ void cflush(BlockQ* q, int4* list, int* cnt) {
   __syncthreads();
   const int c = q->cused;
   if (threadIdx.x == 0) q->cbase = c ? atomicAdd(cnt, c) : 0;
@@ -232,10 +236,9 @@ __device__ __forceinline__ void live_short(const Front& F, const int* off, const
 // one removal work item: the entries [b, min(b + kChunk, end(u))) of removed
 // vertex u.  Non-member live neighbours lose a degree and u from their sums;
 // 2 -> 1 and 3 -> 2 transitions are pushed to the pending lists.
-__device__ __forceinline__ void rm_chunk(const Front& F, FrontCtl* G, BlockQ* q, const int* off,
+__device__ __forceinline__ void rm_chunk(const Front& F, FrontCtl* G, BlockQ* q,
                                          const int* nbr, int s, int p1, int p2, int u, int b,
-                                         long long* edges) {
-  const int e = min(off[u + 1], b + kChunk);
+                                         int e, long long* edges) {
   const int len = e - b;
   int x[kChunk], live[kChunk];
 #pragma unroll
@@ -281,15 +284,14 @@ __device__ __forceinline__ void remove_set(const Ex& E, const Front& F, FrontCtl
                                            const int* off, const int* nbr, int s, int p1, int p2,
                                            long long* edges, long long* walked) {
   const int nrem = vld(&G->nrem[s % 3]), nch = vld(&G->nchunk[s % 3]);
-  for (int c = E.rank; c < nch; c += E.size) {
-    const int2 ch = F.chunk[c];
-    rm_chunk(F, G, q, off, nbr, s, p1, p2, ch.x, ch.y, edges);
-  }
-  for (int k = E.rank; k < nrem; k += E.size) {
+  for (int k = E.rank; k < nrem; k += E.size) {  // independent of the chunks: issued first
     const int u = F.rem[k];
-    *walked += off[u + 1] - off[u];
     F.deg[u] = 0;
     F.forced[u] = 1;
+  }
+  for (int c = E.rank; c < nch; c += E.size) {
+    const int4 ch = __ldcg(F.chunk + c);
+    rm_chunk(F, G, q, nbr, s, p1, p2, ch.x, ch.y, ch.z, edges);
   }
   qflush(q, F.l1[p1], &G->cnt1[p1], F.l2[p2], &G->cnt2[p2]);
 }
@@ -413,7 +415,7 @@ __device__ __forceinline__ void sweep_d1(const Ex& E, const Front& F, FrontCtl* 
     const int u = F.ia[v];
     const bool win = __ldcg(F.key + u) == claim_key(t, v);
     const bool twin = dget(F.deg, u) == 1 && __ldcg(F.ia + u) == v && u < v;
-    if (win && !twin) add_removed(F, G, q, off, s, u);
+    if (win && !twin) add_removed(F, G, q, off, s, u, walked);
   }
   qflush(q, F.rem, &G->nrem[s % 3], F.rem, &G->nrem[s % 3]);
   cflush(q, F.chunk, &G->nchunk[s % 3]);
@@ -522,8 +524,8 @@ __device__ __forceinline__ void sweep_tri(const Ex& E, const Front& F, FrontCtl*
           const unsigned long long key = claim_key(t, v);
           if (__ldcg(F.key + v) == key && __ldcg(F.key + u) == key && __ldcg(F.key + x) == key) {
             F.st[v] = 5;  // in
-            add_removed(F, G, q, off, s, u);
-            add_removed(F, G, q, off, s, x);
+            add_removed(F, G, q, off, s, u, walked);
+            add_removed(F, G, q, off, s, x, walked);
           } else {
             still = 1;
           }
@@ -655,7 +657,7 @@ __global__ void __launch_bounds__(kRootGridThreads, 1)
     F.cand = ip + 9 * nn;
     F.forced = (uint8_t*)(ip + 10 * nn);
     F.trk = F.forced + nn;
-    F.chunk = (int2*)(F.trk + nn);
+    F.chunk = (int4*)(((uintptr_t)(F.trk + nn) + 15) & ~(uintptr_t)15);
   }
   int* hd_out = F.cand;  // the high-degree sweep's ids (cand is free outside triangle sweeps)
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, T = gridDim.x * blockDim.x;
@@ -823,7 +825,7 @@ size_t root_front_bytes(int n, long long m2) {
   const size_t nn = ((size_t)n + 31) & ~(size_t)31;
   // key, nsum, nsq, 10 int arrays, forced, trk, then the chunk list: every vertex
   // is removed at most once, so a step's chunks number at most n + m2 / kChunk
-  return 24 * nn + 40 * nn + 2 * nn + 8 * ((size_t)n + (size_t)m2 / kChunk + 1) + 256;
+  return 24 * nn + 40 * nn + 2 * nn + 16 * ((size_t)n + (size_t)m2 / kChunk + 1) + 256;
 }
 
 int root_front_blocks() {
