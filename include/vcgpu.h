@@ -171,6 +171,12 @@ typedef struct {
   struct vcg_exchange* exchange; /* nullable: in-flight bound / stop exchange with other
                                  searches (vcg_exchange_*); the kernel polls it and
                                  publishes its root scope's achieved best into it */
+  struct vcg_peer* peer;      /* nullable: global best / stop words shared by every
+                                 rank of a distributed solve (vcg_peer_*): the kernel
+                                 reads them and updates them with system-scope atomics,
+                                 no host in the loop */
+  int64_t peer_offset;        /* cover size of this search's root in the global count
+                                 (the subtree's S) */
 } vcg_search_config;
 
 typedef struct {
@@ -232,6 +238,23 @@ int vcg_exchange_reset(vcg_exchange* x);
 int vcg_exchange_post(vcg_exchange* x, int64_t bound, int stop);
 /* the search's best achieved root cover so far (INT32_MAX: none) */
 int vcg_exchange_peek(vcg_exchange* x, int64_t* local_best);
+
+/* Peer words of a distributed solve: [best absolute cover, stop] in one
+ * rank's device memory, mapped into the other ranks' processes by CUDA IPC
+ * (over NVLink when the ranks are on different GPUs) so every running search
+ * kernel reads the global best and publishes its own covers / the PVC stop
+ * with system-scope atomics -- the device-side form of vcg_exchange, with no
+ * host thread relaying.  create + handle on one rank, open on the others
+ * (handle: VCG_PEER_HANDLE_BYTES opaque bytes); offer = atomic min / stop
+ * from the host between searches; read = the current words. */
+#define VCG_PEER_HANDLE_BYTES 64
+typedef struct vcg_peer vcg_peer;
+int vcg_peer_create(vcg_peer** out);
+int vcg_peer_handle(const vcg_peer* p, void* handle);
+int vcg_peer_open(const void* handle, vcg_peer** out);
+int vcg_peer_destroy(vcg_peer* p);
+int vcg_peer_offer(vcg_peer* p, int64_t best, int stop);
+int vcg_peer_read(const vcg_peer* p, int64_t* best, int* stop);
 
 /* Run the persistent search kernel.  hist_out (nullable, capacity n+2)
  * receives the components-per-branch histogram indexed by component count. */

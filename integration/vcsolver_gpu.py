@@ -43,7 +43,8 @@ class SearchConfig(C.Structure):  # vcg_search_config
         ("workers", C.c_int), ("threads", C.c_int), ("worklist_threshold", I64),
         ("timeout", C.c_double), ("check_registry", C.c_int), ("record_cover", C.c_int),
         ("cover_out", P), ("root_deg", P), ("warp_limit", C.c_int), ("gpu_share", C.c_int),
-        ("registry_out", P), ("registry_cap", I64), ("exchange", P),
+        ("registry_out", P), ("registry_cap", I64), ("exchange", P), ("peer", P),
+        ("peer_offset", I64),
     ]
 
 

@@ -44,7 +44,7 @@ class SearchConfig_t(C.Structure):
         ("timeout", C.c_double), ("check_registry", C.c_int), ("record_cover", C.c_int),
         ("cover_out", C.c_void_p), ("root_deg", C.c_void_p), ("warp_limit", C.c_int),
         ("gpu_share", C.c_int), ("registry_out", C.c_void_p), ("registry_cap", I64),
-        ("exchange", C.c_void_p),
+        ("exchange", C.c_void_p), ("peer", C.c_void_p), ("peer_offset", I64),
     ]
 
 
@@ -83,7 +83,8 @@ EXPORTS = (
     "vcg_search", "vcg_node_op", "vcg_last_error", "vcg_device_count", "vcg_launch_count",
     "vcg_set_device", "vcg_get_device", "vcg_expand", "vcg_shutdown", "vcg_brute_force_mvc",
     "vcg_exchange_create", "vcg_exchange_destroy", "vcg_exchange_reset", "vcg_exchange_post",
-    "vcg_exchange_peek",
+    "vcg_exchange_peek", "vcg_peer_create", "vcg_peer_handle", "vcg_peer_open",
+    "vcg_peer_destroy", "vcg_peer_offer", "vcg_peer_read",
 )
 
 
@@ -126,6 +127,12 @@ def _load():
     lib.vcg_exchange_reset.argtypes = [P]
     lib.vcg_exchange_post.argtypes = [P, I64, C.c_int]
     lib.vcg_exchange_peek.argtypes = [P, C.POINTER(I64)]
+    lib.vcg_peer_create.argtypes = [C.POINTER(P)]
+    lib.vcg_peer_handle.argtypes = [P, P]
+    lib.vcg_peer_open.argtypes = [P, C.POINTER(P)]
+    lib.vcg_peer_destroy.argtypes = [P]
+    lib.vcg_peer_offer.argtypes = [P, I64, C.c_int]
+    lib.vcg_peer_read.argtypes = [P, C.POINTER(I64), C.POINTER(C.c_int)]
     lib.vcg_shutdown.restype = None
     return lib
 

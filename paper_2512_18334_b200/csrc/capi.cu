@@ -1736,6 +1736,8 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   static thread_local long long hb_cap = 0;
   const char* hb_env = getenv("VCG_HEARTBEAT");
   P.xch = cfg->exchange ? cfg->exchange->d : nullptr;
+  P.gpeer = cfg->peer ? cfg->peer->d : nullptr;
+  P.gpeer_off = (int)cfg->peer_offset;
   P.hb = nullptr;
   if (hb_env) {
     const long long need = (long long)blocks * kMaxWarps;
@@ -1968,6 +1970,86 @@ extern "C" int vcg_exchange_peek(vcg_exchange* x, int64_t* local_best) {
   CK(cudaMemcpyAsync(&v, x->d + 2, 4, cudaMemcpyDeviceToHost, cudaStreamPerThread));
   CK(cudaStreamSynchronize(cudaStreamPerThread));
   *local_best = v;
+  return 0;
+}
+
+// ------------------------------------------------------------ peer words --
+
+struct vcg_peer {
+  int32_t* d = nullptr;  // [0] best absolute cover, [1] stop, [2..3] pad
+  int owner = 0;         // allocated here (else mapped from another process)
+};
+
+__global__ void k_peer_offer(int32_t* d, int best, int stop) {
+  if (best >= 0) atomicMin_system(d, best);
+  if (stop) atomicExch_system(d + 1, 1);
+}
+
+extern "C" int vcg_peer_create(vcg_peer** out) {
+  if (int r = need_device()) return r;
+  if (!out) return fail(VCG_EINVAL, "bad arguments");
+  auto* p = new vcg_peer();
+  if (cudaMalloc(&p->d, 16) != cudaSuccess) {
+    delete p;
+    return fail(VCG_ERESOURCE, "peer: cudaMalloc failed");
+  }
+  p->owner = 1;
+  const int32_t init[4] = {kInf, 0, 0, 0};
+  CK(cudaMemcpy(p->d, init, 16, cudaMemcpyHostToDevice));
+  *out = p;
+  return 0;
+}
+
+extern "C" int vcg_peer_handle(const vcg_peer* p, void* handle) {
+  if (!p || !handle || !p->owner) return fail(VCG_EINVAL, "bad arguments");
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, p->d));
+  static_assert(sizeof(h) <= VCG_PEER_HANDLE_BYTES, "IPC handle size");
+  memset(handle, 0, VCG_PEER_HANDLE_BYTES);
+  memcpy(handle, &h, sizeof(h));
+  return 0;
+}
+
+extern "C" int vcg_peer_open(const void* handle, vcg_peer** out) {
+  if (int r = need_device()) return r;
+  if (!handle || !out) return fail(VCG_EINVAL, "bad arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* ptr = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess)
+    return fail(VCG_ECUDA, std::string("peer: cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+  auto* p = new vcg_peer();
+  p->d = (int32_t*)ptr;
+  *out = p;
+  return 0;
+}
+
+extern "C" int vcg_peer_destroy(vcg_peer* p) {
+  if (!p) return 0;
+  if (!g_shutdown.load()) {
+    if (p->owner) cudaFree(p->d);
+    else cudaIpcCloseMemHandle(p->d);
+  }
+  delete p;
+  return 0;
+}
+
+extern "C" int vcg_peer_offer(vcg_peer* p, int64_t best, int stop) {
+  if (!p) return fail(VCG_EINVAL, "bad arguments");
+  COUNT_LAUNCH(1);
+  k_peer_offer<<<1, 1>>>(p->d, best < 0 ? -1 : (int)std::min<int64_t>(best, kInf), stop);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(cudaStreamPerThread));
+  return 0;
+}
+
+extern "C" int vcg_peer_read(const vcg_peer* p, int64_t* best, int* stop) {
+  if (!p || !best || !stop) return fail(VCG_EINVAL, "bad arguments");
+  int32_t w[2] = {kInf, 0};
+  CK(cudaMemcpy(w, p->d, 8, cudaMemcpyDeviceToHost));
+  *best = w[0];
+  *stop = w[1];
   return 0;
 }
 

@@ -194,11 +194,50 @@ struct SearchParams {
   // vcg_exchange words: [0] external root bound (kInf: none), [1] external
   // stop, [2] this search's best achieved root cover (kInf: none); or null
   int* xch;
+  // peer exchange (vcg_peer): the distributed solve's global words, in one
+  // rank's device memory and mapped into every rank's address space by CUDA
+  // IPC (NVLink peer memory across GPUs): [0] best absolute cover, [1] stop.
+  // This search's root covers are offset by gpeer_off (the subtree's S).
+  int* gpeer;
+  int gpeer_off;
 };
+
+__device__ __forceinline__ int ld_relaxed_sys(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// external bound / stop from the exchange words (thread 0 of a block or lane
+// 0 of a warp): true when the search must stop
+__device__ inline bool xch_poll(const SearchParams& P, int root_key_idx_unused = 0) {
+  (void)root_key_idx_unused;
+  bool stop = false;
+  int bound = kInf;
+  if (P.xch) {
+    const int xb = __ldcg(&P.xch[0]), xs = __ldcg(&P.xch[1]);
+    stop |= xs != 0;
+    bound = xb;
+  }
+  if (P.gpeer) {
+    const int gb = ld_relaxed_sys(&P.gpeer[0]), gs = ld_relaxed_sys(&P.gpeer[1]);
+    stop |= gs != 0;
+    if (gb < kInf) bound = min(bound, gb - P.gpeer_off);
+  }
+  if (bound <= 0) stop = true;
+  if (stop) {
+    atomicExch(&P.ctl->stop, 1);
+    return true;
+  }
+  if (bound < kInf) atomicMin(&P.reg.key[P.root_index], 2 * bound + 1);
+  return false;
+}
 
 // an achieved root-scope cover of `value` vertices: publish it to the exchange
 __device__ __forceinline__ void xch_publish(const SearchParams& P, int idx, int value) {
-  if (P.xch && idx == P.root_index) atomicMin(&P.xch[2], value);
+  if (idx != P.root_index) return;
+  if (P.xch) atomicMin(&P.xch[2], value);
+  if (P.gpeer) atomicMin_system(&P.gpeer[0], value + P.gpeer_off);
 }
 
 template <typename T>
@@ -406,6 +445,7 @@ __device__ inline void reg_submit(const SearchParams& P, int idx, int value, boo
   if (best <= P.k_red) {
     atomicExch(&P.ctl->found, 1);
     atomicExch(&P.ctl->stop, 1);
+    if (P.gpeer) atomicExch_system(&P.gpeer[1], 1);  // PVC answered: every rank stops
   }
 }
 

@@ -828,15 +828,7 @@ __global__ void __launch_bounds__(VCG_SEARCH_MAXT, VCG_SEARCH_MINB) search_kerne
         }
         // in-flight exchange (vcg_exchange): a cover found elsewhere bounds
         // the root scope (not achieved here); an external stop ends the search
-        if (!stop && P.xch && (xpoll++ & 15) == 0) {
-          const int xb = __ldcg(&P.xch[0]), xs = __ldcg(&P.xch[1]);
-          if (xs || xb <= 0) {
-            atomicExch(&P.ctl->stop, 1);
-            stop = 1;
-          } else if (xb < kInf) {
-            atomicMin(&P.reg.key[P.root_index], 2 * xb + 1);
-          }
-        }
+        if (!stop && (P.xch || P.gpeer) && (xpoll++ & 15) == 0 && xch_poll(P)) stop = 1;
         st.flag = stop;
       }
       __syncthreads();

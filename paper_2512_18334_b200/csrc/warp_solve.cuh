@@ -894,10 +894,14 @@ __device__ inline bool warp_epoch(const SearchParams& P, void* wws_raw, int* bus
   WS& ws = ((WS*)wws_raw)[threadIdx.x >> 5];
   bool any = false;
   unsigned backoff = 64;
+  unsigned polls = 0;
   while (true) {
     long long pos = -1;
     int stop = 0, node_work = 0;
     if (lane == 0) {
+      // the exchange words are polled here too: a block can stay in the
+      // warp tier for the whole search
+      if ((P.xch || P.gpeer) && (polls++ & 7) == 0) xch_poll(P);
       stop = ld_relaxed(&P.ctl->stop);
       node_work = (long long)ld_relaxed_u64(P.q.count) > 0;
       if (!stop && !node_work) {

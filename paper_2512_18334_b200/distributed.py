@@ -15,16 +15,17 @@ one from a shared ticket counter (an atomic ``add`` on the process group's
 c10d store), so a rank stuck in a deep subtree never holds up the others and
 the ranks finish within one subtree of each other.
 
-Bound and termination propagation (engine.py:453-495 across processes):
-the global best cover size lives in the store (compare-and-set minimum).
-While a rank's search kernel runs, a host thread on that rank polls the
-kernel's own best achieved root cover through a ``vcg_exchange`` (device
-words read and written by DMA on the copy engines, so the persistent kernel
-keeps every SM), offers it to the store, and posts the store's best back as
-the subtree's external bound (a cover of that size exists elsewhere; the
-kernel lowers its root key to it, not achieved).  PVC: the first rank that
-reaches k sets the store's stop flag, which the other ranks post to their
-kernels and which stops the ticket loop everywhere.
+Bound and termination propagation (engine.py:453-495 across processes),
+default ``exchange="peer"``: the global best cover size and the PVC stop
+flag are two device words on rank 0's GPU, mapped into every rank by CUDA
+IPC (NVLink peer memory across GPUs).  Every running search kernel polls
+them (block loop and warp-tier loop), lowers its subtree's root bound to
+global best - S_i, and publishes its own covers (+ S_i) and a PVC answer with
+system-scope atomics -- no host in the loop.  Fallback ``exchange="store"``
+(a rank that cannot map the words): the best is a compare-and-set minimum
+in the c10d store, relayed to each running kernel by a host thread through
+a ``vcg_exchange`` (device words read and written by DMA on the copy
+engines).  Either way a PVC answer stops the ticket loop everywhere.
 
 A subtree whose residual graph is disconnected is solved by the
 component-aware search itself.  Reference behaviour replaced: engine.py:200
@@ -152,14 +153,104 @@ def _allreduce(values, op, group=None):
     return [int(x) for x in t.cpu().tolist()]
 
 
-def _coordinator(group):
+class PeerCoordinator(Coordinator):
+    """The global best and PVC stop as device words (vcg_peer): allocated on
+    rank 0's GPU, mapped into every other rank by CUDA IPC -- NVLink peer
+    memory across GPUs -- so the running search kernels read the global bound
+    and publish their covers / the PVC stop themselves with system-scope
+    atomics (no host thread relaying).  Tickets stay on the store."""
+
+    def __init__(self, store, prefix, peer):
+        super().__init__(store, prefix)
+        self.peer = peer  # vcg_peer* (c_void_p)
+
+    def offer(self, v: int) -> None:
+        from . import _lib
+
+        v = int(v)
+        with self._lock:
+            if self._best is not None and v >= self._best:
+                return
+            _lib.check(_lib.lib.vcg_peer_offer(self.peer, v, 0))
+            self._best = v
+
+    def _read(self):
+        from . import _lib
+
+        b, st = C.c_int64(), C.c_int()
+        _lib.check(_lib.lib.vcg_peer_read(self.peer, C.byref(b), C.byref(st)))
+        return int(b.value), bool(st.value)
+
+    def best(self) -> int:
+        with self._lock:
+            b = self._read()[0]
+            self._best = b if self._best is None else min(self._best, b)
+            return b
+
+    def set_found(self) -> None:
+        from . import _lib
+
+        with self._lock:
+            _lib.check(_lib.lib.vcg_peer_offer(self.peer, -1, 1))
+            self._found = True
+
+    def found(self) -> bool:
+        with self._lock:
+            if not self._found:
+                self._found = self._read()[1]
+            return self._found
+
+
+def _open_peer(dist, group, rank):
+    """Rank 0 creates the peer words, every rank maps them; None unless every
+    rank succeeded (the store exchange is the fallback)."""
+    from . import _lib
+
+    h = C.c_void_p()
+    blob = [None]
+    ok = 1
+    if rank == 0:
+        handle = (C.c_char * 64)()
+        ok = int(_lib.lib.vcg_peer_create(C.byref(h)) == 0 and
+                 _lib.lib.vcg_peer_handle(h, handle) == 0)
+        blob[0] = bytes(handle) if ok else None
+    dist.broadcast_object_list(blob, src=dist.get_global_rank(group, 0) if group else 0,
+                               group=group)
+    if rank != 0:
+        ok = int(blob[0] is not None and
+                 _lib.lib.vcg_peer_open(C.create_string_buffer(blob[0], 64), C.byref(h)) == 0)
+    if _allreduce([ok], "min", group)[0]:
+        return h
+    if h.value:
+        _lib.lib.vcg_peer_destroy(h)
+    return None
+
+
+def _close_peer(coord, dist, group, rank):
+    from . import _lib
+
+    if not isinstance(coord, PeerCoordinator):
+        return
+    if rank != 0:  # mappings are closed before the owner frees the words
+        _lib.lib.vcg_peer_destroy(coord.peer)
+    dist.barrier(group=group)
+    if rank == 0:
+        _lib.lib.vcg_peer_destroy(coord.peer)
+
+
+def _coordinator(group, exchange="store"):
     dist = _dist()
     call = next(_CALLS)  # every rank makes the same sequence of calls
     if dist is None or dist.get_world_size(group) == 1:
         return Coordinator()
     from torch.distributed import distributed_c10d as c10d
 
-    return Coordinator(c10d._get_default_store(), prefix=f"vcg/solve{call}/")
+    store, prefix = c10d._get_default_store(), f"vcg/solve{call}/"
+    if exchange == "peer":
+        peer = _open_peer(dist, group, dist.get_rank(group))
+        if peer is not None:
+            return PeerCoordinator(store, prefix, peer)
+    return Coordinator(store, prefix)
 
 
 # ----------------------------------------------------------------- backend --
@@ -213,6 +304,20 @@ class GpuBackend:
         from .engine import run_search
 
         deg = np.ascontiguousarray(root_deg, dtype=np.int32)
+        sub_cfg = replace(cfg, timeout=timeout)
+        if isinstance(coord, PeerCoordinator):
+            # the kernel itself reads / updates the global words
+            def peer_hook(sc):
+                sc.root_deg = deg.ctypes.data
+                sc.peer = coord.peer
+                sc.peer_offset = S_i
+
+            res, hist, _ = run_search(rg, sub_cfg, width, bound, False, k_red,
+                                      config_hook=peer_hook)
+            improved = int(res.best) < bound and bool(res.best_achieved)
+            return SubtreeResult(int(res.best) if improved else None,
+                                 int(res.tree_nodes_visited), bool(res.found), hist,
+                                 bool(res.timed_out))
         x = self._exchange()
         _lib.check(_lib.lib.vcg_exchange_reset(x))
         _lib.check(_lib.lib.vcg_exchange_post(x, int(bound), int(coord.found())))
@@ -236,7 +341,6 @@ class GpuBackend:
             sc.root_deg = deg.ctypes.data
             sc.exchange = x
 
-        sub_cfg = replace(cfg, timeout=timeout)
         t = threading.Thread(target=exchanger, daemon=True)
         t.start()
         try:
@@ -252,8 +356,15 @@ class GpuBackend:
 # ------------------------------------------------------------------- solve --
 
 def solve_distributed(g, config: SolverConfig | None = None, group=None,
-                      subtrees_per_rank: int = 8, backend=None) -> SolveResult:
-    """engine.py:561 solve, one instance across every rank of ``group``."""
+                      subtrees_per_rank: int = 8, backend=None,
+                      exchange: str = "auto") -> SolveResult:
+    """engine.py:561 solve, one instance across every rank of ``group``.
+
+    ``exchange``: "peer" -- the global best / stop as device words every
+    rank's kernels update directly (CUDA IPC / NVLink peer memory);
+    "store" -- the c10d store, relayed to each running kernel by a host
+    thread through a vcg_exchange; "auto" -- peer for the GPU backend,
+    falling back to the store when a rank cannot map the words."""
     cfg = config if config is not None else SolverConfig()
     cfg.validate()
     if cfg.record_cover:
@@ -262,7 +373,9 @@ def solve_distributed(g, config: SolverConfig | None = None, group=None,
     dist = _dist()
     rank = dist.get_rank(group) if dist else 0
     world = dist.get_world_size(group) if dist else 1
-    coord = _coordinator(group)
+    if exchange not in ("auto", "peer", "store"):
+        raise ValueError(f"unknown exchange {exchange!r}")
+    use_peer = exchange == "peer" or (exchange == "auto" and isinstance(be, GpuBackend))
     t_start = time.perf_counter()
     deadline = None if cfg.timeout is None else t_start + cfg.timeout
 
@@ -295,6 +408,7 @@ def solve_distributed(g, config: SolverConfig | None = None, group=None,
     else:
         best_init = max(1, min(pre.greedy_reduced, pre.greedy_original - pre.forced_count))
 
+    coord = _coordinator(group, "peer" if use_peer else "store")
     t1 = time.perf_counter()
     sub = be.expand(rg, cfg, best_init, max(1, subtrees_per_rank * world))
     best0 = min(best_init, sub.best)
@@ -349,6 +463,7 @@ def solve_distributed(g, config: SolverConfig | None = None, group=None,
         for h in parts:
             for key, c in h.items():
                 hist[key] = hist.get(key, 0) + c
+        _close_peer(coord, dist, group, rank)
     stats.tree_nodes_visited = nodes
     stats.components_per_branch = hist
     if cfg.mode == "mvc":
@@ -362,4 +477,5 @@ def solve_distributed(g, config: SolverConfig | None = None, group=None,
     return result
 
 
-__all__ = ["solve_distributed", "GpuBackend", "Subtrees", "SubtreeResult", "Coordinator"]
+__all__ = ["solve_distributed", "GpuBackend", "Subtrees", "SubtreeResult", "Coordinator",
+           "PeerCoordinator"]

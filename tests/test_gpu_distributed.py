@@ -91,7 +91,7 @@ def test_exchange_bound_stop_and_publish():
         _lib.lib.vcg_exchange_destroy(x)
 
 
-def _gpu_worker(rank, world, port, cases, q):
+def _gpu_worker(rank, world, port, cases, q, exchange="auto"):
     import os
 
     import torch.distributed as dist
@@ -105,18 +105,22 @@ def _gpu_worker(rank, world, port, cases, q):
     for name, n, edges, opt, pvc in cases:
         n, off, nbr = csr(n, edges)
         g = vc.StaticGraph(n, off, nbr)
-        r = solve_distributed(g, vc.SolverConfig(), subtrees_per_rank=3)
+        r = solve_distributed(g, vc.SolverConfig(), subtrees_per_rank=3, exchange=exchange)
         ks = {int(k): solve_distributed(g, vc.SolverConfig(mode="pvc", k=int(k)),
-                                        subtrees_per_rank=3).found for k in pvc}
+                                        subtrees_per_rank=3, exchange=exchange).found
+              for k in pvc}
         out.append((name, r.cover_size, r.exact, ks))
     q.put((rank, out))
     dist.destroy_process_group()
 
 
-def test_two_ranks_share_one_gpu():
+@pytest.mark.parametrize("exchange", ["peer", "store"])
+def test_two_ranks_share_one_gpu(exchange):
     """The GPU backend at world size 2 (two processes on cuda:0 over gloo):
-    subtrees from the store's ticket counter, bounds and PVC stops through the
-    store and each rank's vcg_exchange -- the reference's answers on every rank."""
+    subtrees from the store's ticket counter; bounds and PVC stops through the
+    peer words (CUDA IPC, updated by the kernels themselves) or through the
+    store and each rank's vcg_exchange -- the reference's answers on every
+    rank."""
     import socket
 
     import torch.multiprocessing as mp
@@ -129,7 +133,8 @@ def test_two_ranks_share_one_gpu():
              for c in golden("solve.json")[::9] if c["n"] > 0]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, cases, q)) for r in range(2)]
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, cases, q, exchange))
+             for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=900) for _ in procs)
@@ -140,3 +145,50 @@ def test_two_ranks_share_one_gpu():
     for (name, _, _, opt, pvc), (name2, mvc, exact, ks) in zip(cases, res[0]):
         assert name == name2 and mvc == opt and exact, name
         assert ks == {int(k): f for k, f in pvc.items()}, name
+
+
+def _peer_worker(rank, port, q):
+    """Both ranks map rank 0's peer words; covers offered by each are seen by
+    both, a stop set by one is seen by the other."""
+    import ctypes as C
+    import os
+
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    from paper_2512_18334_b200 import distributed as D
+
+    coord = D._coordinator(None, "peer")
+    kind = type(coord).__name__
+    coord.offer(100 - rank)
+    dist.barrier()
+    b1 = coord.best()
+    if rank == 1:
+        coord.set_found()
+    dist.barrier()
+    f = coord.found()
+    D._close_peer(coord, dist, None, rank)
+    q.put((rank, kind, b1, f))
+    dist.destroy_process_group()
+
+
+def test_peer_words_two_processes():
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_peer_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r, (k, b, f)) for r, k, b, f in (q.get(timeout=300) for _ in procs))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in (0, 1):
+        assert res[r] == ("PeerCoordinator", 99, True), res
