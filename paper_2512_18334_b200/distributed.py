@@ -12,8 +12,9 @@ which yields open subtrees that partition the remaining search:
 Load balance (engine.py:245-273 take/steal, :413 offload -- here across
 processes): subtrees are not dealt statically; an idle rank takes the next
 one from a shared ticket counter (an atomic ``add`` on the process group's
-c10d store), so a rank stuck in a deep subtree never holds up the others and
-the ranks finish within one subtree of each other.
+c10d store), largest residual first (LPT), so a rank stuck in a deep subtree
+never holds up the others and the ranks finish within one short subtree of
+each other.
 
 Bound and termination propagation (engine.py:453-495 across processes),
 default ``exchange="peer"``: the global best cover size and the PVC stop
@@ -419,7 +420,11 @@ def solve_distributed(g, config: SolverConfig | None = None, group=None,
     coord.offer(best0)
     if k_red is not None and best0 <= k_red:
         coord.set_found()
-    order = np.nonzero(~edge_free)[0]
+    # tickets in longest-processing-time order: the subtrees with the most
+    # residual edges first (the same order on every rank), so the last
+    # tickets are the short ones and the ranks finish together
+    cand = np.nonzero(~edge_free)[0]
+    order = cand[np.argsort(-sub.deg[cand].sum(axis=1), kind="stable")] if len(cand) else cand
     nodes = sub.nodes if rank == 0 else 0
     hist: dict[int, int] = {}
     timed_out = False
