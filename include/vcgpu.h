@@ -121,12 +121,18 @@ typedef struct {
  * 1 = `bound` given (PVC; greedy_original is not computed, reported as -1),
  * 2 = `bound` given and greedy_original computed as well.
  * forced_out: capacity n, original ids in forcing order (index order under
- * VCG_ROOT_ANY_ORDER).
+ * VCG_ROOT_ANY_ORDER); NULL keeps them on the device with the reduced graph
+ * (vcg_graph_forced), which takes their download off the solve's path.
  * vertex_map_out: capacity n, reduced id -> original id.
  * reduced_out: new graph handle (the input handle itself is never aliased). */
 int vcg_root_reduce(const vcg_graph* g, int enabled, int crown, int has_bound, int64_t bound,
                     vcg_preprocessed* info, int32_t* forced_out, int64_t* vertex_map_out,
                     vcg_graph** reduced_out);
+
+/* The forced ids of the root reduction that produced `reduced` when it was
+ * called with forced_out == NULL: *count of them, copied to out (capacity
+ * *count, nullable). */
+int vcg_graph_forced(const vcg_graph* reduced, int32_t* out, int64_t* count);
 
 typedef struct {
   int width;                  /* 8, 16 or 32: degree-array entry width */

@@ -84,7 +84,7 @@ EXPORTS = (
     "vcg_set_device", "vcg_get_device", "vcg_expand", "vcg_shutdown", "vcg_brute_force_mvc",
     "vcg_exchange_create", "vcg_exchange_destroy", "vcg_exchange_reset", "vcg_exchange_post",
     "vcg_exchange_peek", "vcg_peer_create", "vcg_peer_handle", "vcg_peer_open",
-    "vcg_peer_destroy", "vcg_peer_offer", "vcg_peer_read",
+    "vcg_peer_destroy", "vcg_peer_offer", "vcg_peer_read", "vcg_graph_forced",
 )
 
 
@@ -133,6 +133,7 @@ def _load():
     lib.vcg_peer_destroy.argtypes = [P]
     lib.vcg_peer_offer.argtypes = [P, I64, C.c_int]
     lib.vcg_peer_read.argtypes = [P, C.POINTER(I64), C.POINTER(C.c_int)]
+    lib.vcg_graph_forced.argtypes = [P, P, C.POINTER(I64)]
     lib.vcg_shutdown.restype = None
     return lib
 

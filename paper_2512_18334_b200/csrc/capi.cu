@@ -219,6 +219,11 @@ struct vcg_graph {
   std::vector<int32_t> own_nbr;
   DevBuf d_off{true};  // int32[n+1]
   DevBuf d_nbr{true};  // int32[2m]
+  // a root reduction's output graph: the forced ids of the reduction that
+  // made it, kept on the device when the caller did not ask for them
+  // (vcg_graph_forced downloads them on demand)
+  DevBuf d_forced{true};
+  int64_t nforced = -1;
   void adopt_owned() {
     hoff = own_off.data();
     hnbr = own_nbr.data();
@@ -931,6 +936,18 @@ __global__ void k_flags_from_deg(const uint32_t* deg, int n, int32_t* flag) {
 
 static constexpr int kSpecFailed = 1000;  // internal: speculation refuted, rerun
 
+// the reduction's forced ids stay with its output graph when the caller did
+// not take them (forced_out == NULL)
+static void attach_forced(vcg_graph* red, DevBuf& facc, int64_t count, const int32_t* forced_out) {
+  if (forced_out) return;
+  // the device-to-device copies are complete before another host thread
+  // (e.g. the caller of a solve_batch worker) may download them
+  cudaStreamSynchronize(cudaStreamPerThread);
+  red->nforced = count;
+  std::swap(red->d_forced.p, facc.p);
+  std::swap(red->d_forced.bytes, facc.bytes);
+}
+
 static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_bound,
                             int64_t bound, vcg_preprocessed* info, int32_t* forced_out,
                             int64_t* vertex_map_out, vcg_graph** reduced_out, int spec_ok) {
@@ -975,6 +992,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
   std::vector<int64_t> vmap;
   int64_t forced_count = 0;
   bool residual_empty = false;  // the rules left no edge: no compaction needed
+  DevBuf facc{true};            // forced ids on the device (forced_out == NULL)
   bool host_compact = false;
   std::vector<int32_t> host_deg;
   if (!rules_on) {
@@ -1029,7 +1047,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
     std::vector<int32_t> hdeg;  // host copy of the degrees (crown / host compaction)
     int first = 1;
     int pos = 0;
-    int64_t nforced = 0;  // forced ids written to forced_out
+    int64_t nforced = 0;  // forced ids written to forced_out (or to facc)
     static thread_local cudaEvent_t rk0 = nullptr, rk1 = nullptr;
     if (!rk0) {
       CK(cudaEventCreate(&rk0));
@@ -1104,6 +1122,11 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
       first = 0;
       if (ret[7] > 0 && forced_out)  // straight into the caller's buffer
         CK(cudaMemcpy(forced_out + nforced, dout.p, (size_t)ret[7] * 4, cudaMemcpyDeviceToHost));
+      if (ret[7] > 0 && !forced_out) {  // kept on the device for the reduced graph
+        if (!facc.p && facc.ensure((size_t)std::max(n, 1) * 4)) return VCG_ERESOURCE;
+        CK(cudaMemcpyAsync(facc.as<int32_t>() + nforced, dout.p, (size_t)ret[7] * 4,
+                           cudaMemcpyDeviceToDevice, cudaStreamPerThread));
+      }
       nforced += ret[7];
       info->rule_counts[0] += ret[1];
       info->rule_counts[1] += ret[2];
@@ -1128,7 +1151,13 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
         crown_applied_last = nh > 0;
         if (nh > 0) {
           info->rule_counts[3] += 1;
-          if (forced_out) std::copy(heads.begin(), heads.end(), forced_out + nforced);
+          if (forced_out) {
+            std::copy(heads.begin(), heads.end(), forced_out + nforced);
+          } else if (!heads.empty()) {
+            if (!facc.p && facc.ensure((size_t)std::max(n, 1) * 4)) return VCG_ERESOURCE;
+            CK(cudaMemcpy(facc.as<int32_t>() + nforced, heads.data(), heads.size() * 4,
+                          cudaMemcpyHostToDevice));
+          }
           nforced += (int64_t)heads.size();
           forced_count += nh;
           progressed += nh;
@@ -1216,6 +1245,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
     info->greedy_original = -1;
     if (vertex_map_out)
       for (size_t i = 0; i < vmap.size(); ++i) vertex_map_out[i] = vmap[i];
+    attach_forced(red, facc, forced_count, forced_out);
     *reduced_out = red;
     return 0;
   }
@@ -1229,7 +1259,17 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
     }
   if (vertex_map_out)
     for (size_t i = 0; i < vmap.size(); ++i) vertex_map_out[i] = vmap[i];
+  attach_forced(red, facc, forced_count, forced_out);
   *reduced_out = red;
+  return 0;
+}
+
+extern "C" int vcg_graph_forced(const vcg_graph* reduced, int32_t* out, int64_t* count) {
+  if (!reduced || !count) return fail(VCG_EINVAL, "bad arguments");
+  if (reduced->nforced < 0) return fail(VCG_EINVAL, "not a root reduction's graph");
+  *count = reduced->nforced;
+  if (out && reduced->nforced > 0)
+    CK(cudaMemcpy(out, reduced->d_forced.p, (size_t)reduced->nforced * 4, cudaMemcpyDeviceToHost));
   return 0;
 }
 

@@ -362,7 +362,7 @@ def _solve(g: StaticGraph, cfg: SolverConfig, lazy: bool):
     bound = cfg.k if cfg.mode == "pvc" else None
     pre = root_reduce(g, enabled=cfg.use_root_reduce, crown=cfg.use_crown, bound=bound,
                       width_override=cfg.width, need_greedy_original=bound is None,
-                      ordered=False, lazy_greedy=lazy)
+                      ordered=False, lazy_greedy=lazy, lazy_forced=True)
     stats.phase_seconds["root_reduce"] = time.perf_counter() - t0
     for key, val in pre.rule_counts.items():
         stats.rule_counts[key] = stats.rule_counts.get(key, 0) + val

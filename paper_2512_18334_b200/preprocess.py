@@ -47,13 +47,60 @@ def select_width(max_degree: int, override: int | None = None) -> int:
     raise ValueError(f"max degree {max_degree} exceeds every supported width")
 
 
+class LazyForced:
+    """The root reduction's forced ids, left on the device with the reduced
+    graph (vcg_graph_forced) and downloaded on first use: the solve path
+    only needs their count.  Behaves like the int32 array it stands for."""
+
+    def __init__(self, graph: StaticGraph, count: int):
+        self._graph = graph
+        self._count = count
+        self._arr = None
+
+    def _get(self) -> np.ndarray:
+        if self._arr is None:
+            out = np.empty(max(self._count, 1), dtype=np.int32)
+            cnt = C.c_int64()
+            _lib.check(_lib.lib.vcg_graph_forced(self._graph.device().handle, out.ctypes.data,
+                                                 C.byref(cnt)))
+            self._arr = out[: cnt.value]
+        return self._arr
+
+    def __len__(self) -> int:
+        return self._count
+
+    def __array__(self, dtype=None, copy=None):
+        a = self._get()
+        return a if dtype is None else a.astype(dtype)
+
+    def __getitem__(self, i):
+        return self._get()[i]
+
+    def __iter__(self):
+        return iter(self._get())
+
+    def tolist(self) -> list:
+        return self._get().tolist()
+
+    @property
+    def dtype(self):
+        return np.dtype(np.int32)
+
+    @property
+    def shape(self):
+        return (self._count,)
+
+    def __repr__(self) -> str:
+        return f"LazyForced({self._count} ids on the device)"
+
+
 @dataclass
 class Preprocessed:
     """preprocess.py:61 -- result of the root reduction pass."""
 
     graph: StaticGraph
     vertex_map: np.ndarray  # reduced id -> original id
-    forced_ids: np.ndarray  # int32, original ids forced into the cover
+    forced_ids: np.ndarray  # int32, original ids forced into the cover (or LazyForced)
     greedy_original: int
     greedy_reduced: int
     width: int
@@ -83,7 +130,8 @@ class Preprocessed:
 def root_reduce(g: StaticGraph, enabled: bool = True, crown: bool = True,
                 bound: int | None = None, width_override: int | None = None,
                 need_greedy_original: bool = True, ordered: bool = True,
-                lazy_greedy: bool = False, speculate: bool = True) -> Preprocessed:
+                lazy_greedy: bool = False, speculate: bool = True,
+                lazy_forced: bool = False) -> Preprocessed:
     """preprocess.py:77 root_reduce on the device.
 
     ``need_greedy_original=False`` (used by PVC solves, where the bound is k)
@@ -95,10 +143,12 @@ def root_reduce(g: StaticGraph, enabled: bool = True, crown: bool = True,
     input: ``greedy_original`` is then -1, the search starts from
     ``greedy_reduced`` (achieved) and ``spec_need`` says which greedy value
     the speculative reduction assumed (solve() certifies it against the
-    optimum).  ``speculate=False`` runs the rules with the real bound."""
+    optimum).  ``speculate=False`` runs the rules with the real bound.
+    ``lazy_forced=True`` (the solve path) leaves the forced ids on the device
+    until first use (``forced_ids`` is then a LazyForced)."""
     n = g.num_vertices
     info = _lib.Preprocessed_t()
-    forced = np.empty(max(n, 1), dtype=np.int32)  # written by the library
+    forced = None if lazy_forced else np.empty(max(n, 1), dtype=np.int32)  # written by the library
     vmap = np.empty(max(n, 1), dtype=np.int64)
     h = C.c_void_p()
     _lib.check(_lib.lib.vcg_root_reduce(
@@ -106,14 +156,16 @@ def root_reduce(g: StaticGraph, enabled: bool = True, crown: bool = True,
         (1 if enabled else 0) | (0 if ordered else 2) | (4 if lazy_greedy else 0)
         | (0 if speculate else 8), int(crown),
         0 if bound is None else (2 if need_greedy_original else 1),
-        int(bound) if bound is not None else 0, C.byref(info), forced.ctypes.data,
-        vmap.ctypes.data, C.byref(h)))
+        int(bound) if bound is not None else 0, C.byref(info),
+        None if forced is None else forced.ctypes.data, vmap.ctypes.data, C.byref(h)))
     reduced = StaticGraph.from_device(DeviceGraph(h.value))
+    forced_ids = (LazyForced(reduced, int(info.forced_count)) if forced is None
+                  else forced[: info.forced_count])
     md = int(info.max_degree_reduced)
     return Preprocessed(
         graph=reduced,
         vertex_map=vmap[: info.n_reduced].copy(),
-        forced_ids=forced[: info.forced_count],
+        forced_ids=forced_ids,
         greedy_original=int(info.greedy_original),
         greedy_reduced=int(info.greedy_reduced),
         width=select_width(md, width_override),
