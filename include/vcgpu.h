@@ -19,6 +19,8 @@
  *   vcg_search                             <- engine.py:160 _Engine.run (the
  *                                            threaded search behind solve(),
  *                                            engine.py:561)
+ *   vcg_crown_reduce                       <- reductions.py:263 crown_reduce
+ *                                            (one crown on a node's degrees)
  *   vcg_node_op                            <- kernels/__init__.py:33-44, the
  *                                            per-node kernel API (pure.py /
  *                                            _native.pyx), one node per call
@@ -68,6 +70,19 @@ int vcg_induced_subgraph(const vcg_graph* g, const int64_t* keep, int64_t nkeep,
 /* Max-degree greedy cover (lowest index on ties).  members may be NULL,
  * else receives the picks in order (capacity n). */
 int vcg_greedy_bound(const vcg_graph* g, int32_t* members, int64_t* size);
+
+/* One crown reduction (reductions.py:263 crown_reduce) on the live window
+ * [lo, hi] of a node's degree array deg (uint32[n], updated in place: the
+ * heads are removed).  heads (capacity n) receives the forced heads in
+ * increasing order, indep (capacity n, may be NULL) the crown's independent
+ * side in increasing order; *edges_removed the edges the heads took.  Both
+ * counts are 0 when no crown exists.  Host C++ -- the same routine
+ * vcg_root_reduce runs between its device fixpoint passes (a maximum
+ * bipartite matching is a sequential augmenting-path search on a residual
+ * that the device rules have already shrunk). */
+int vcg_crown_reduce(int64_t n, const int64_t* offsets, const int32_t* neighbors, uint32_t* deg,
+                     int64_t lo, int64_t hi, int32_t* heads, int64_t* nheads, int32_t* indep,
+                     int64_t* nindep, int64_t* edges_removed);
 
 typedef struct {
   int64_t n_reduced;

@@ -85,6 +85,7 @@ EXPORTS = (
     "vcg_exchange_create", "vcg_exchange_destroy", "vcg_exchange_reset", "vcg_exchange_post",
     "vcg_exchange_peek", "vcg_peer_create", "vcg_peer_handle", "vcg_peer_open",
     "vcg_peer_destroy", "vcg_peer_offer", "vcg_peer_read", "vcg_graph_forced",
+    "vcg_crown_reduce",
 )
 
 
@@ -122,6 +123,8 @@ def _load():
     lib.vcg_expand.argtypes = [P, C.POINTER(ExpandConfig_t), C.POINTER(ExpandResult_t), P, P, I64]
     lib.vcg_node_op.argtypes = [C.c_int, C.c_int, I64, P, P, P, I64, I64, I64, I64, P, I64, P]
     lib.vcg_brute_force_mvc.argtypes = [I64, P, P, C.POINTER(I64), P]
+    lib.vcg_crown_reduce.argtypes = [I64, P, P, P, I64, I64, P, C.POINTER(I64), P,
+                                     C.POINTER(I64), C.POINTER(I64)]
     lib.vcg_exchange_create.argtypes = [C.POINTER(P)]
     lib.vcg_exchange_destroy.argtypes = [P]
     lib.vcg_exchange_reset.argtypes = [P]

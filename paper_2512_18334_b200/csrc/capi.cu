@@ -528,6 +528,33 @@ extern "C" int vcg_greedy_bound(const vcg_graph* g, int32_t* members, int64_t* s
   return 0;
 }
 
+extern "C" int vcg_crown_reduce(int64_t n, const int64_t* offsets, const int32_t* neighbors,
+                                uint32_t* deg, int64_t lo, int64_t hi, int32_t* heads,
+                                int64_t* nheads, int32_t* indep, int64_t* nindep,
+                                int64_t* edges_removed) {
+  if (n < 0 || !offsets || !deg || !heads || !nheads || !edges_removed ||
+      (n > 0 && offsets[n] > 0 && !neighbors))
+    return fail(VCG_EINVAL, "bad arguments");
+  if (n > INT32_MAX) return fail(VCG_EINVAL, "more than 2^31-1 vertices");
+  lo = std::max<int64_t>(lo, 0);
+  hi = std::min<int64_t>(hi, n - 1);
+  std::vector<int32_t> d(n);
+  for (int64_t v = 0; v < n; ++v) {
+    if (deg[v] > (uint32_t)INT32_MAX) return fail(VCG_EINVAL, "degree out of range");
+    d[v] = (int32_t)deg[v];
+  }
+  std::vector<int32_t> h, crown;
+  int64_t er = 0;
+  crown_reduce_host(n, offsets, neighbors, d.data(), lo, hi, &h, &er, &crown);
+  std::copy(h.begin(), h.end(), heads);
+  if (indep) std::copy(crown.begin(), crown.end(), indep);
+  for (int64_t v = 0; v < n; ++v) deg[v] = (uint32_t)d[v];
+  *nheads = (int64_t)h.size();
+  if (nindep) *nindep = h.empty() ? 0 : (int64_t)crown.size();
+  *edges_removed = er;
+  return 0;
+}
+
 // ------------------------------------------------------- node workspaces --
 
 template <typename T>

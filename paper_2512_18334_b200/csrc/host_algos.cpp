@@ -155,8 +155,9 @@ bool try_augment(int32_t root, const std::vector<std::vector<int32_t>>& adj,
 // reductions.py:263 crown_reduce on a host degree array (int32, in/out).
 int64_t crown_reduce_host(int64_t n, const int64_t* off, const int32_t* nbr, int32_t* deg,
                           int64_t lo, int64_t hi, std::vector<int32_t>* heads_out,
-                          int64_t* edges_removed) {
+                          int64_t* edges_removed, std::vector<int32_t>* crown_out) {
   heads_out->clear();
+  if (crown_out) crown_out->clear();
   *edges_removed = 0;
   if (lo > hi) return 0;
   std::vector<int32_t> live;
@@ -266,6 +267,10 @@ int64_t crown_reduce_host(int64_t n, const int64_t* off, const int32_t* nbr, int
   }
   *heads_out = heads;
   *edges_removed = er;
+  if (crown_out) {
+    std::sort(crown.begin(), crown.end());
+    *crown_out = std::move(crown);
+  }
   return (int64_t)heads.size();
 }
 
