@@ -25,6 +25,9 @@
  *                                            per-node kernel API (pure.py /
  *                                            _native.pyx), one node per call
  *   vcg_brute_force_mvc                    <- oracle.py:28 brute_force_mvc
+ *   vcg_registry_*                         <- registry.py:79-224 Registry (the
+ *                                            search's device registry protocol,
+ *                                            one operation per call or per thread)
  */
 #ifndef VCGPU_H
 #define VCGPU_H
@@ -343,6 +346,48 @@ int vcg_get_device(void);
  * thread-local destructors while the runtimes unload.  No reference
  * counterpart (the reference holds no device state). */
 void vcg_shutdown(void);
+
+/* ------------------------------------------------ registry protocol --
+ * registry.py:79-224 Registry as a device object: the search kernel's
+ * registry arena (12 int32 fields per entry, the vcg_search registry_out row
+ * layout) and its atomic encodings, one protocol operation per call.
+ * Operations (a, b, c are the reference's arguments in order):
+ *   NEW_CHILD        a = best_init (>= 1), b = parent (-1: none), c = achieved -> index
+ *   NEW_PARENT       a = initial_sum (>= 0), b = ancestor                    -> index
+ *   ATOMIC_MIN_BEST  a = candidate, b = achieved                    -> prior best
+ *   BEST_SNAPSHOT                                   -> ret[0] best, ret[1] achieved
+ *   INC/DEC_LIVE_NODES, INC/DEC_LIVE_COMPS                          -> new count
+ *   ADD_TO_SUM       a = delta, b = achieved, c = folded            -> new sum
+ *   MARK_DISCOVERY_DONE
+ * Protocol violations return VCG_EPROTOCOL (registry.py:20
+ * RegistryProtocolError): an increment on a finished entry is refused, a
+ * decrement below zero stays applied. */
+#define VCG_REG_NEW_CHILD 0
+#define VCG_REG_NEW_PARENT 1
+#define VCG_REG_ATOMIC_MIN_BEST 2
+#define VCG_REG_BEST_SNAPSHOT 3
+#define VCG_REG_INC_LIVE_NODES 4
+#define VCG_REG_DEC_LIVE_NODES 5
+#define VCG_REG_ADD_TO_SUM 6
+#define VCG_REG_INC_LIVE_COMPS 7
+#define VCG_REG_DEC_LIVE_COMPS 8
+#define VCG_REG_MARK_DISCOVERY_DONE 9
+
+typedef struct vcg_registry vcg_registry;
+int vcg_registry_create(int64_t capacity, vcg_registry** out);
+int vcg_registry_destroy(vcg_registry* r);
+int64_t vcg_registry_size(const vcg_registry* r);
+int vcg_registry_op(vcg_registry* r, int op, int64_t idx, int64_t a, int64_t b, int64_t c,
+                    int64_t* ret /* [2] */);
+/* count device threads at once: thread i runs `rounds` passes of
+ * ops[0..nops) (nops <= 8, operations on existing entries) on entry idx[i]
+ * with (a[i], b[i]) (a / b may be NULL: 0); ret[i] = its last result;
+ * *protocol_error = the first violation code seen (0: none). */
+int vcg_registry_concurrent(vcg_registry* r, const int* ops, int nops, int rounds,
+                            const int64_t* idx, const int64_t* a, const int64_t* b,
+                            int64_t count, int64_t* ret, int* protocol_error);
+/* entries [0, *count) as 12-int32 rows (rows may be NULL to read the count) */
+int vcg_registry_download(const vcg_registry* r, int32_t* rows, int64_t cap, int64_t* count);
 
 #ifdef __cplusplus
 }

@@ -85,7 +85,8 @@ EXPORTS = (
     "vcg_exchange_create", "vcg_exchange_destroy", "vcg_exchange_reset", "vcg_exchange_post",
     "vcg_exchange_peek", "vcg_peer_create", "vcg_peer_handle", "vcg_peer_open",
     "vcg_peer_destroy", "vcg_peer_offer", "vcg_peer_read", "vcg_graph_forced",
-    "vcg_crown_reduce",
+    "vcg_crown_reduce", "vcg_registry_create", "vcg_registry_destroy", "vcg_registry_size",
+    "vcg_registry_op", "vcg_registry_concurrent", "vcg_registry_download",
 )
 
 
@@ -123,6 +124,13 @@ def _load():
     lib.vcg_expand.argtypes = [P, C.POINTER(ExpandConfig_t), C.POINTER(ExpandResult_t), P, P, I64]
     lib.vcg_node_op.argtypes = [C.c_int, C.c_int, I64, P, P, P, I64, I64, I64, I64, P, I64, P]
     lib.vcg_brute_force_mvc.argtypes = [I64, P, P, C.POINTER(I64), P]
+    lib.vcg_registry_create.argtypes = [I64, C.POINTER(P)]
+    lib.vcg_registry_destroy.argtypes = [P]
+    lib.vcg_registry_size.argtypes = [P]
+    lib.vcg_registry_size.restype = I64
+    lib.vcg_registry_op.argtypes = [P, C.c_int, I64, I64, I64, I64, P]
+    lib.vcg_registry_concurrent.argtypes = [P, P, C.c_int, C.c_int, P, P, P, I64, P, P]
+    lib.vcg_registry_download.argtypes = [P, P, I64, C.POINTER(I64)]
     lib.vcg_crown_reduce.argtypes = [I64, P, P, P, I64, I64, P, C.POINTER(I64), P,
                                      C.POINTER(I64), C.POINTER(I64)]
     lib.vcg_exchange_create.argtypes = [C.POINTER(P)]

@@ -26,6 +26,7 @@ import numpy as np
 from . import _lib
 from .graph import StaticGraph
 from .preprocess import Preprocessed, greedy_bound, root_reduce
+from .registry import ChildEntry, ParentEntry, Registry  # noqa: F401  (re-exported)
 
 RULE_KEYS = (
     "degree_one",
@@ -116,95 +117,6 @@ class Stats:
         }
 
 
-@dataclass
-class ChildEntry:
-    """registry.py:24 ChildEntry, as read back from the device registry."""
-
-    best: int
-    achieved: bool
-    live_nodes: int
-    parent: int | None
-
-
-@dataclass
-class ParentEntry:
-    """registry.py:43 ParentEntry, as read back from the device registry."""
-
-    sum: int
-    sum_achieved: bool
-    live_comps: int
-    ancestor: int
-    initial_sum: int
-    folded_total: int
-    children: list[int]
-    discovery_done: bool
-
-
-class Registry:
-    """Post-solve view of the device branch registry (registry.py:79-224):
-    ``entries`` in allocation order, ``entry(idx)``, and the reference's
-    per-entry quiescence / conservation diagnostics.
-
-    The entries are copied back from HBM when the solve asked for them
-    (``check_registry=True`` or ``deterministic=True``); otherwise only the
-    entry count is known and the entry accessors raise."""
-
-    def __init__(self, count: int, raw: np.ndarray | None = None):
-        self.count = count
-        self.entries: list | None = None
-        if raw is not None:
-            self.entries = [self._decode(raw[i]) for i in range(count)]
-
-    @staticmethod
-    def _decode(f) -> ChildEntry | ParentEntry:
-        key, live, link, kind = int(f[0]), int(f[1]), int(f[2]), int(f[3])
-        if kind == 0:
-            return ChildEntry(best=key >> 1, achieved=not (key & 1), live_nodes=live,
-                              parent=None if link < 0 else link)
-        return ParentEntry(sum=int(f[4]), sum_achieved=bool(f[5]), live_comps=live,
-                           ancestor=link, initial_sum=int(f[6]), folded_total=int(f[7]),
-                           children=list(range(int(f[8]), int(f[8]) + int(f[9]))),
-                           discovery_done=bool(f[10]))
-
-    def __len__(self) -> int:
-        return self.count
-
-    def _need(self):
-        if self.entries is None:
-            raise RuntimeError("solve with check_registry=True (or deterministic=True) to read "
-                               "the registry entries back from the device")
-        return self.entries
-
-    def entry(self, idx: int):
-        return self._need()[idx]
-
-    def quiescence_violations(self) -> list[str]:
-        """registry.py:198 -- entries still holding live counts."""
-        out = []
-        for i, e in enumerate(self._need()):
-            if isinstance(e, ChildEntry):
-                if e.live_nodes != 0:
-                    out.append(f"child entry {i}: live_nodes == {e.live_nodes}")
-            elif e.live_comps != 0:
-                out.append(f"parent entry {i}: live_comps == {e.live_comps}")
-        return out
-
-    def conservation_violations(self) -> list[str]:
-        """registry.py:211 -- parents whose sum disagrees with initial +
-        folded + children bests."""
-        entries = self._need()
-        out = []
-        for i, e in enumerate(entries):
-            if isinstance(e, ParentEntry):
-                kids = [entries[c].best for c in e.children]
-                expected = e.initial_sum + e.folded_total + sum(kids)
-                if e.sum != expected:
-                    out.append(f"parent entry {i}: sum {e.sum} != {expected} "
-                               f"(initial {e.initial_sum} + folded {e.folded_total} "
-                               f"+ children {kids})")
-        return out
-
-
 RegistrySummary = Registry  # round-1 name
 
 
@@ -291,8 +203,8 @@ def run_search(rg: StaticGraph, cfg: SolverConfig, width: int, best_init: int,
     h = {int(i): int(c) for i, c in enumerate(hist) if c}
     local = cover[: res.cover_size].tolist() if record and res.cover_size >= 0 else None
     count = int(res.registry_entries)
-    res.registry_view = Registry(count, reg_raw if reg_raw is not None and count <= len(reg_raw)
-                                 else None)
+    res.registry_view = Registry.snapshot(
+        count, reg_raw if reg_raw is not None and count <= len(reg_raw) else None)
     return res, h, local
 
 

@@ -66,3 +66,11 @@ def test_gpu_share_and_batch_validation():
     with pytest.raises(ValueError):
         vc.solve_batch([g, g], [vc.SolverConfig()])  # one graph per config
     assert vc.solve_batch(g, []) == []
+
+
+def test_registry_object_needs_a_device():
+    from paper_2512_18334_b200 import _lib
+    from paper_2512_18334_b200.registry import Registry
+
+    with pytest.raises(_lib.GpuError):
+        Registry()
