@@ -223,3 +223,40 @@ def test_reductions_match_reference_golden():
         assert (node.solution_size, node.edges_remaining, node.lo, node.hi) == (
             st["solution_size"], st["edges_remaining"], st["lo"], st["hi"])
         assert [int(v) for v in np.flatnonzero(node.inclusion)] == st["inclusion"]
+
+
+def test_search_node_mirror():
+    """test_graph.py:91-153, the SearchNode half, on the device node ops."""
+    from paper_2512_18334_b200.graph import (SearchNode, recompute_node_bounds,
+                                             remove_neighbors, remove_vertex)
+
+    g = make_graph(4, path_edges(4))
+    node = SearchNode.for_graph(g, 8)
+    assert (node.solution_size, node.edges_remaining, node.lo, node.hi) == (0, 3, 0, 3)
+    assert node.inclusion is None and node.live_count() == 4
+    node = SearchNode.for_graph(g, 8, track_inclusion=True)
+    clone = node.copy()
+    assert remove_vertex(node, g, 1, into_cover=True) == 2
+    assert (node.edges_remaining, node.solution_size) == (1, 1)
+    assert node.degrees.tolist() == [0, 0, 1, 1]
+    assert node.inclusion.tolist() == [False, True, False, False]
+    assert remove_vertex(node, g, 0, into_cover=True) == 0 and node.solution_size == 2
+    assert (clone.solution_size, clone.edges_remaining) == (0, 3)
+    assert clone.degrees.tolist() == [1, 2, 2, 1] and not clone.inclusion.any()
+    g = make_graph(5, clique_edges(5))
+    node = SearchNode.for_graph(g, 8, track_inclusion=True)
+    out = np.zeros(16, dtype=np.int32)
+    removed, pos = remove_neighbors(node, g, 0, out, 0)
+    assert removed == 4 and sorted(out[:pos].tolist()) == [1, 2, 3, 4]
+    assert (node.solution_size, node.edges_remaining) == (4, 0)
+    assert node.inclusion.tolist() == [False, True, True, True, True]
+    g = make_graph(5, path_edges(5))
+    node = SearchNode.for_graph(g, 8)
+    remove_vertex(node, g, 0, into_cover=False)
+    remove_vertex(node, g, 1, into_cover=True)
+    recompute_node_bounds(node)
+    assert (node.lo, node.hi) == (2, 4)
+    for v in (2, 3, 4):
+        remove_vertex(node, g, v, into_cover=False)
+    recompute_node_bounds(node)
+    assert node.lo > node.hi and node.live_count() == 0
