@@ -1893,6 +1893,9 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   res->trace[5] = (int64_t)ctl.wc_fix;
   res->trace[6] = (int64_t)ctl.wc_comp;
   res->trace[7] = (int64_t)ctl.wc_split;
+#ifdef VCG_WARP_PROFILE
+  res->trace[3] = (int64_t)ctl.wc_iter;  // profile builds: fixpoint iterations in place of max nodes
+#endif
   res->kernel_t0_ns = (int64_t)ctl.t0;
   res->kernel_t1_ns = (int64_t)ctl.t_end;
 

@@ -37,6 +37,21 @@ namespace vcg {
 // per-phase cycle counters of warp tasks (SolveResult.phase_cycles
 // warp_*_cycles): build with -DVCG_WARP_PROFILE; off by default, the
 // counters live in local memory on the hot path
+// idle warps poll the task ring with exponential backoff (ns)
+#ifndef VCG_EPOCH_STICKY
+#define VCG_EPOCH_STICKY 1
+#endif
+#ifndef VCG_WBACKOFF_MIN
+#define VCG_WBACKOFF_MIN 64
+#endif
+#ifndef VCG_WBACKOFF_MAX
+#define VCG_WBACKOFF_MAX 2048
+#endif
+#ifdef VCG_TASK_TRACE  // per-task printf of the slow tasks (diagnostic builds)
+#define TTRACE(...) __VA_ARGS__
+#else
+#define TTRACE(...)
+#endif
 #ifdef VCG_WARP_PROFILE
 #define WPROF(...) __VA_ARGS__
 #else
@@ -99,6 +114,8 @@ struct WStats {
   unsigned long long c_fix, c_comp, c_split;  // cycles in the node phases
   unsigned long long c_iter;                   // fixpoint loop iterations
   unsigned long long rules[6];
+  unsigned long long t_exp, t_rsplit, t_wait, t_rfail;  // VCG_TASK_TRACE, per task
+  unsigned long long t_ph[5];                           // split phases (VCG_TASK_TRACE)
 };
 
 // ------------------------------------------------------------ masks --
@@ -540,7 +557,8 @@ __device__ inline void warp_emit_component(const SearchParams& P, const WS& ws, 
 template <typename M, typename WS>
 __device__ inline bool warp_registry_split(const SearchParams& P, WS& ws, const WTaskHdr& th,
                                            int pbase, int ng, int S_abs, int special,
-                                           int best_abs) {
+                                           int best_abs, WStats& st) {
+  TTRACE(long long tq = clock64());
   constexpr int K = WS::kW;
   const int lane = threadIdx.x & 31;
   const Registry& R = P.reg;
@@ -567,6 +585,7 @@ __device__ inline bool warp_registry_split(const SearchParams& P, WS& ws, const 
   pos = __shfl_sync(0xffffffffu, pos, 0);
   if (p == -2) return false;
   if (p < 0) return true;  // registry exhausted: the search stops
+  TTRACE(st.t_ph[0] += clock64() - tq; tq = clock64());
   if (lane == 0) {
     atomicAdd(&R.live[th.scope], 1);  // the parent entry's reference on the scope
     R.kind[p] = 1;
@@ -596,11 +615,14 @@ __device__ inline bool warp_registry_split(const SearchParams& P, WS& ws, const 
     __threadfence();
   }
   __syncwarp();
+  TTRACE(st.t_ph[1] += clock64() - tq; tq = clock64());
   for (int j = 0; j < ng; ++j) {
     if (lane == 0) q_wait_free(P.bq, pos + j);
     __syncwarp();
+    TTRACE(st.t_ph[2] += clock64() - tq; tq = clock64());
     warp_emit_component<M, WS>(P, ws, wload<M>(&ws.pend[K * (pbase + j)]), p + 1 + j,
                                th.depth + 1, pos + j);
+    TTRACE(st.t_ph[3] += clock64() - tq; tq = clock64());
   }
   if (lane == 0) {
     __threadfence();
@@ -608,6 +630,7 @@ __device__ inline bool warp_registry_split(const SearchParams& P, WS& ws, const 
     if (atomicSub(&R.live[p], 1) == 1) reg_cascade(P, p);
   }
   __syncwarp();
+  TTRACE(st.t_ph[4] += clock64() - tq);
   return true;
 }
 
@@ -728,7 +751,10 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WS& ws, const WTas
       const int top0 = nf > 1 ? ws.fr[1].base : sp;
       if (__shfl_sync(0xffffffffu, shed, 0) && top0 > ws.fr[0].base) {
         const int b = ws.fr[0].base;
-        if (warp_export(P, ws, th, n, &ws.stL[K * b], ws.stS[b])) ws.fr[0].base = b + 1;
+        if (warp_export(P, ws, th, n, &ws.stL[K * b], ws.stS[b])) {
+          ws.fr[0].base = b + 1;
+          TTRACE(++st.t_exp);
+        }
       }
     }
     if (skip_count) skip_count = false;
@@ -809,9 +835,15 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WS& ws, const WTas
         continue;
       }
       if constexpr (K > 1) {  // wide-task variants only
-        if (f == 0 && n > 64 && !overflow && P.warp_split_export &&
-            warp_registry_split<M, WS>(P, ws, th, pbase, ng, th.S + S, special, th.S + F.best))
-          continue;  // the components run as tasks of their own
+        if (f == 0 && n > 64 && !overflow && P.warp_split_export) {
+          TTRACE(const long long tw0 = clock64());
+          const bool ok =
+              warp_registry_split<M, WS>(P, ws, th, pbase, ng, th.S + S, special, th.S + F.best,
+                                       st);
+          TTRACE(st.t_wait += (unsigned long long)(clock64() - tw0); if (ok) ++st.t_rsplit;
+                 else ++st.t_rfail);
+          if (ok) continue;  // the components run as tasks of their own
+        }
       }
       if (overflow || nf >= kWFrames) {
         if (lane == 0) {
@@ -884,16 +916,17 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WS& ws, const WTas
 
 // One warp-tier epoch of a block (all threads call it, block-uniformly).
 // Every warp takes tasks from the ring and solves them; a warp leaves once
-// the ring is empty and no warp of its block is still busy (new tasks can
-// only come from busy blocks), or as soon as node-level work is queued (the
-// block is needed there), or on stop.  Returns whether the block ran a task.
+// no warp of its block is still busy and either the ring is empty (new tasks
+// can only come from busy blocks) or node-level work is queued (the block is
+// needed there), or on stop.  Returns whether the block ran a task.
 template <int WW>
 __device__ inline bool warp_epoch(const SearchParams& P, void* wws_raw, int* busy, WStats& st) {
   using WS = WarpWsT<WW>;
+  constexpr bool kSticky = VCG_EPOCH_STICKY && WW > 1;
   const int lane = threadIdx.x & 31;
   WS& ws = ((WS*)wws_raw)[threadIdx.x >> 5];
   bool any = false;
-  unsigned backoff = 64;
+  unsigned backoff = VCG_WBACKOFF_MIN;
   unsigned polls = 0;
   while (true) {
     long long pos = -1;
@@ -904,7 +937,13 @@ __device__ inline bool warp_epoch(const SearchParams& P, void* wws_raw, int* bus
       if ((P.xch || P.gpeer) && (polls++ & 7) == 0) xch_poll(P);
       stop = ld_relaxed(&P.ctl->stop);
       node_work = (long long)ld_relaxed_u64(P.q.count) > 0;
-      if (!stop && !node_work) {
+      // node-level work needs every warp of the block: while a sibling is
+      // still inside a wide task (long: up to thousands of nodes) the block
+      // cannot take it, so an idle warp keeps taking tasks instead of
+      // waiting at the block barrier for that sibling (G(180, 0.08): 386 ->
+      // 531 M nodes/s).  With 64-vertex tasks the sibling is done soon and
+      // the block is better off returning to the node queue.
+      if (!stop && (!node_work || (kSticky && *(volatile int*)busy > 0))) {
         pos = q_reserve_pop(P.bq);
         if (pos >= 0) atomicAdd(busy, 1);
       }
@@ -917,13 +956,13 @@ __device__ inline bool warp_epoch(const SearchParams& P, void* wws_raw, int* bus
       int b = 0;
       if (lane == 0) b = *(volatile int*)busy;
       b = __shfl_sync(0xffffffffu, b, 0);
-      if (node_work || b == 0) break;
+      if (b == 0 || (node_work && !kSticky)) break;
       if (lane == 0) __nanosleep(backoff);
-      backoff = backoff < 2048 ? backoff * 2 : 2048;
+      backoff = backoff < VCG_WBACKOFF_MAX ? backoff * 2 : VCG_WBACKOFF_MAX;
       __syncwarp();
       continue;
     }
-    backoff = 64;
+    backoff = VCG_WBACKOFF_MIN;
     any = true;
     const char* slot = P.bq.data + (pos % P.bq.cap) * P.bq_slot;
     const int4 h = __ldcg((const int4*)slot);
@@ -964,6 +1003,13 @@ __device__ inline bool warp_epoch(const SearchParams& P, void* wws_raw, int* bus
       atomicSub(busy, 1);
     }
     const unsigned long long dt = (unsigned long long)(clock64() - t0);
+    TTRACE(if (lane == 0 && dt > 400000ull)
+             printf("task n=%d depth=%d nodes=%llu cycles=%llu exports=%llu rsplits=%llu "
+                    "rfail=%llu split_cycles=%llu f0best=%d ph=%llu/%llu/%llu/%llu/%llu\n", n,
+                    th.depth, st.nodes - nodes0, dt, st.t_exp, st.t_rsplit, st.t_rfail, st.t_wait,
+                    ws.fr[0].best, st.t_ph[0], st.t_ph[1], st.t_ph[2], st.t_ph[3], st.t_ph[4]);
+           st.t_exp = st.t_rsplit = st.t_wait = st.t_rfail = 0;
+           for (int i = 0; i < 5; ++i) st.t_ph[i] = 0);
     st.tasks += 1;
     st.cyc += dt;
     if (dt > st.maxcyc) {

@@ -1,4 +1,5 @@
-"""Per-warp-node cycle split (needs a -DVCG_WARP_PROFILE build): fixpoint,
+"""Per-warp-node cycle split (needs a -DVCG_WARP_PROFILE build, which reports
+the fixpoint iterations in place of warp_task_max_nodes): fixpoint,
 component test, splits, rest -- on the strong instance and rgg2000."""
 import os
 import sys
@@ -19,4 +20,4 @@ for name, gen, cfg in (("gnp180_0.08", lambda: synth.gnp(180, 0.08, 1), vc.Solve
     print(f"{name}: warp nodes {r.warp_nodes}, per node: task {pc['warp_task_cycles']/wn:.0f} cyc = "
           f"fixpoint {pc['warp_fix_cycles']/wn:.0f} + components {pc['warp_comp_cycles']/wn:.0f} + "
           f"splits {pc['warp_split_cycles']/wn:.0f} + rest; fixpoint iterations/node "
-          f"{r.phase_cycles.get('warp_iter', 0)}", flush=True)
+          f"{pc['warp_task_max_nodes'] / wn:.2f}; rules {r.stats.rule_counts}", flush=True)
