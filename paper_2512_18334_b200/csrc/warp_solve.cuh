@@ -266,6 +266,23 @@ __device__ __forceinline__ bool whas(const W256& L, int v) {
   const unsigned long long w = k == 0 ? L.w[0] : k == 1 ? L.w[1] : k == 2 ? L.w[2] : L.w[3];
   return v < 256 && ((w >> (v & 63)) & 1ull);
 }
+// bits [32 j, 32 j + 32) of a mask: the lane-indexed ballot word of the
+// lanes' j-th vertices (j is a compile-time constant in the unrolled loops)
+__device__ __forceinline__ unsigned wchunk(unsigned x, int) { return x; }
+__device__ __forceinline__ unsigned wchunk(unsigned long long x, int j) {
+  return (unsigned)(x >> (32 * j));
+}
+__device__ __forceinline__ unsigned wchunk(W128 x, int j) {
+  return (unsigned)((j < 2 ? x.lo : x.hi) >> (32 * (j & 1)));
+}
+__device__ __forceinline__ unsigned wchunk(const W256& x, int j) {
+  return (unsigned)(x.w[j >> 1] >> (32 * (j & 1)));
+}
+// the lane's own j-th vertex (lane + 32 j) is in x: one shift, no range tests
+template <typename M>
+__device__ __forceinline__ bool wown(const M& x, int j, int lane) {
+  return (wchunk(x, j) >> lane) & 1u;
+}
 // mask from per-lane predicates p[r] on the lane's r-th vertex
 template <typename M>
 __device__ __forceinline__ M wballot(const bool (&p)[WT<M>::R]);
@@ -361,7 +378,7 @@ __device__ __forceinline__ M w_component(const WLane<M>& q, M L, int r) {
     M c{};
 #pragma unroll
     for (int j = 0; j < WT<M>::R; ++j)
-      if (whas(fr, q.v[j])) c |= q.row(j);
+      if (wown(fr, j, q.v[0])) c |= q.row(j);
     fr = wor(c) & L & ~comp;
     comp |= fr;
   }
@@ -376,15 +393,13 @@ template <typename M, typename WS>
 __device__ __forceinline__ int w_fixpoint(const WS& ws, const WLane<M>& q, M& L, int& S,
                                           int best, int (&d)[WT<M>::R], WStats& st) {
   constexpr int R = WT<M>::R;
+  // Isolated vertices stay in L during the loop (no live row contains them,
+  // so no rule sees them) and leave it once, at the fixpoint.
+  bool p[R];
   while (true) {
     WPROF(++st.c_iter);
-    bool p[R];
 #pragma unroll
-    for (int j = 0; j < R; ++j) {
-      d[j] = whas(L, q.v[j]) ? wpopc(q.row(j) & L) : 0;
-      p[j] = d[j] > 0;
-    }
-    L = wballot<M>(p);  // isolated vertices leave the graph
+    for (int j = 0; j < R; ++j) d[j] = wown(L, j, q.v[0]) ? wpopc(q.row(j) & L) : 0;
     const int k = best - S - 1;  // vertices an improving cover may still take
     if (k < 0) return -1;
     // degree one (pure.py:82): the neighbour of a pendant vertex is forced;
@@ -397,8 +412,8 @@ __device__ __forceinline__ int w_fixpoint(const WS& ws, const WLane<M>& q, M& L,
 #pragma unroll
       for (int j = 0; j < R; ++j)
         if (d[j] == 1) {
-          const int u = wlsb(q.row(j) & L);
-          if (!(whas(p1, u) && u < q.v[j])) c |= wbit<M>(u);
+          const M nb = q.row(j) & L;  // the single live neighbour
+          if (!nz(nb & p1) || wlsb(nb) > q.v[j]) c |= nb;
         }
       const M F = wor(c);
       L &= ~F;
@@ -464,6 +479,9 @@ __device__ __forceinline__ int w_fixpoint(const WS& ws, const WLane<M>& q, M& L,
     }
     break;
   }
+#pragma unroll
+  for (int j = 0; j < R; ++j) p[j] = d[j] > 0;
+  L = wballot<M>(p);  // isolated vertices leave the graph
   int sum = 0;
 #pragma unroll
   for (int j = 0; j < R; ++j) sum += d[j];
@@ -794,14 +812,14 @@ __device__ inline bool warp_solve_task(const SearchParams& P, WS& ws, const WTas
         const int size = wpopc(comp);
         bool p[R];
 #pragma unroll
-        for (int j = 0; j < R; ++j) p[j] = whas(comp, q.v[j]) && d[j] != size - 1;
+        for (int j = 0; j < R; ++j) p[j] = wown(comp, j, q.v[0]) && d[j] != size - 1;
         bool cyc = false;
         if (!nz(wballot<M>(p))) {
           special += size - 1;  // clique: all but one vertex
           st.rules[4] += 1;
         } else {
 #pragma unroll
-          for (int j = 0; j < R; ++j) p[j] = whas(comp, q.v[j]) && d[j] != 2;
+          for (int j = 0; j < R; ++j) p[j] = wown(comp, j, q.v[0]) && d[j] != 2;
           cyc = size >= 3 && !nz(wballot<M>(p));
           if (cyc) {
             special += (size + 1) / 2;  // chordless cycle
