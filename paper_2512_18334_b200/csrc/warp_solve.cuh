@@ -403,22 +403,36 @@ __device__ __forceinline__ int w_fixpoint(const WS& ws, const WLane<M>& q, M& L,
     const int k = best - S - 1;  // vertices an improving cover may still take
     if (k < 0) return -1;
     // degree one (pure.py:82): the neighbour of a pendant vertex is forced;
-    // of an isolated edge only the higher end (the in-order sweep's choice)
+    // of an isolated edge only the higher end (the in-order sweep's choice).
+    // High degree (pure.py:158) on the same snapshot: a vertex of degree > k
+    // is in every cover that still improves the bound.  Both at once is
+    // sound -- every improving cover holds H, and the pendant exchange
+    // argument never removes a vertex of H (degree 1 <= k) -- and saves the
+    // rescan between them (the node-level sweeps keep the reference's
+    // order; the warp tier only runs in parallel mode).
 #pragma unroll
     for (int j = 0; j < R; ++j) p[j] = d[j] == 1;
     const M p1 = wballot<M>(p);
-    if (nz(p1)) {
-      M c{};
 #pragma unroll
-      for (int j = 0; j < R; ++j)
-        if (d[j] == 1) {
-          const M nb = q.row(j) & L;  // the single live neighbour
-          if (!nz(nb & p1) || wlsb(nb) > q.v[j]) c |= nb;
-        }
-      const M F = wor(c);
+    for (int j = 0; j < R; ++j) p[j] = d[j] > k;
+    const M H = wballot<M>(p);
+    if (nz(p1 | H)) {
+      M F = H;
+      if (nz(p1)) {
+        M c{};
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+          if (d[j] == 1) {
+            const M nb = q.row(j) & L;  // the single live neighbour
+            if (!nz(nb & p1) || wlsb(nb) > q.v[j]) c |= nb;
+          }
+        F |= wor(c);
+      }
       L &= ~F;
-      S += wpopc(F);
-      st.rules[0] += wpopc(F);
+      const int nf = wpopc(F), nh = wpopc(H);
+      S += nf;
+      st.rules[0] += nf - nh;
+      st.rules[2] += nh;
       continue;
     }
     // degree-two triangle (pure.py:113): in index order with revalidation.
@@ -465,17 +479,6 @@ __device__ __forceinline__ int w_fixpoint(const WS& ws, const WLane<M>& q, M& L,
         st.rules[1] += applied;
         continue;
       }
-    }
-    // high degree (pure.py:158): a vertex of degree > k is in every cover
-    // that still improves the bound
-#pragma unroll
-    for (int j = 0; j < R; ++j) p[j] = d[j] > k;
-    const M H = wballot<M>(p);
-    if (nz(H)) {
-      L &= ~H;
-      S += wpopc(H);
-      st.rules[2] += wpopc(H);
-      continue;
     }
     break;
   }
