@@ -1135,6 +1135,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
                 "us: solo %.1f, grid d1 %.1f, grid tri %.1f, hd %.1f\n",
                 root_front_blocks(), ret[10], ret[11], ret[12], ret[13], ret[14], ret[0],
                 ret[15] * 1e-3, ret[16] * 1e-3, ret[17] * 1e-3, ret[18] * 1e-3);
+      if (use_front && trace_on()) root_front_print_log(X.r_fctl.p);
       if (use_front && trace_on())
         fprintf(stderr, "[vcg root] d1 phases us: A %.1f syncA %.1f B %.1f syncB %.1f C %.1f syncC %.1f\n",
                 ret[19] * 1e-3, ret[22] * 1e-3, ret[20] * 1e-3, ret[23] * 1e-3, ret[21] * 1e-3,
@@ -1736,6 +1737,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   P.bq_slot = bslot;
   P.warp_split_export = !getenv("VCG_NO_WSPLIT");
   P.bq_low = std::max(8LL, (long long)blocks * (threads / 32) / 4);
+  if (const char* e = getenv("VCG_BQLOW")) P.bq_low = atoll(e);  // experiments
   {
     const char* e1 = getenv("VCG_WCHECK");
     const char* e2 = getenv("VCG_WEXPORT");

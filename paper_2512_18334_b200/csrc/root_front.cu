@@ -46,6 +46,7 @@
 // reset pass is needed; removal-set membership is a per-vertex sweep tag.
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "root_grid.cuh"
@@ -55,11 +56,20 @@ namespace vcg {
 
 namespace {
 
+// -DVCG_FRONT_PROF: sub-phase timers of the degree-one sweep (diagnostic
+// builds; they add block barriers)
+#ifdef VCG_FRONT_PROF
+#define FPROF(...) __VA_ARGS__
+#else
+#define FPROF(...)
+#endif
+
 constexpr int kSolo = 0;     // default: frontier size below which block 0 sweeps alone
 constexpr int kChunk = 8;    // adjacency entries per removal work item
 constexpr int kTrack = 12;   // adjacencies longer than this keep live-neighbour id sums
 
 enum Phase { F_D1 = 0, F_TRI = 1, F_HD = 2, F_DONE = 3 };
+constexpr int kLog = 96;
 
 struct St {  // fixpoint state, replicated in every thread (uniform transitions)
   int phase, p1, p2, s, tg;
@@ -74,8 +84,10 @@ struct FrontCtl {
   int err, hd_applied, wlo, whi;  // wlo = max(INT_MAX - lowest live), whi = max(highest live + 1)
   unsigned long long edges, walked, items;
   unsigned bar, nbar;                         // grid_barrier word, barriers passed
-  unsigned long long tph[8];                  // phase times (ns, thread 0): A, B, C, barriers
+  unsigned long long tph[16];                 // phase times (ns, thread 0): A, B, C, barriers, sub-phases
   St st;                                      // block 0 -> grid after a solo segment
+  int nlog;                                   // per-sweep log (trace builds read it)
+  long long slog[kLog][5];                    // phase, end ns, frontier, removed, chunks
   int partial[kRootGridMaxBlocks];
 };
 
@@ -126,7 +138,13 @@ struct Ex {  // executor: the whole grid, or block 0 alone
 };
 
 __device__ __forceinline__ int vld(const int* p) { return *(const volatile int*)p; }
-__device__ __forceinline__ int dget(const uint32_t* d, int v) { return (int)__ldcg(d + v); }
+// Degrees are decremented speculatively (rm_chunk), so a dead vertex's word
+// may have gone below zero: every reader clamps, sweep_hd and the final pass
+// store the zeros back.
+__device__ __forceinline__ int dget(const uint32_t* d, int v) {
+  const int x = (int)__ldcg(d + v);
+  return x > 0 ? x : 0;
+}
 
 __device__ __forceinline__ unsigned long long claim_key(int tg, int v) {
   return ((unsigned long long)(unsigned)tg << 32) | (unsigned long long)(unsigned)(kInf - v);
@@ -235,36 +253,41 @@ __device__ __forceinline__ void live_short(const Front& F, const int* off, const
 
 // one removal work item: the entries [b, min(b + kChunk, end(u))) of removed
 // vertex u.  Non-member live neighbours lose a degree and u from their sums;
-// 2 -> 1 and 3 -> 2 transitions are pushed to the pending lists.
+// 2 -> 1 and 3 -> 2 transitions are pushed to the pending lists.  The degree
+// decrement is issued with the removal-tag load, not after a degree read: a
+// dead neighbour's word goes negative (harmless, readers clamp) and the
+// atomic's old value says whether the neighbour was live -- one dependent
+// round trip less per chunk.  A neighbour in the same removal set is told
+// apart by its tag (its word is zeroed by remove_set either way).
 __device__ __forceinline__ void rm_chunk(const Front& F, FrontCtl* G, BlockQ* q,
                                          const int* nbr, int s, int p1, int p2, int u, int b,
                                          int e, long long* edges) {
   const int len = e - b;
-  int x[kChunk], live[kChunk];
+  int x[kChunk], r[kChunk];
+  unsigned old[kChunk];
+  uint8_t tr[kChunk];
 #pragma unroll
   for (int j = 0; j < kChunk; ++j) x[j] = j < len ? __ldg(nbr + b + j) : -1;
 #pragma unroll
   for (int j = 0; j < kChunk; ++j) {
-    live[j] = 0;
+    r[j] = 0;
+    tr[j] = 0;
+    old[j] = 0;
     if (x[j] >= 0) {
-      const int r = __ldcg(F.rs + x[j]);
-      const int d = dget(F.deg, x[j]);
-      const int tr = __ldg(F.trk + x[j]);
-      if (r == s) {
-        if (x[j] > u) ++*edges;  // both ends removed together: counted once
-      } else if (d > 0) {
-        live[j] = 1 + tr;
-      }
+      r[j] = __ldcg(F.rs + x[j]);
+      tr[j] = __ldg(F.trk + x[j]);
+      old[j] = atomicSub(F.deg + x[j], 1u);
     }
   }
-  unsigned old[kChunk];
   const unsigned long long uu = (unsigned long long)u;
 #pragma unroll
   for (int j = 0; j < kChunk; ++j) {
-    old[j] = 0;
-    if (live[j]) {
-      old[j] = atomicSub(F.deg + x[j], 1u);
-      if (live[j] > 1) {  // tracked neighbour: u leaves its sums
+    if (x[j] < 0) continue;
+    if (r[j] == s) {
+      if (x[j] > u) ++*edges;  // both ends removed together: counted once
+      old[j] = 0;
+    } else if ((int)old[j] > 0) {
+      if (tr[j]) {  // tracked neighbour: u leaves its sums
         atomicAdd(F.nsum + x[j], 0ull - uu);
         atomicAdd(F.nsq + x[j], 0ull - uu * uu);
       }
@@ -278,12 +301,27 @@ __device__ __forceinline__ void rm_chunk(const Front& F, FrontCtl* G, BlockQ* q,
   }
 }
 
+struct Timer {  // thread 0's phase clock
+  unsigned long long t;
+  bool on;
+  __device__ explicit Timer(bool o) : t(o ? globaltimer() : 0), on(o) {}
+  __device__ void lap(FrontCtl* G, int i) {
+    if (on) {
+      const unsigned long long now = globaltimer();
+      G->tph[i] += now - t;
+      t = now;
+    }
+  }
+};
+
 // phase C of a sweep: remove every member of the step's set (rem / chunks);
 // transitions go to the pending lists l1[p1] / l2[p2]
 __device__ __forceinline__ void remove_set(const Ex& E, const Front& F, FrontCtl* G, BlockQ* q,
                                            const int* off, const int* nbr, int s, int p1, int p2,
                                            long long* edges, long long* walked) {
+  FPROF(Timer tm(E.rank == 0));
   const int nrem = vld(&G->nrem[s % 3]), nch = vld(&G->nchunk[s % 3]);
+  FPROF(tm.lap(G, 6));
   for (int k = E.rank; k < nrem; k += E.size) {  // independent of the chunks: issued first
     const int u = F.rem[k];
     F.deg[u] = 0;
@@ -293,7 +331,9 @@ __device__ __forceinline__ void remove_set(const Ex& E, const Front& F, FrontCtl
     const int4 ch = __ldcg(F.chunk + c);
     rm_chunk(F, G, q, nbr, s, p1, p2, ch.x, ch.y, ch.z, edges);
   }
+  FPROF(tm.lap(G, 7); __syncthreads(); tm.lap(G, 8));
   qflush(q, F.l1[p1], &G->cnt1[p1], F.l2[p2], &G->cnt2[p2]);
+  FPROF(tm.lap(G, 9));
 }
 
 // live-neighbour sums of every tracked live vertex (thread per vertex, a
@@ -355,18 +395,17 @@ __device__ __forceinline__ void next_slots(FrontCtl* G, int s) {
   G->nrem[z] = G->ncand[z] = G->ch[z] = G->dmax[z] = G->nchunk[z] = 0;
 }
 
-struct Timer {  // thread 0's phase clock
-  unsigned long long t;
-  bool on;
-  __device__ explicit Timer(bool o) : t(o ? globaltimer() : 0), on(o) {}
-  __device__ void lap(FrontCtl* G, int i) {
-    if (on) {
-      const unsigned long long now = globaltimer();
-      G->tph[i] += now - t;
-      t = now;
-    }
-  }
-};
+
+// thread 0 of the grid appends one record per sweep (after its last barrier)
+__device__ __forceinline__ void slog(FrontCtl* G, int rank, int ph, int ncur, int s) {
+  if (rank != 0 || G->nlog >= kLog) return;
+  long long* r = G->slog[G->nlog++];
+  r[0] = ph;
+  r[1] = (long long)globaltimer();
+  r[2] = ncur;
+  r[3] = vld(&G->nrem[s % 3]);
+  r[4] = vld(&G->nchunk[s % 3]);
+}
 
 // One degree-one sweep (pure.py:82) over the pending list l1[p1].
 __device__ __forceinline__ void sweep_d1(const Ex& E, const Front& F, FrontCtl* G, BlockQ* q,
@@ -387,6 +426,7 @@ __device__ __forceinline__ void sweep_d1(const Ex& E, const Front& F, FrontCtl* 
     next_slots(G, s);
     G->items += (unsigned long long)ncur;
   }
+  FPROF(tm.lap(G, 13));
   // A: targets (the neighbour-id sum of a degree-1 vertex) and claims
   for (int k = E.rank; k < ncur; k += E.size) {
     const int v = L[k];
@@ -417,7 +457,9 @@ __device__ __forceinline__ void sweep_d1(const Ex& E, const Front& F, FrontCtl* 
     const bool twin = dget(F.deg, u) == 1 && __ldcg(F.ia + u) == v && u < v;
     if (win && !twin) add_removed(F, G, q, off, s, u, walked);
   }
+  FPROF(tm.lap(G, 10); __syncthreads(); tm.lap(G, 11));
   qflush(q, F.rem, &G->nrem[s % 3], F.rem, &G->nrem[s % 3]);
+  FPROF(tm.lap(G, 12));
   cflush(q, F.chunk, &G->nchunk[s % 3]);
   tm.lap(G, 1);
   E.sync();
@@ -428,6 +470,7 @@ __device__ __forceinline__ void sweep_d1(const Ex& E, const Front& F, FrontCtl* 
   tm.lap(G, 2);
   E.sync();
   tm.lap(G, 5);
+  slog(G, E.rank, 1, ncur, s);
   S.p1 = nxt;
   S.d1 += nr;
   S.forced += nr;
@@ -543,6 +586,7 @@ __device__ __forceinline__ void sweep_tri(const Ex& E, const Front& F, FrontCtl*
     E.sync();
     tri = nr / 2;
   }
+  slog(G, E.rank, 2, ncur, s);
   S.p2 = nxt;
   S.d2t += tri;
   S.forced += 2 * tri;
@@ -564,7 +608,9 @@ __device__ __forceinline__ void sweep_hd(const Front& F, FrontCtl* G, BlockQ* q,
   if (gt == 0) next_slots(G, s);
   int ch = 0, dm = 0;
   for (int v = gt; v < n; v += T) {
-    const int d = dget(F.deg, v);
+    const int raw = (int)__ldcg(F.deg + v);
+    if (raw < 0) F.deg[v] = 0;  // dead below zero (rm_chunk): the block-level sweep reads raw
+    const int d = raw > 0 ? raw : 0;
     ch += (d > 0 && d > bud);
     dm = d > dm ? d : dm;
   }
@@ -613,6 +659,7 @@ __device__ __forceinline__ void sweep_hd(const Front& F, FrontCtl* G, BlockQ* q,
     }
     grid_barrier(&G->bar);
   }
+  slog(G, gt, 3, CH, s);
   S.hd += applied;
   S.forced += applied;
   S.cycle += applied;
@@ -633,6 +680,7 @@ __global__ void __launch_bounds__(kRootGridThreads, 1)
                  int solo_max) {
   __shared__ BlockScratch bs;
   __shared__ BlockQ q;
+  const unsigned long long t_start = globaltimer();
   if (threadIdx.x == 0) q.cnt[0] = q.cnt[1] = q.ccnt = q.cused = 0;
   init_block_scratch(&bs);
   FrontCtl* G = (FrontCtl*)ctl_mem;  // zeroed by the host before the launch
@@ -684,6 +732,12 @@ __global__ void __launch_bounds__(kRootGridThreads, 1)
   grid_barrier(&G->bar);  // degrees initialised
   init_sums(F, off, nbr, n, init != 0);
   grid_barrier(&G->bar);
+  if (gt == 0) {
+    G->slog[0][0] = 0;
+    G->slog[0][1] = (long long)globaltimer();
+    G->slog[0][2] = (long long)t_start;
+    G->nlog = 1;
+  }
   St S{F_D1, 0, 0, 1, 1, 0, 0, 0, 0, 0, -1, 0, 1, 0};
   long long edges = 0, walked = 0;
   const Ex EG{gt, T, true, &G->bar};
@@ -740,7 +794,9 @@ __global__ void __launch_bounds__(kRootGridThreads, 1)
   int cnt = 0, mn = kInf, mx = -1;
   for (int v = b; v < e; ++v) {
     cnt += F.forced[v];
-    if (dget(F.deg, v) > 0) {
+    const int raw = (int)__ldcg(F.deg + v);
+    if (raw < 0) F.deg[v] = 0;  // the host and the next launch read the array raw
+    if (raw > 0) {
       mn = min(mn, v);
       mx = v;
     }
@@ -820,6 +876,22 @@ __global__ void __launch_bounds__(kRootGridThreads, 1)
 }
 
 size_t root_front_ctl_bytes() { return sizeof(FrontCtl); }
+
+// VCG_TRACE: the per-sweep log of the last launch (ctl on the device)
+void root_front_print_log(const void* ctl) {
+  FrontCtl h;
+  if (cudaMemcpy(&h, ctl, sizeof(FrontCtl), cudaMemcpyDeviceToHost) != cudaSuccess) return;
+  static const char* nm[4] = {"init", "d1", "tri", "hd"};
+  if (h.tph[7]) fprintf(stderr, "[vcg root]   sub-phases us: C vld %.1f chunks %.1f sync %.1f flush %.1f | B work %.1f sync %.1f qflush %.1f cflush %.1f | pre-A %.1f\n",
+          h.tph[6] * 1e-3, h.tph[7] * 1e-3, h.tph[8] * 1e-3, h.tph[9] * 1e-3, h.tph[10] * 1e-3,
+          h.tph[11] * 1e-3, h.tph[12] * 1e-3, h.tph[1] * 1e-3, h.tph[13] * 1e-3);
+  fprintf(stderr, "[vcg root]   init (degrees, lists, sums) %.1f us\n",
+          (h.slog[0][1] - h.slog[0][2]) * 1e-3);
+  for (int i = 1; i < h.nlog && i < kLog; ++i)
+    fprintf(stderr, "[vcg root]   sweep %2d %-4s %7.1f us  frontier %8lld removed %8lld chunks %8lld\n",
+            i, nm[h.slog[i][0] & 3], (h.slog[i][1] - h.slog[i - 1][1]) * 1e-3, h.slog[i][2],
+            h.slog[i][3], h.slog[i][4]);
+}
 
 size_t root_front_bytes(int n, long long m2) {
   const size_t nn = ((size_t)n + 31) & ~(size_t)31;

@@ -30,6 +30,7 @@ cudaError_t root_grid_launch(int n, const int32_t* off, const int32_t* nbr, char
 // full passes over the degree array), then sweeps, sweeps run by one block,
 // adjacency entries walked, frontier entries examined.
 size_t root_front_ctl_bytes();
+void root_front_print_log(const void* ctl);
 size_t root_front_bytes(int n, long long m2);
 int root_front_blocks();
 cudaError_t root_front_launch(int n, const int32_t* off, const int32_t* nbr, char* ws,

@@ -115,7 +115,7 @@ struct WStats {
   unsigned long long c_iter;                   // fixpoint loop iterations
   unsigned long long rules[6];
   unsigned long long t_exp, t_rsplit, t_wait, t_rfail;  // VCG_TASK_TRACE, per task
-  unsigned long long t_ph[5];                           // split phases (VCG_TASK_TRACE)
+  unsigned long long t_ph[8];                           // split phases (VCG_TASK_TRACE)
 };
 
 // ------------------------------------------------------------ masks --
@@ -521,8 +521,8 @@ __device__ inline bool warp_export(const SearchParams& P, const WS& ws, const WT
 // unchanged), rows restricted to c and compacted, so a small component runs
 // on narrow masks.
 template <typename M, typename WS>
-__device__ inline void warp_emit_component(const SearchParams& P, const WS& ws, M c, int scope,
-                                           int depth, long long pos) {
+__device__ inline long long warp_emit_component(const SearchParams& P, const WS& ws, M c, int scope,
+                                                int depth, long long pos) {
   const int lane = threadIdx.x & 31;
   const int sz = wpopc(c);
   const int Wn = wrows(sz);
@@ -563,7 +563,10 @@ __device__ inline void warp_emit_component(const SearchParams& P, const WS& ws, 
     if (Wn > 2) __stcg((ulonglong2*)(dst + sz * Wn), make_ulonglong2(lv[2], lv[3]));
   }
   __syncwarp();
+  TTRACE(const long long tp = clock64());
   if (lane == 0) q_publish_push(P.bq, pos);
+  TTRACE(__syncwarp(); return clock64() - tp);
+  return 0;
 }
 
 // A frame-0 node of a wide task that splits into ng >= 2 general components
@@ -641,8 +644,10 @@ __device__ inline bool warp_registry_split(const SearchParams& P, WS& ws, const 
     if (lane == 0) q_wait_free(P.bq, pos + j);
     __syncwarp();
     TTRACE(st.t_ph[2] += clock64() - tq; tq = clock64());
-    warp_emit_component<M, WS>(P, ws, wload<M>(&ws.pend[K * (pbase + j)]), p + 1 + j,
+    const long long tpub = warp_emit_component<M, WS>(P, ws, wload<M>(&ws.pend[K * (pbase + j)]), p + 1 + j,
                                th.depth + 1, pos + j);
+    (void)tpub;
+    TTRACE(st.t_ph[7] += tpub; st.t_ph[5] += 1; st.t_ph[6] += wpopc(wload<M>(&ws.pend[K * (pbase + j)])));
     TTRACE(st.t_ph[3] += clock64() - tq; tq = clock64());
   }
   if (lane == 0) {
@@ -1026,11 +1031,12 @@ __device__ inline bool warp_epoch(const SearchParams& P, void* wws_raw, int* bus
     const unsigned long long dt = (unsigned long long)(clock64() - t0);
     TTRACE(if (lane == 0 && dt > 400000ull)
              printf("task n=%d depth=%d nodes=%llu cycles=%llu exports=%llu rsplits=%llu "
-                    "rfail=%llu split_cycles=%llu f0best=%d ph=%llu/%llu/%llu/%llu/%llu\n", n,
+                    "rfail=%llu split_cycles=%llu f0best=%d ph=%llu/%llu/%llu/%llu/%llu emits=%llu emitted_v=%llu pub=%llu\n", n,
                     th.depth, st.nodes - nodes0, dt, st.t_exp, st.t_rsplit, st.t_rfail, st.t_wait,
-                    ws.fr[0].best, st.t_ph[0], st.t_ph[1], st.t_ph[2], st.t_ph[3], st.t_ph[4]);
+                    ws.fr[0].best, st.t_ph[0], st.t_ph[1], st.t_ph[2], st.t_ph[3], st.t_ph[4], st.t_ph[5],
+                    st.t_ph[6], st.t_ph[7]);
            st.t_exp = st.t_rsplit = st.t_wait = st.t_rfail = 0;
-           for (int i = 0; i < 5; ++i) st.t_ph[i] = 0);
+           for (int i = 0; i < 8; ++i) st.t_ph[i] = 0);
     st.tasks += 1;
     st.cyc += dt;
     if (dt > st.maxcyc) {
