@@ -46,6 +46,7 @@
 // reset pass is needed; removal-set membership is a per-vertex sweep tag.
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 
@@ -103,26 +104,45 @@ struct Front {  // device arrays (root_front_bytes)
   uint8_t* trk;                     // adjacency longer than kTrack: sums maintained
 };
 
+// Per-block copy of FrontCtl's control header (list lengths, step slots,
+// claim-round flags, err): refreshed by warp 0 inside every barrier, one word
+// per lane.  Every thread used to read these words from L2 after each barrier:
+// 2368 warps' loads of one address queue at one L2 slice (ncu: the loop
+// bounds after a barrier were the top long-scoreboard lines).
+constexpr int kHdr = 32;
+__device__ __forceinline__ int* hdr_cache() {
+  __shared__ int c[kHdr];
+  return c;
+}
+__device__ __forceinline__ void hdr_refresh(const int* G) {  // warp 0, after the acquire
+  if (threadIdx.x < kHdr) hdr_cache()[threadIdx.x] = __ldcg(G + threadIdx.x);
+}
+
 // Grid barrier.  cooperative_groups' grid.sync() polls with acquire loads,
 // each followed by an L1 invalidate (CCTL.IVALL; ncu: 8.5 M in one launch).
 // This one polls with volatile loads and __nanosleep and acquires once, after
 // the flip.  Arrival flips bit 31 of the word (block 0 adds 2^31 - (blocks -
-// 1), the others 1), so it needs no reset.
-__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+// 1), the others 1), so it needs no reset.  Warp 0 then refreshes the
+// block's header copy.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, const int* hdr) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
-    __threadfence();
-    const unsigned old = atomicAdd(bar, inc);
-    if (blockIdx.x == 0) bar[1] += 1;  // barriers passed (FrontCtl::nbar)
-    unsigned ns = 32;
-    while (((old ^ *(volatile unsigned*)bar) & 0x80000000u) == 0) {
-      __nanosleep(ns);
-      if (ns < 256) ns <<= 1;
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) {
+      const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+      __threadfence();
+      const unsigned old = atomicAdd(bar, inc);
+      if (blockIdx.x == 0) bar[1] += 1;  // barriers passed (FrontCtl::nbar)
+      unsigned ns = 32;
+      while (((old ^ *(volatile unsigned*)bar) & 0x80000000u) == 0) {
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+      }
+      unsigned v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      (void)v;
     }
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-    (void)v;
+    __syncwarp();
+    hdr_refresh(hdr);
   }
   __syncthreads();
 }
@@ -131,13 +151,24 @@ struct Ex {  // executor: the whole grid, or block 0 alone
   int rank, size;
   bool grid;
   unsigned* bar;
+  const int* hdr;
   __device__ void sync() const {
-    if (grid) grid_barrier(bar);
-    else __syncthreads();
+    if (grid) {
+      grid_barrier(bar, hdr);
+    } else {
+      __syncthreads();
+      hdr_refresh(hdr);
+      __syncthreads();
+    }
   }
 };
 
 __device__ __forceinline__ int vld(const int* p) { return *(const volatile int*)p; }
+// a header word as of the block's last barrier (stable from that barrier to
+// the next one: written only by atomics of the phase that ends there)
+__device__ __forceinline__ int cld(const void* G, const int* p) {
+  return hdr_cache()[p - (const int*)G];
+}
 // Degrees are decremented speculatively (rm_chunk), so a dead vertex's word
 // may have gone below zero: every reader clamps, sweep_hd and the final pass
 // store the zeros back.
@@ -320,7 +351,7 @@ __device__ __forceinline__ void remove_set(const Ex& E, const Front& F, FrontCtl
                                            const int* off, const int* nbr, int s, int p1, int p2,
                                            long long* edges, long long* walked) {
   FPROF(Timer tm(E.rank == 0));
-  const int nrem = vld(&G->nrem[s % 3]), nch = vld(&G->nchunk[s % 3]);
+  const int nrem = cld(G, &G->nrem[s % 3]), nch = cld(G, &G->nchunk[s % 3]);
   FPROF(tm.lap(G, 6));
   for (int k = E.rank; k < nrem; k += E.size) {  // independent of the chunks: issued first
     const int u = F.rem[k];
@@ -413,7 +444,7 @@ __device__ __forceinline__ void sweep_d1(const Ex& E, const Front& F, FrontCtl* 
                                          long long* walked) {
   const int s = S.s, t = S.tg;
   const int cur = S.p1, nxt = S.p1 ^ 1;
-  const int ncur = vld(&G->cnt1[cur]);
+  const int ncur = cld(G, &G->cnt1[cur]);
   if (ncur == 0) {  // nothing to sweep: no barriers, no step slot used
     S.sweeps += 1;
     S.phase = F_TRI;
@@ -465,7 +496,7 @@ __device__ __forceinline__ void sweep_d1(const Ex& E, const Front& F, FrontCtl* 
   E.sync();
   tm.lap(G, 4);
   // C: removal
-  const int nr = vld(&G->nrem[s % 3]);
+  const int nr = cld(G, &G->nrem[s % 3]);
   remove_set(E, F, G, q, off, nbr, s, nxt, S.p2, edges, walked);
   tm.lap(G, 2);
   E.sync();
@@ -506,7 +537,7 @@ __device__ __forceinline__ void sweep_tri(const Ex& E, const Front& F, FrontCtl*
   const int lane = threadIdx.x & 31;
   const int s = S.s;
   const int cur = S.p2, nxt = S.p2 ^ 1;
-  const int ncur = vld(&G->cnt2[cur]);
+  const int ncur = cld(G, &G->cnt2[cur]);
   if (ncur == 0) {
     S.sweeps += 1;
     S.phase = F_HD;
@@ -540,7 +571,7 @@ __device__ __forceinline__ void sweep_tri(const Ex& E, const Front& F, FrontCtl*
   }
   qflush(q, F.cand, ncand, F.cand, ncand);
   E.sync();
-  const int nc = vld(ncand);
+  const int nc = cld(G, ncand);
   int tri = 0;
   if (nc > 0) {
     while (true) {
@@ -579,9 +610,9 @@ __device__ __forceinline__ void sweep_tri(const Ex& E, const Front& F, FrontCtl*
       cflush(q, F.chunk, &G->nchunk[s % 3]);
       S.tg += 1;
       E.sync();
-      if (!vld(open)) break;
+      if (!cld(G, open)) break;
     }
-    const int nr = vld(&G->nrem[s % 3]);
+    const int nr = cld(G, &G->nrem[s % 3]);
     remove_set(E, F, G, q, off, nbr, s, S.p1, nxt, edges, walked);
     E.sync();
     tri = nr / 2;
@@ -623,9 +654,9 @@ __device__ __forceinline__ void sweep_hd(const Front& F, FrontCtl* G, BlockQ* q,
       if (vals[1]) atomicMax(&G->dmax[s % 3], vals[1]);
     }
   }
-  grid_barrier(&G->bar);
+  grid_barrier(&G->bar, (const int*)G);
   S.passes += 1;
-  const int CH = vld(&G->ch[s % 3]), DM = vld(&G->dmax[s % 3]);
+  const int CH = cld(G, &G->ch[s % 3]), DM = cld(G, &G->dmax[s % 3]);
   if (bud > kSpecBudget / 2) S.spec_m = max(S.spec_m, DM + S.forced);
   int applied = 0;
   if (CH > 0) {
@@ -640,8 +671,8 @@ __device__ __forceinline__ void sweep_hd(const Front& F, FrontCtl* G, BlockQ* q,
         G->cnt2[S.p2] = 0;
       }
     }
-    grid_barrier(&G->bar);
-    applied = vld(&G->hd_applied);
+    grid_barrier(&G->bar, (const int*)G);
+    applied = cld(G, &G->hd_applied);
     if (applied > 0) {
       for (int v = gt; v < n; v += T) {
         const int d = dget(F.deg, v);
@@ -657,7 +688,7 @@ __device__ __forceinline__ void sweep_hd(const Front& F, FrontCtl* G, BlockQ* q,
       NodeWs<uint32_t> w = carve_ws<uint32_t>(wsmem, n, bs, off, nbr);
       for (int v = threadIdx.x; v < n; v += blockDim.x) w.ic[v] = 0;
     }
-    grid_barrier(&G->bar);
+    grid_barrier(&G->bar, (const int*)G);
   }
   slog(G, gt, 3, CH, s);
   S.hd += applied;
@@ -729,9 +760,9 @@ __global__ void __launch_bounds__(kRootGridThreads, 1)
       w.ic[v] = 0;
     }
   }
-  grid_barrier(&G->bar);  // degrees initialised
+  grid_barrier(&G->bar, (const int*)G);  // degrees initialised
   init_sums(F, off, nbr, n, init != 0);
-  grid_barrier(&G->bar);
+  grid_barrier(&G->bar, (const int*)G);
   if (gt == 0) {
     G->slog[0][0] = 0;
     G->slog[0][1] = (long long)globaltimer();
@@ -740,8 +771,8 @@ __global__ void __launch_bounds__(kRootGridThreads, 1)
   }
   St S{F_D1, 0, 0, 1, 1, 0, 0, 0, 0, 0, -1, 0, 1, 0};
   long long edges = 0, walked = 0;
-  const Ex EG{gt, T, true, &G->bar};
-  const Ex EB{(int)threadIdx.x, (int)blockDim.x, false, &G->bar};
+  const Ex EG{gt, T, true, &G->bar, (const int*)G};
+  const Ex EB{(int)threadIdx.x, (int)blockDim.x, false, &G->bar, (const int*)G};
   // %globaltimer profile (thread 0): ns in solo segments, grid degree-one
   // sweeps, grid triangle sweeps, high-degree points
   unsigned long long tcat[4] = {0, 0, 0, 0}, tprev = gt == 0 ? globaltimer() : 0;
@@ -753,21 +784,21 @@ __global__ void __launch_bounds__(kRootGridThreads, 1)
     }
   };
   while (S.phase != F_DONE) {
-    if (vld(&G->err)) break;
-    const int work = S.phase == F_D1 ? vld(&G->cnt1[S.p1]) : vld(&G->cnt2[S.p2]);
+    if (cld(G, &G->err)) break;
+    const int work = S.phase == F_D1 ? cld(G, &G->cnt1[S.p1]) : cld(G, &G->cnt2[S.p2]);
     if (S.phase != F_HD && work < solo_max) {
       if (blockIdx.x == 0) {
         while (true) {
           if (S.phase == F_D1) sweep_d1(EB, F, G, &q, off, nbr, S, &edges, &walked);
           else sweep_tri(EB, F, G, &q, off, nbr, S, &edges, &walked);
           S.solo += 1;
-          if (S.phase == F_HD || vld(&G->err)) break;
-          const int wk = S.phase == F_D1 ? vld(&G->cnt1[S.p1]) : vld(&G->cnt2[S.p2]);
+          if (S.phase == F_HD || cld(G, &G->err)) break;
+          const int wk = S.phase == F_D1 ? cld(G, &G->cnt1[S.p1]) : cld(G, &G->cnt2[S.p2]);
           if (wk >= solo_max) break;
         }
         if (threadIdx.x == 0) G->st = S;
       }
-      grid_barrier(&G->bar);
+      grid_barrier(&G->bar, (const int*)G);
       {
         const volatile int* r = (const volatile int*)&G->st;
         int* p = (int*)&S;
@@ -821,7 +852,7 @@ __global__ void __launch_bounds__(kRootGridThreads, 1)
         atomicAdd(k ? &G->walked : &G->edges, (unsigned long long)x);
     }
   }
-  grid_barrier(&G->bar);
+  grid_barrier(&G->bar, (const int*)G);
   int base, total;
   {
     const volatile int* partial = G->partial;
@@ -875,6 +906,7 @@ __global__ void __launch_bounds__(kRootGridThreads, 1)
   }
 }
 
+static_assert(offsetof(FrontCtl, edges) <= kHdr * sizeof(int), "control header exceeds the cached words");
 size_t root_front_ctl_bytes() { return sizeof(FrontCtl); }
 
 // VCG_TRACE: the per-sweep log of the last launch (ctl on the device)
