@@ -771,7 +771,9 @@ __global__ void __launch_bounds__(kRootGridThreads, 1)
   }
   St S{F_D1, 0, 0, 1, 1, 0, 0, 0, 0, 0, -1, 0, 1, 0};
   long long edges = 0, walked = 0;
-  const Ex EG{gt, T, true, &G->bar, (const int*)G};
+  // grid ranks interleave blocks (rank = thread * blocks + block): a small
+  // frontier spreads over every SM instead of filling block 0
+  const Ex EG{(int)(threadIdx.x * gridDim.x + blockIdx.x), T, true, &G->bar, (const int*)G};
   const Ex EB{(int)threadIdx.x, (int)blockDim.x, false, &G->bar, (const int*)G};
   // %globaltimer profile (thread 0): ns in solo segments, grid degree-one
   // sweeps, grid triangle sweeps, high-degree points
