@@ -93,6 +93,7 @@ struct FrontCtl {
 };
 
 struct Front {  // device arrays (root_front_bytes)
+  int n;
   uint32_t* deg;
   unsigned long long* key;          // claims
   unsigned long long *nsum, *nsq;   // live-neighbour id sums
@@ -228,11 +229,10 @@ __device__ __forceinline__ void two_from_sums(const Front& F, int v, int* a, int
 
 // u joins the removal set of step s: the rem list, and its adjacency as
 // kChunk-entry work items
-__device__ __forceinline__ void add_removed(const Front& F, FrontCtl* G, BlockQ* q,
-                                            const int* off, int s, int u, long long* walked) {
+__device__ __forceinline__ void add_removed_at(const Front& F, FrontCtl* G, BlockQ* q, int s,
+                                               int u, int b, int e, long long* walked) {
   F.rs[u] = s;
   qpush(q, 0, F.rem, &G->nrem[s % 3], u);
-  const int b = off[u], e = off[u + 1];
   *walked += e - b;
   const int nc = (e - b + kChunk - 1) / kChunk;
   if (nc > 0) {
@@ -249,6 +249,11 @@ __device__ __forceinline__ void add_removed(const Front& F, FrontCtl* G, BlockQ*
   }
 }
 
+__device__ __forceinline__ void add_removed(const Front& F, FrontCtl* G, BlockQ* q,
+                                            const int* off, int s, int u, long long* walked) {
+  add_removed_at(F, G, q, s, u, off[u], off[u + 1], walked);
+}
+
 // every thread of the block calls: publishes the staged removal chunks
 __device__ __forceinline__ void cflush(BlockQ* q, int4* list, int* cnt) {
   __syncthreads();
@@ -261,11 +266,11 @@ __device__ __forceinline__ void cflush(BlockQ* q, int4* list, int* cnt) {
   if (threadIdx.x == 0) q->ccnt = q->cused = 0;
 }
 
-// the first two live neighbours of an untracked vertex (adjacency <= kTrack):
-// all its entries and their degrees loaded at once, two dependent round trips
-__device__ __forceinline__ void live_short(const Front& F, const int* off, const int* nbr, int v,
-                                           int* a, int* b) {
-  const int s0 = off[v], len = off[v + 1] - s0;
+// the first two live neighbours of an untracked vertex (adjacency <= kTrack)
+// whose slice [s0, s0 + len) is known: its entries and their degrees loaded
+// at once, two dependent round trips
+__device__ __forceinline__ void live_short_at(const Front& F, const int* nbr, int s0, int len,
+                                              int* a, int* b) {
   int x[kTrack], d[kTrack];
 #pragma unroll
   for (int j = 0; j < kTrack; ++j) x[j] = j < len ? __ldg(nbr + s0 + j) : -1;
@@ -280,6 +285,12 @@ __device__ __forceinline__ void live_short(const Front& F, const int* off, const
     }
   *a = u;
   *b = w;
+}
+
+__device__ __forceinline__ void live_short(const Front& F, const int* off, const int* nbr, int v,
+                                           int* a, int* b) {
+  const int s0 = off[v];
+  live_short_at(F, nbr, s0, off[v + 1] - s0, a, b);
 }
 
 // one removal work item: the entries [b, min(b + kChunk, end(u))) of removed
@@ -458,36 +469,40 @@ __device__ __forceinline__ void sweep_d1(const Ex& E, const Front& F, FrontCtl* 
     G->items += (unsigned long long)ncur;
   }
   FPROF(tm.lap(G, 13));
-  // A: targets (the neighbour-id sum of a degree-1 vertex) and claims
+  // AB: targets and decisions in one phase.  A degree-1 candidate v with
+  // live neighbour u removes u unless v is the higher end of an isolated
+  // candidate edge (u has degree 1 too: its only live neighbour is v, so u
+  // removes v); of the candidates targeting one u the first to tag it adds
+  // it to the removal set.  Degrees do not change before phase C, so this
+  // is the reference's in-order sweep (the candidate that wins a shared
+  // target only changes which thread enqueues it), with one grid barrier
+  // less than a claim round.  Everything a candidate needs is loaded in one
+  // round trip (degree, tracked flag, id sum, adjacency bounds).
   for (int k = E.rank; k < ncur; k += E.size) {
     const int v = L[k];
-    if (dget(F.deg, v) != 1) {
-      L[k] = -1;
-      continue;
-    }
+    const int d = dget(F.deg, v);
+    const uint8_t tr = __ldg(F.trk + v);
+    const unsigned long long s1 = __ldcg(F.nsum + v);
+    const int o0 = __ldg(off + v), o1 = __ldg(off + v + 1);
+    if (d != 1) continue;
     int u, u2;
-    if (__ldg(F.trk + v)) u = (int)__ldcg(F.nsum + v);
-    else live_short(F, off, nbr, v, &u, &u2);
-    if (u < 0 || dget(F.deg, u) <= 0) {  // inconsistent degree array: report, never loop
+    if (tr) u = (int)s1;
+    else live_short_at(F, nbr, o0, o1 - o0, &u, &u2);
+    if (u < 0 || u >= F.n) {  // inconsistent degree array: report, never loop
       atomicExch(&G->err, 1);
-      L[k] = -1;
       continue;
     }
-    F.ia[v] = u;
-    atomicMax(F.key + u, claim_key(t, v));
+    const int du = dget(F.deg, u);
+    const int ob = __ldg(off + u), oe = __ldg(off + u + 1);
+    if (du <= 0) {
+      atomicExch(&G->err, 1);
+      continue;
+    }
+    if (du == 1 && u < v) continue;  // isolated candidate edge: u removes v
+    if (atomicMax(F.rs + u, s) < s) add_removed_at(F, G, q, s, u, ob, oe, walked);
   }
+  (void)t;
   tm.lap(G, 0);
-  E.sync();
-  tm.lap(G, 3);
-  // B: decisions (lowest-index claimant; isolated candidate edges once)
-  for (int k = E.rank; k < ncur; k += E.size) {
-    const int v = L[k];
-    if (v < 0) continue;
-    const int u = F.ia[v];
-    const bool win = __ldcg(F.key + u) == claim_key(t, v);
-    const bool twin = dget(F.deg, u) == 1 && __ldcg(F.ia + u) == v && u < v;
-    if (win && !twin) add_removed(F, G, q, off, s, u, walked);
-  }
   FPROF(tm.lap(G, 10); __syncthreads(); tm.lap(G, 11));
   qflush(q, F.rem, &G->nrem[s % 3], F.rem, &G->nrem[s % 3]);
   FPROF(tm.lap(G, 12));
@@ -718,6 +733,7 @@ __global__ void __launch_bounds__(kRootGridThreads, 1)
   Front F;
   {
     const size_t nn = ((size_t)n + 31) & ~(size_t)31;
+    F.n = n;
     F.deg = (uint32_t*)wsmem;
     unsigned long long* lp = (unsigned long long*)fmem;
     F.key = lp;
