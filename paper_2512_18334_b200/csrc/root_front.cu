@@ -122,7 +122,7 @@ __device__ __forceinline__ void hdr_refresh(const int* G) {  // warp 0, after th
 // Grid barrier.  cooperative_groups' grid.sync() polls with acquire loads,
 // each followed by an L1 invalidate (CCTL.IVALL; ncu: 8.5 M in one launch).
 // This one polls with volatile loads and __nanosleep and acquires once, after
-// the flip.  Arrival flips bit 31 of the word (block 0 adds 2^31 - (blocks -
+// the flip (an acquire fence instead measured slower).  Arrival flips bit 31 of the word (block 0 adds 2^31 - (blocks -
 // 1), the others 1), so it needs no reset.  Warp 0 then refreshes the
 // block's header copy.
 __device__ __forceinline__ void grid_barrier(unsigned* bar, const int* hdr) {
@@ -252,6 +252,24 @@ __device__ __forceinline__ void add_removed_at(const Front& F, FrontCtl* G, Bloc
 __device__ __forceinline__ void add_removed(const Front& F, FrontCtl* G, BlockQ* q,
                                             const int* off, int s, int u, long long* walked) {
   add_removed_at(F, G, q, s, u, off[u], off[u + 1], walked);
+}
+
+// every thread of the block calls: publishes the removal list (staging queue
+// 0) and the staged removal chunks with their two reservations in one round
+// trip (qflush + cflush back to back cost two)
+__device__ __forceinline__ void rflush(BlockQ* q, int* rem, int* nrem, int4* chunks, int* nch) {
+  __syncthreads();
+  const int c0 = min(q->cnt[0], kQ), c = q->cused;
+  if (threadIdx.x == 0) {
+    q->base[0] = c0 ? atomicAdd(nrem, c0) : 0;
+    q->cbase = c ? atomicAdd(nch, c) : 0;
+  }
+  __syncthreads();
+  const int b0 = q->base[0], b = q->cbase;
+  for (int i = threadIdx.x; i < c0; i += blockDim.x) rem[b0 + i] = q->buf[0][i];
+  for (int i = threadIdx.x; i < c; i += blockDim.x) chunks[b + i] = q->cbuf[i];
+  __syncthreads();
+  if (threadIdx.x == 0) q->cnt[0] = q->ccnt = q->cused = 0;
 }
 
 // every thread of the block calls: publishes the staged removal chunks
@@ -504,9 +522,8 @@ __device__ __forceinline__ void sweep_d1(const Ex& E, const Front& F, FrontCtl* 
   (void)t;
   tm.lap(G, 0);
   FPROF(tm.lap(G, 10); __syncthreads(); tm.lap(G, 11));
-  qflush(q, F.rem, &G->nrem[s % 3], F.rem, &G->nrem[s % 3]);
+  rflush(q, F.rem, &G->nrem[s % 3], F.chunk, &G->nchunk[s % 3]);
   FPROF(tm.lap(G, 12));
-  cflush(q, F.chunk, &G->nchunk[s % 3]);
   tm.lap(G, 1);
   E.sync();
   tm.lap(G, 4);
@@ -621,8 +638,7 @@ __device__ __forceinline__ void sweep_tri(const Ex& E, const Front& F, FrontCtl*
         }
       }
       if (__any_sync(0xffffffffu, still) && lane == 0) atomicOr(open, 1);
-      qflush(q, F.rem, &G->nrem[s % 3], F.rem, &G->nrem[s % 3]);
-      cflush(q, F.chunk, &G->nchunk[s % 3]);
+      rflush(q, F.rem, &G->nrem[s % 3], F.chunk, &G->nchunk[s % 3]);
       S.tg += 1;
       E.sync();
       if (!cld(G, open)) break;
