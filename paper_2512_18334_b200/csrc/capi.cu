@@ -1736,6 +1736,7 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   P.warp_limit = warp_limit;
   P.bq_slot = bslot;
   P.warp_split_export = !getenv("VCG_NO_WSPLIT");
+  P.tma_load = !getenv("VCG_NO_TMA");  // VCG_NO_TMA: per-thread loads instead
   P.bq_low = std::max(8LL, (long long)blocks * (threads / 32) / 4);
   if (const char* e = getenv("VCG_BQLOW")) P.bq_low = atoll(e);  // experiments
   {

@@ -173,6 +173,7 @@ struct SearchParams {
   Queue bq;
   long long bq_slot;      // bytes per warp-task slot (warp_solve.cuh wslot_bytes)
   int warp_split_export;  // wide warp tasks hand frame-0 splits to the registry
+  int tma_load;           // node records into shared-memory workspaces by TMA bulk copy
   int warp_limit;         // 0 = off
   long long bq_low;       // a long warp task sheds work while the ring holds fewer
   int w_check_mask;       // a warp task polls stop / bound / ring every (mask + 1) nodes
@@ -542,6 +543,60 @@ __device__ inline int load_node(const char* src, NodeHdr* hdr, void* payload, lo
   const uint4* sd = s + 2;
   uint4* dd = (uint4*)payload;
   for (long long i = threadIdx.x; i < words; i += blockDim.x) dd[i] = __ldcg(sd + i);
+  return gn;
+}
+
+// The same load with the payload moved by the Tensor Memory Accelerator: one
+// thread reads the header's graph fields (the size depends on them), then
+// issues a 1-D bulk copy (cp.async.bulk, global -> shared) that completes on
+// an mbarrier every thread waits on; the other threads issue no loads.
+// Shared-memory payloads only (kSmem search variants).  `phase` is the
+// mbarrier's parity, flipped per use.
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+template <typename T>
+__device__ inline int load_node_tma(const char* src, NodeHdr* hdr, void* payload, long long extra,
+                                    int n_root, const int* keys, int* best_out,
+                                    unsigned long long* bar, unsigned* phase, int* err) {
+  const uint4* s = (const uint4*)src;
+  const uint4 h1 = __ldcg(s + 1);  // scope, depth, graph, gn
+  const int gn = h1.z ? (int)h1.w : n_root;
+  const unsigned bytes = (unsigned)(deg_bytes<T>(gn) + extra);
+  const unsigned ab = (unsigned)__cvta_generic_to_shared(bar);
+  if (threadIdx.x == 0) {
+    ((uint4*)hdr)[0] = __ldcg(s);
+    // the block's earlier generic-proxy accesses of the payload (ordered
+    // before this thread by the caller's barrier) precede the async writes
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ab), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            (unsigned)__cvta_generic_to_shared(payload)),
+        "l"(s + 2), "r"(bytes), "r"(ab)
+        : "memory");
+  }
+  if (threadIdx.x == 1) {
+    ((uint4*)hdr)[1] = h1;
+    *best_out = ld_relaxed(&keys[(int)h1.x]) >> 1;
+  }
+  unsigned done = 0;
+  for (unsigned spin = 0; !done; ++spin) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(ab), "r"(*phase)
+        : "memory");
+    if (!done && spin > (1u << 24)) {  // never hang the search: report and stop
+      atomicExch(err, 1);
+      break;
+    }
+  }
+  *phase ^= 1u;
   return gn;
 }
 

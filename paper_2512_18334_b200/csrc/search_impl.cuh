@@ -755,6 +755,9 @@ __global__ void __launch_bounds__(VCG_SEARCH_MAXT, VCG_SEARCH_MINB) search_kerne
   // tier runs in blocks of <= 256 threads)
   __shared__ int wgl[kWTierWarps * 64 * kWW];
   __shared__ int wbusy;
+  __shared__ __align__(8) unsigned long long tma_bar;  // node-record bulk copies (kSmem)
+  unsigned tma_phase = 0;
+  if (kSmem && threadIdx.x == 0) mbar_init(&tma_bar);
   char* base = kSmem ? (char*)dsmem : P.gws + (long long)blockIdx.x * P.gws_bytes;
   NodeWs<T> ws = carve_ws<T>(base, P.n, &bs, P.off, P.nbr);
   if (kSmem && P.csr_in_smem) {
@@ -838,8 +841,12 @@ __global__ void __launch_bounds__(VCG_SEARCH_MAXT, VCG_SEARCH_MINB) search_kerne
     if (!cont) {
       if (wk.top > 0) {
         wk.top -= 1;
-        const int gn = load_node<T>(wk.stack_slot(wk.top), &st.hdr, ws.deg, wk.extra, P.n,
-                                    P.reg.key, &st.best_s);
+        const int gn =
+            kSmem && P.tma_load
+                ? load_node_tma<T>(wk.stack_slot(wk.top), &st.hdr, ws.deg, wk.extra, P.n, P.reg.key,
+                                   &st.best_s, &tma_bar, &tma_phase, &P.ctl->error)
+                : load_node<T>(wk.stack_slot(wk.top), &st.hdr, ws.deg, wk.extra, P.n, P.reg.key,
+                               &st.best_s);
         if (threadIdx.x == 0) ++wk.rec_in;
         __syncthreads();
         wk.set_graph(st.hdr.graph, gn);
@@ -877,8 +884,12 @@ __global__ void __launch_bounds__(VCG_SEARCH_MAXT, VCG_SEARCH_MINB) search_kerne
           continue;
         }
         backoff = 32;
-        const int gn = load_node<T>(wk.queue_slot(pos), &st.hdr, ws.deg, wk.extra, P.n,
-                                    P.reg.key, &st.best_s);
+        const int gn =
+            kSmem && P.tma_load
+                ? load_node_tma<T>(wk.queue_slot(pos), &st.hdr, ws.deg, wk.extra, P.n, P.reg.key,
+                                   &st.best_s, &tma_bar, &tma_phase, &P.ctl->error)
+                : load_node<T>(wk.queue_slot(pos), &st.hdr, ws.deg, wk.extra, P.n, P.reg.key,
+                               &st.best_s);
         __syncthreads();
         wk.set_graph(st.hdr.graph, gn);
         if (threadIdx.x == 0) {
