@@ -108,6 +108,11 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes a while to print its first sample: the timed
+            # region starts only once it is streaming
+            deadline = time.time() + 3.0
+            while len(self.lines) < 2 and time.time() < deadline:
+                time.sleep(0.01)
         except (OSError, FileNotFoundError):
             self.proc = None
         return self
