@@ -181,3 +181,68 @@ def test_scale_root_pipeline_matches_oracle(name):
     rp = vc.solve(g, vc.SolverConfig())
     assert rp.cover_size == exp["mvc"]
     assert rp.stats.rule_counts == r.stats.rule_counts
+
+
+def _families():
+    """Adversarial shapes for the frontier kernel's degree-one phase, which
+    decides targets and tags them in one phase and decrements degrees
+    speculatively: isolated candidate edges (every vertex degree 1), stars
+    and double stars (many candidates on one target), long paths and
+    caterpillars (one peel per sweep), pendant chains hanging off hubs that
+    are themselves removed in the same sweep, triangles on paths (the
+    triangle sweep after the degree-one cascade), plus random sparse graphs
+    with many pendants."""
+    rng = random.Random(7)
+    out = []
+    m = 400
+    out.append(("matching", 2 * m, [(2 * i, 2 * i + 1) for i in range(m)]))
+    out.append(("stars", 41 * 30, [(41 * s, 41 * s + j) for s in range(30) for j in range(1, 41)]))
+    out.append(("double_stars", 62 * 20,
+                [e for s in range(20) for e in [(62 * s, 62 * s + 1)] +
+                 [(62 * s + (j & 1), 62 * s + 2 + j) for j in range(60)]]))
+    out.append(("path", 3001, [(i, i + 1) for i in range(3000)]))
+    out.append(("caterpillar", 3000, [(i, i + 1) for i in range(999)] +
+                [(i % 1000, 1000 + i) for i in range(2000)]))
+    hub_e = []
+    for h in range(50):  # hub h (id 100 * h) with 40 pendant chains of length 1-3
+        base = 100 * h
+        nxt = base + 1
+        for _ in range(30):
+            ln = rng.randint(1, 3)
+            prev = base
+            for _ in range(ln):
+                if nxt >= base + 100:
+                    break
+                hub_e.append((prev, nxt))
+                prev, nxt = nxt, nxt + 1
+        if h:
+            hub_e.append((base, base - 100))  # hubs in a chain
+    out.append(("hub_chains", 5000, hub_e))
+    tri = [(i, i + 1) for i in range(1999)] + [(i, i + 2) for i in range(0, 1998, 3)]
+    out.append(("triangles_on_path", 2000, tri))
+    for s in range(4):
+        n = 6000
+        e = {(min(u, v), max(u, v)) for u, v in
+             ((rng.randrange(n), rng.randrange(n)) for _ in range(4000 + 3000 * s)) if u != v}
+        e |= {(rng.randrange(n // 4), v) for v in range(n // 4, n) if rng.random() < 0.6}
+        out.append((f"random_pendants_{s}", n, sorted(e)))
+    return out
+
+
+def test_front_root_reduce_families(front_root):
+    """The frontier kernel against the oracle's restatement of
+    preprocess.py:77 on the adversarial families above: the same forced set,
+    rule counts, vertex map and reduced graph."""
+    import oracle
+    import paper_2512_18334_b200 as vc
+
+    for name, n, edges in _families():
+        nn, off, nbr = csr(n, edges)
+        want = oracle.root_reduce(nn, off, nbr)
+        pre = vc.root_reduce(vc.StaticGraph(nn, off, nbr), ordered=False)
+        assert pre.kernel["kind"] == "frontier", name
+        assert pre.forced == sorted(want["forced"]), name
+        assert pre.rule_counts == want["rule_counts"], name
+        assert pre.vertex_map.tolist() == want["vertex_map"], name
+        assert pre.graph.offsets.tolist() == want["offsets"].tolist(), name
+        assert pre.graph.neighbors.tolist() == want["neighbors"].tolist(), name

@@ -257,3 +257,24 @@ def test_registry_reclamation_answers_and_reuse(monkeypatch):
     r = vc.solve(vc.StaticGraph(n, off, nbr), vc.SolverConfig(timeout=4.0))
     assert r.stats.component_branches > len(r.registry)
     assert r.cover_size is not None
+
+
+def test_node_loads_with_and_without_tma(monkeypatch):
+    """Node records enter the shared-memory workspace by a TMA bulk copy by
+    default; the per-thread load path (VCG_NO_TMA=1) gives the same
+    deterministic statistics, and both match the reference's."""
+    import paper_2512_18334_b200 as vc
+
+    cases = golden("solve.json")[::5]
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("VCG_NO_TMA", env)
+        for case in cases:
+            n, off, nbr = csr(case["n"], case["edges"])
+            g = vc.StaticGraph(n, off, nbr)
+            run = case["runs"]["det"]
+            r = vc.solve(g, vc.SolverConfig(deterministic=True))
+            assert r.cover_size == run["cover_size"], (case["name"], env)
+            assert stats_without_time(r.stats.as_dict()) == run["stats"], (case["name"], env)
+            p = vc.solve(g, vc.SolverConfig(check_registry=True))
+            assert p.cover_size == run["cover_size"], (case["name"], env)
