@@ -1093,6 +1093,7 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
       COUNT_LAUNCH(1);
       hdeg_current = false;
       const int budget = spec ? kSpecBudget : (int)(bound0 - forced_count);
+      const auto tl0 = std::chrono::steady_clock::now();
       CK(cudaEventRecord(rk0, cudaStreamPerThread));
       if (use_front) {
         CK(root_front_launch(n, g->d_off.as<int32_t>(), g->d_nbr.as<int32_t>(), ws.as<char>(),
@@ -1112,8 +1113,14 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
       }
       CK(cudaGetLastError());
       CK(cudaEventRecord(rk1, cudaStreamPerThread));
+      const auto tl1 = std::chrono::steady_clock::now();
       CK(cudaMemcpy(ret, dret.p, fast ? 144 : use_front ? 208 : use_grid ? 88 : 80,
                     cudaMemcpyDeviceToHost));
+      const auto tl2 = std::chrono::steady_clock::now();
+      if (trace_on())
+        fprintf(stderr, "[vcg root] host: launch call %.1f us, launch..ret copied %.1f us\n",
+                std::chrono::duration<double, std::micro>(tl1 - tl0).count(),
+                std::chrono::duration<double, std::micro>(tl2 - tl0).count());
       {
         float kms = 0.f;
         CK(cudaEventElapsedTime(&kms, rk0, rk1));
