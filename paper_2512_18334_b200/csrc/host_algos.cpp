@@ -152,6 +152,29 @@ bool try_augment(int32_t root, const std::vector<std::vector<int32_t>>& adj,
 
 }  // namespace
 
+// Per-thread scratch of size n, initialised once and restored after every
+// call by walking the entries the call touched: a crown round on a 1M-vertex
+// graph with a small live set used to spend ~1 ms allocating and clearing
+// seven n-sized arrays.
+namespace {
+struct CrownScratch {
+  std::vector<int32_t> partner, left_slot, pair_left, pair_right;
+  std::vector<int> dist;
+  std::vector<char> in_crown, is_head;
+  void fit(int64_t n) {
+    if ((int64_t)partner.size() >= n) return;
+    partner.assign(n, -1);
+    left_slot.assign(n, -1);
+    pair_left.assign(n, -1);
+    pair_right.assign(n, -1);
+    dist.assign(n, kAbsent);
+    in_crown.assign(n, 0);
+    is_head.assign(n, 0);
+  }
+};
+thread_local CrownScratch t_crown;
+}  // namespace
+
 // reductions.py:263 crown_reduce on a host degree array (int32, in/out).
 int64_t crown_reduce_host(int64_t n, const int64_t* off, const int32_t* nbr, int32_t* deg,
                           int64_t lo, int64_t hi, std::vector<int32_t>* heads_out,
@@ -164,7 +187,28 @@ int64_t crown_reduce_host(int64_t n, const int64_t* off, const int32_t* nbr, int
   for (int64_t v = lo; v <= hi; ++v)
     if (deg[v] > 0) live.push_back((int32_t)v);
   if (live.empty()) return 0;
-  std::vector<int32_t> partner(n, -1);
+  CrownScratch& X = t_crown;
+  X.fit(n);
+  std::vector<int32_t>& partner = X.partner;
+  std::vector<int32_t>& left_slot = X.left_slot;
+  std::vector<int32_t>& pair_left = X.pair_left;
+  std::vector<int32_t>& pair_right = X.pair_right;
+  std::vector<int>& dist = X.dist;
+  std::vector<char>& in_crown = X.in_crown;
+  std::vector<char>& is_head = X.is_head;
+  // every index written below is a live vertex (live vertices lie in the
+  // window, and partners, heads and left vertices are live): restore them
+  struct Restore {
+    CrownScratch& X;
+    const std::vector<int32_t>& live;
+    ~Restore() {
+      for (int32_t v : live) {
+        X.partner[v] = X.left_slot[v] = X.pair_left[v] = X.pair_right[v] = -1;
+        X.dist[v] = kAbsent;
+        X.in_crown[v] = X.is_head[v] = 0;
+      }
+    }
+  } restore{X, live};
   for (int32_t v : live) {
     if (partner[v] >= 0) continue;
     for (int64_t i = off[v]; i < off[v + 1]; ++i) {
@@ -180,7 +224,6 @@ int64_t crown_reduce_host(int64_t n, const int64_t* off, const int32_t* nbr, int
   for (int32_t v : live)
     if (partner[v] < 0) outside.push_back(v);
   if (outside.empty()) return 0;
-  std::vector<int32_t> left_slot(n, -1);
   std::vector<std::vector<int32_t>> adj(outside.size());
   for (size_t i = 0; i < outside.size(); ++i) {
     int32_t v = outside[i];
@@ -189,8 +232,6 @@ int64_t crown_reduce_host(int64_t n, const int64_t* off, const int32_t* nbr, int
       if (deg[nbr[j]] > 0) adj[i].push_back(nbr[j]);
   }
   // reductions.py:229 _hopcroft_karp
-  std::vector<int32_t> pair_left(n, -1), pair_right(n, -1);
-  std::vector<int> dist(n, kAbsent);
   std::vector<int32_t> touched;
   while (true) {
     for (int32_t t : touched) dist[t] = kAbsent;
@@ -224,7 +265,6 @@ int64_t crown_reduce_host(int64_t n, const int64_t* off, const int32_t* nbr, int
         ++augmented;
     if (augmented == 0) break;
   }
-  std::vector<char> in_crown(n, 0), is_head(n, 0);
   std::vector<int32_t> crown;
   for (int32_t v : outside)
     if (pair_left[v] < 0) {
