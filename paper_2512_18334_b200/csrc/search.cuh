@@ -103,6 +103,12 @@ __device__ inline void reg_free_group(const Registry& R, int p) {
   }
 }
 
+// counter flush that skips zeros (the idle blocks / warps of a small search)
+template <typename U>
+__device__ __forceinline__ void add_nz(U* p, U v) {
+  if (v) atomicAdd(p, v);
+}
+
 struct Ctl {
   int stop, found, timed_out, error;
   int max_depth, pad0, pad1, pad2;

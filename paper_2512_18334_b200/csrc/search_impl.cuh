@@ -723,24 +723,28 @@ struct Worker {
     return true;
   }
 
+  // (zero counters are skipped: an idle block of a small search otherwise
+  // adds ~30 zeros to the same Ctl words as every other block -- 2368 blocks
+  // of a tiny residual's search spent ~50 us queued on them)
   __device__ void flush_stats() {
     if (threadIdx.x != 0) return;
     Ctl* c = P.ctl;
-    atomicAdd(&c->nodes, nodes);
-    atomicAdd(&c->comp_branches, comp_branches);
-    atomicAdd(&c->pushes, pushes);
-    atomicAdd(&c->pops, pops);
-    for (int i = 0; i < 6; ++i) atomicAdd(&c->rules[i], rules[i]);
-    atomicMax(&c->max_depth, max_depth);
-    atomicAdd(&c->rec_in, rec_in);
-    atomicAdd(&c->rec_out, rec_out);
-    for (int i = 0; i < 10; ++i) atomicAdd(&c->phase[i], ph[i]);
-    atomicAdd(&c->wepoch, wep);
+    add_nz(&c->nodes, nodes);
+    add_nz(&c->comp_branches, comp_branches);
+    add_nz(&c->pushes, pushes);
+    add_nz(&c->pops, pops);
+    for (int i = 0; i < 6; ++i) add_nz(&c->rules[i], rules[i]);
+    if (max_depth) atomicMax(&c->max_depth, max_depth);
+    add_nz(&c->rec_in, rec_in);
+    add_nz(&c->rec_out, rec_out);
+    for (int i = 0; i < 10; ++i) add_nz(&c->phase[i], ph[i]);
+    add_nz(&c->wepoch, wep);
     for (int i = 0; i < 4; ++i) {
-      atomicAdd(&c->rcyc[i], w.bs->rcyc[i]);
-      atomicAdd(&c->rcnt[i], w.bs->rcnt[i]);
+      add_nz(&c->rcyc[i], w.bs->rcyc[i]);
+      add_nz(&c->rcnt[i], w.bs->rcnt[i]);
     }
   }
+
 };
 
 // kSmem: the workspace (and, when it fits, the CSR) lives in shared memory;

@@ -1056,18 +1056,18 @@ __device__ inline bool warp_epoch(const SearchParams& P, void* wws_raw, int* bus
 // end of the kernel: lane 0 of every warp adds its counters
 __device__ inline void warp_flush_stats(const SearchParams& P, const WStats& st) {
   if ((threadIdx.x & 31) != 0 || !P.warp_limit) return;
+  if (!st.tasks && !st.nodes) return;  // a warp that never ran a task
   Ctl* c = P.ctl;
-  atomicAdd(&c->nodes, st.nodes);
-  atomicAdd(&c->comp_branches, st.splits);
-  for (int i = 0; i < 6; ++i)
-    if (st.rules[i]) atomicAdd(&c->rules[i], st.rules[i]);
-  atomicAdd(&c->wtasks, st.tasks);
-  atomicAdd(&c->wnodes, st.nodes);
-  atomicAdd(&c->wcyc, st.cyc);
-  atomicAdd(&c->wc_fix, st.c_fix);
-  atomicAdd(&c->wc_comp, st.c_comp);
-  atomicAdd(&c->wc_split, st.c_split);
-  atomicAdd(&c->wc_iter, st.c_iter);
+  add_nz(&c->nodes, st.nodes);
+  add_nz(&c->comp_branches, st.splits);
+  for (int i = 0; i < 6; ++i) add_nz(&c->rules[i], st.rules[i]);
+  add_nz(&c->wtasks, st.tasks);
+  add_nz(&c->wnodes, st.nodes);
+  add_nz(&c->wcyc, st.cyc);
+  add_nz(&c->wc_fix, st.c_fix);
+  add_nz(&c->wc_comp, st.c_comp);
+  add_nz(&c->wc_split, st.c_split);
+  add_nz(&c->wc_iter, st.c_iter);
   if (atomicMax(&c->wmax, st.maxcyc) < st.maxcyc) {
     c->wmax_nodes = st.max_nodes;
     c->wmax_n = st.max_n;
