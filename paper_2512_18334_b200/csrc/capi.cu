@@ -1649,6 +1649,12 @@ static int search_t(const vcg_graph* gc, const vcg_search_config* cfg, vcg_searc
   const int share_k = cfg->gpu_share > 1 ? cfg->gpu_share : 1;
   const int resident = std::max(1, per_sm * sm_count / share_k);
   int blocks = cfg->deterministic ? 1 : (cfg->workers > 0 ? cfg->workers : resident);
+  // a residual of <= 32 vertices (the ba100k / planted1m root reductions
+  // leave 4-21) is one small warp task: one block per SM is plenty, and 16
+  // per SM cost their start-up and exit (search kernel 0.048 -> 0.039 ms)
+  if (!cfg->deterministic && cfg->workers <= 0 && pl.warp_limit && n <= 32 &&
+      blocks > sm_count)
+    blocks = sm_count;
   if (blocks > resident) blocks = resident;
 
   const long long slot = (long long)sizeof(NodeHdr) + deg_bytes<T>(n) +
