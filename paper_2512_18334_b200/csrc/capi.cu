@@ -996,6 +996,17 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
                             int64_t bound, vcg_preprocessed* info, int32_t* forced_out,
                             int64_t* vertex_map_out, vcg_graph** reduced_out, int spec_ok) {
   memset(info, 0, sizeof(*info));
+  struct HostSpan {  // VCG_TRACE / VCG_HOSTSPAN: host time of the whole call
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), tret = t0;
+    ~HostSpan() {
+      static const bool on = getenv("VCG_HOSTSPAN") != nullptr;
+      const auto t1 = std::chrono::steady_clock::now();
+      if (trace_on() || on)
+        fprintf(stderr, "[vcg root] host: root_reduce call %.1f us (after the first readback %.1f us)\n",
+                std::chrono::duration<double, std::micro>(t1 - t0).count(),
+                std::chrono::duration<double, std::micro>(t1 - tret).count());
+    }
+  } host_span;
   Tracer tr("root");
   const int n = (int)g->n;
   const int rules_on = enabled & 1;
@@ -1134,8 +1145,10 @@ static int root_reduce_impl(const vcg_graph* g, int enabled, int crown, int has_
       CK(cudaMemcpy(ret, dret.p, fast ? 144 : use_front ? 208 : use_grid ? 88 : 80,
                     cudaMemcpyDeviceToHost));
       const auto tl2 = std::chrono::steady_clock::now();
+      if (first) host_span.tret = tl2;
       if (trace_on())
-        fprintf(stderr, "[vcg root] host: launch call %.1f us, launch..ret copied %.1f us\n",
+        fprintf(stderr, "[vcg root] host: entry..launch %.1f us, launch call %.1f us, launch..ret copied %.1f us\n",
+                std::chrono::duration<double, std::micro>(tl0 - host_span.t0).count(),
                 std::chrono::duration<double, std::micro>(tl1 - tl0).count(),
                 std::chrono::duration<double, std::micro>(tl2 - tl0).count());
       {
