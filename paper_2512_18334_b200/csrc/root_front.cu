@@ -396,40 +396,70 @@ __device__ __forceinline__ void remove_set(const Ex& E, const Front& F, FrontCtl
   FPROF(tm.lap(G, 9));
 }
 
-// live-neighbour sums of every tracked live vertex (thread per vertex, a
-// warp for adjacencies longer than 32)
+// live-neighbour sums of every tracked live vertex.  Each lane reads its own
+// vertex's flag, degree and adjacency bounds in one round trip; tracked ones
+// with up to 64 entries are then summed by 8-lane groups, four vertices per
+// warp at a time (longer ones by the whole warp, one after another),
+// each lane loading every 8th entry (all loads of a round in flight) and the
+// group reducing with shuffles.  (A whole warp per tracked vertex, one vertex
+// after another, cost two dependent round trips per vertex: 36 of the 57 us
+// init on planted1m.)
 __device__ __forceinline__ void init_sums(const Front& F, const int* off, const int* nbr, int n,
                                           bool all_live) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, T = gridDim.x * blockDim.x;
   for (int base = gt - lane; base < n; base += T) {
     const int v = base + lane;
-    bool lng = false;
-    if (v < n && F.trk[v] && dget(F.deg, v) > 0) {
-      const int b = off[v], e = off[v + 1];
-      if (e - b <= 32) {
-        unsigned long long s1 = 0, s2 = 0;
-        for (int i = b; i < e; ++i) {
+    int b = 0, e = 0;
+    bool tracked = false;
+    if (v < n) {
+      const uint8_t tr = F.trk[v];
+      const int d = dget(F.deg, v);
+      b = __ldg(off + v);
+      e = __ldg(off + v + 1);
+      tracked = tr && d > 0;
+    }
+    const bool hub = tracked && e - b > 64;  // whole-warp path below
+    unsigned m = __ballot_sync(0xffffffffu, tracked && !hub);
+    while (m) {
+      // group grp takes the (grp + 1)-th remaining tracked vertex
+      const unsigned src = __fns(m, 0, grp + 1);
+      const bool act = src < 32u;
+      const int sl = act ? (int)src : 0;
+      const int vb = __shfl_sync(0xffffffffu, b, sl), ve = __shfl_sync(0xffffffffu, e, sl);
+      unsigned long long s1 = 0, s2 = 0;
+      if (act) {
+        int i = vb + sub;
+#pragma unroll 4
+        for (; i < ve; i += 8) {
           const int x = __ldg(nbr + i);
           if (all_live || dget(F.deg, x) > 0) {
             s1 += (unsigned long long)x;
             s2 += (unsigned long long)x * (unsigned long long)x;
           }
         }
-        F.nsum[v] = s1;
-        F.nsq[v] = s2;
-      } else {
-        lng = true;
       }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      }
+      if (act && sub == 0) {
+        F.nsum[base + sl] = s1;
+        F.nsq[base + sl] = s2;
+      }
+      // drop the (up to) four vertices taken this round
+#pragma unroll
+      for (int g = 0; g < 4; ++g) m &= m - 1;
     }
-    unsigned m = __ballot_sync(0xffffffffu, lng);
-    while (m) {
-      const int src = __ffs(m) - 1;
-      m &= m - 1;
-      const int vv = base + src;
+    unsigned h = __ballot_sync(0xffffffffu, hub);  // long adjacencies: a warp each
+    while (h) {
+      const int src = __ffs(h) - 1;
+      h &= h - 1;
+      const int vb = __shfl_sync(0xffffffffu, b, src), ve = __shfl_sync(0xffffffffu, e, src);
       unsigned long long s1 = 0, s2 = 0;
-      const int e = off[vv + 1];
-      for (int i = off[vv] + lane; i < e; i += 32) {
+#pragma unroll 4
+      for (int i = vb + lane; i < ve; i += 32) {
         const int x = __ldg(nbr + i);
         if (all_live || dget(F.deg, x) > 0) {
           s1 += (unsigned long long)x;
@@ -442,8 +472,8 @@ __device__ __forceinline__ void init_sums(const Front& F, const int* off, const 
         s2 += __shfl_xor_sync(0xffffffffu, s2, o);
       }
       if (lane == 0) {
-        F.nsum[vv] = s1;
-        F.nsq[vv] = s2;
+        F.nsum[base + src] = s1;
+        F.nsq[base + src] = s2;
       }
     }
   }
