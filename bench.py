@@ -100,7 +100,41 @@ class ClockSampler:
         self.proc = None
         self.lines = []
 
+    def _nvml_loop(self, nv, h):
+        """NVML every 2 ms (nvidia-smi -lms prints every ~100 ms, so a 15 ms
+        timed region often held no sample); same line format."""
+        R = (nv.nvmlClocksThrottleReasonHwSlowdown, nv.nvmlClocksThrottleReasonHwThermalSlowdown,
+             nv.nvmlClocksThrottleReasonSwThermalSlowdown, nv.nvmlClocksThrottleReasonSwPowerCap)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                util = nv.nvmlDeviceGetUtilizationRates(h).gpu
+            except nv.NVMLError:
+                break
+            self.lines.append(", ".join([str(sm), str(mx)] +
+                                        ["Active" if rs & r else "Not Active" for r in R] +
+                                        [str(util)]))
+            time.sleep(0.002)
+
     def __enter__(self):
+        self.stop = False
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.source = "nvml (2 ms)"
+            self.t = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+            self.t.start()
+            deadline = time.time() + 3.0
+            while len(self.lines) < 2 and time.time() < deadline:
+                time.sleep(0.005)
+            if self.lines:
+                return self
+        except Exception:  # no NVML: nvidia-smi below
+            self.stop = True
+        self.source = "nvidia-smi -lms 20"
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -122,6 +156,7 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.stop = True
         if self.proc:
             self.proc.terminate()
             try:
@@ -161,7 +196,7 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
                 "reasons": sorted(reasons), "samples": len(sm),
-                "samples_in_window": max(0, w1 - w0)}
+                "samples_in_window": max(0, w1 - w0), "source": getattr(self, "source", None)}
 
 
 # ------------------------------------------------------------ reference ----
