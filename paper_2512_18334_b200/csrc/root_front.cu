@@ -185,8 +185,24 @@ __device__ __forceinline__ unsigned long long claim_key(int tg, int v) {
 // Appends to the global lists go through two block-local staging queues in
 // shared memory: one global atomic per block and phase instead of one per
 // entry (the list counters are the kernel's only hot words).
-constexpr int kQ = 2048;
-constexpr int kQC = 1024;  // staged removal chunks (16 B each)
+// The staging queues live in dynamic shared memory (the kernel runs one
+// 512-thread block per SM, so there is room): 8192 appends per list and 4096
+// removal chunks per block.  With the 48 KB static limit (2048 / 1024) the
+// two heavy planted1m sweeps (600 k transitions, 230 k chunks) overflowed
+// into per-entry global appends: 93 / 80 us -> 52 / 56 us, root kernel 0.39 ->
+// 0.32 ms.  Larger queues measured slower (12288 / 6144: 0.43 ms, the L1
+// carve-out shrinks), fewer staged chunks too (8192 / 2048: 0.43 ms).
+#ifndef VCG_FRONT_DYNQ
+#define VCG_FRONT_DYNQ 1
+#endif
+#ifndef VCG_FRONT_KQ
+#define VCG_FRONT_KQ 8192
+#endif
+#ifndef VCG_FRONT_KQC
+#define VCG_FRONT_KQC 4096
+#endif
+constexpr int kQ = VCG_FRONT_KQ;
+constexpr int kQC = VCG_FRONT_KQC;  // staged removal chunks (16 B each)
 struct BlockQ {
   int cnt[2], base[2];
   int buf[2][kQ];
@@ -771,7 +787,12 @@ __global__ void __launch_bounds__(kRootGridThreads, 1)
                  int budget, int32_t* out, long long* ret, int init, void* ctl_mem,
                  int solo_max) {
   __shared__ BlockScratch bs;
+#if VCG_FRONT_DYNQ
+  extern __shared__ __align__(16) unsigned char qmem[];  // the staging queues (dynamic)
+  BlockQ& q = *(BlockQ*)qmem;
+#else
   __shared__ BlockQ q;
+#endif
   const unsigned long long t_start = globaltimer();
   if (threadIdx.x == 0) q.cnt[0] = q.cnt[1] = q.ccnt = q.cused = 0;
   init_block_scratch(&bs);
@@ -1003,7 +1024,12 @@ int root_front_blocks() {
   if (dev != dev_cached) {
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_root_front, kRootGridThreads, 0);
+#if VCG_FRONT_DYNQ
+    cudaFuncSetAttribute((const void*)k_root_front, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(BlockQ));
+#endif
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_root_front, kRootGridThreads,
+                                                  VCG_FRONT_DYNQ ? sizeof(BlockQ) : 0);
     per_sm = per_sm > 2 ? 2 : per_sm;
     blocks = sms * per_sm;
     if (blocks > kRootGridMaxBlocks) blocks = kRootGridMaxBlocks;
@@ -1024,7 +1050,8 @@ cudaError_t root_front_launch(int n, const int32_t* off, const int32_t* nbr, cha
   int solo_max = solo_env >= 0 ? solo_env : kSolo;
   void* args[] = {&n, &off, &nbr, &ws, &front, &budget, &out, &ret, &init, &ctl, &solo_max};
   return cudaLaunchCooperativeKernel((const void*)k_root_front, dim3(blocks),
-                                     dim3(kRootGridThreads), args, 0, cudaStreamPerThread);
+                                     dim3(kRootGridThreads), args,
+                                     VCG_FRONT_DYNQ ? sizeof(BlockQ) : 0, cudaStreamPerThread);
 }
 
 }  // namespace vcg
