@@ -328,29 +328,32 @@ __device__ __forceinline__ void live_short(const Front& F, const int* off, const
 }
 
 // one removal work item: the entries [b, min(b + kChunk, end(u))) of removed
-// vertex u.  Non-member live neighbours lose a degree and u from their sums;
-// 2 -> 1 and 3 -> 2 transitions are pushed to the pending lists.  The degree
-// decrement is issued with the removal-tag load, not after a degree read: a
-// dead neighbour's word goes negative (harmless, readers clamp) and the
-// atomic's old value says whether the neighbour was live -- one dependent
-// round trip less per chunk.  A neighbour in the same removal set is told
-// apart by its tag (its word is zeroed by remove_set either way).
+// vertex u.  Live neighbours lose a degree and (tracked ones) u from their
+// sums; 2 -> 1 and 3 -> 2 transitions are pushed to the pending lists.  The
+// decrement is issued without a prior degree read: a dead neighbour's word
+// goes negative (harmless, readers clamp) and the atomic's old value says
+// whether the neighbour was live.  A neighbour in the same removal set is
+// decremented and pushed like a live one -- its word is zeroed by
+// remove_set either way and the next sweep drops it by its degree -- so no
+// removal-tag load: two L2 requests per entry instead of three (the heavy
+// sweeps are L2-request bound).  The solve path does not count removed
+// edges (the reduced graph's size comes from the compaction).
 __device__ __forceinline__ void rm_chunk(const Front& F, FrontCtl* G, BlockQ* q,
                                          const int* nbr, int s, int p1, int p2, int u, int b,
                                          int e, long long* edges) {
+  (void)s;
+  (void)edges;
   const int len = e - b;
-  int x[kChunk], r[kChunk];
+  int x[kChunk];
   unsigned old[kChunk];
   uint8_t tr[kChunk];
 #pragma unroll
   for (int j = 0; j < kChunk; ++j) x[j] = j < len ? __ldg(nbr + b + j) : -1;
 #pragma unroll
   for (int j = 0; j < kChunk; ++j) {
-    r[j] = 0;
     tr[j] = 0;
     old[j] = 0;
     if (x[j] >= 0) {
-      r[j] = __ldcg(F.rs + x[j]);
       tr[j] = __ldg(F.trk + x[j]);
       old[j] = atomicSub(F.deg + x[j], 1u);
     }
@@ -358,16 +361,9 @@ __device__ __forceinline__ void rm_chunk(const Front& F, FrontCtl* G, BlockQ* q,
   const unsigned long long uu = (unsigned long long)u;
 #pragma unroll
   for (int j = 0; j < kChunk; ++j) {
-    if (x[j] < 0) continue;
-    if (r[j] == s) {
-      if (x[j] > u) ++*edges;  // both ends removed together: counted once
-      old[j] = 0;
-    } else if ((int)old[j] > 0) {
-      if (tr[j]) {  // tracked neighbour: u leaves its sums
-        atomicAdd(F.nsum + x[j], 0ull - uu);
-        atomicAdd(F.nsq + x[j], 0ull - uu * uu);
-      }
-      ++*edges;
+    if (tr[j] && (int)old[j] > 0) {  // tracked live neighbour: u leaves its sums
+      atomicAdd(F.nsum + x[j], 0ull - uu);
+      atomicAdd(F.nsq + x[j], 0ull - uu * uu);
     }
   }
 #pragma unroll
@@ -546,11 +542,10 @@ __device__ __forceinline__ void sweep_d1(const Ex& E, const Front& F, FrontCtl* 
     const int v = L[k];
     const int d = dget(F.deg, v);
     const uint8_t tr = __ldg(F.trk + v);
-    const unsigned long long s1 = __ldcg(F.nsum + v);
     const int o0 = __ldg(off + v), o1 = __ldg(off + v + 1);
     if (d != 1) continue;
     int u, u2;
-    if (tr) u = (int)s1;
+    if (tr) u = (int)__ldcg(F.nsum + v);  // tracked candidates only (L2 requests)
     else live_short_at(F, nbr, o0, o1 - o0, &u, &u2);
     if (u < 0 || u >= F.n) {  // inconsistent degree array: report, never loop
       atomicExch(&G->err, 1);
@@ -969,7 +964,7 @@ __global__ void __launch_bounds__(kRootGridThreads, 1)
     ret[1] = S.d1;
     ret[2] = S.d2t;
     ret[3] = S.hd;
-    ret[4] = (long long)*(volatile unsigned long long*)&G->edges;
+    ret[4] = -1;  // removed edges are not counted on the solve path (rm_chunk); unused
     if (hi < 0) {  // pure.py:238 empty window
       ret[5] = n > 1 ? n : 1;
       ret[6] = 0;
