@@ -170,13 +170,24 @@ __device__ __forceinline__ int vld(const int* p) { return *(const volatile int*)
 __device__ __forceinline__ int cld(const void* G, const int* p) {
   return hdr_cache()[p - (const int*)G];
 }
-// Degrees are decremented speculatively (rm_chunk), so a dead vertex's word
-// may have gone below zero: every reader clamps, sweep_hd and the final pass
-// store the zeros back.
-__device__ __forceinline__ int dget(const uint32_t* d, int v) {
-  const int x = (int)__ldcg(d + v);
-  return x > 0 ? x : 0;
+// Degree words.  Bit 30 flags a tracked vertex (adjacency > kTrack), so a
+// removal's decrement returns the flag with the old degree (one L2 request
+// per adjacency entry); the low 30 bits hold the live degree, or, once the
+// vertex is dead, kDead -- decremented speculatively by later removals
+// (rm_chunk) but never below kDeadMin, so "dead" is low bits >= kDeadMin.
+// sweep_hd decodes the array for the block-level high-degree pass (and
+// re-encodes it after); the final pass leaves plain degrees for the host
+// and the next launch.
+constexpr uint32_t kTrkBit = 1u << 30, kLowMask = kTrkBit - 1u;
+constexpr uint32_t kDead = 1u << 29, kDeadMin = 1u << 28;
+__device__ __forceinline__ int dval(uint32_t w) {
+  const uint32_t x = w & kLowMask;
+  return x >= kDeadMin ? 0 : (int)x;
 }
+__device__ __forceinline__ uint32_t denc(int d, bool trk) {
+  return (trk ? kTrkBit : 0u) | (d > 0 ? (uint32_t)d : kDead);
+}
+__device__ __forceinline__ int dget(const uint32_t* d, int v) { return dval(__ldcg(d + v)); }
 
 __device__ __forceinline__ unsigned long long claim_key(int tg, int v) {
   return ((unsigned long long)(unsigned)tg << 32) | (unsigned long long)(unsigned)(kInf - v);
@@ -350,18 +361,13 @@ __device__ __forceinline__ void rm_chunk(const Front& F, FrontCtl* G, BlockQ* q,
 #pragma unroll
   for (int j = 0; j < kChunk; ++j) x[j] = j < len ? __ldg(nbr + b + j) : -1;
 #pragma unroll
-  for (int j = 0; j < kChunk; ++j) {
-    tr[j] = 0;
-    old[j] = 0;
-    if (x[j] >= 0) {
-      tr[j] = __ldg(F.trk + x[j]);
-      old[j] = atomicSub(F.deg + x[j], 1u);
-    }
-  }
+  for (int j = 0; j < kChunk; ++j) old[j] = x[j] >= 0 ? atomicSub(F.deg + x[j], 1u) : 0u;
   const unsigned long long uu = (unsigned long long)u;
 #pragma unroll
   for (int j = 0; j < kChunk; ++j) {
-    if (tr[j] && (int)old[j] > 0) {  // tracked live neighbour: u leaves its sums
+    tr[j] = (old[j] & kTrkBit) != 0;
+    old[j] = (unsigned)dval(old[j]);  // the neighbour's degree before (0: dead)
+    if (tr[j] && old[j] > 0u) {  // tracked live neighbour: u leaves its sums
       atomicAdd(F.nsum + x[j], 0ull - uu);
       atomicAdd(F.nsq + x[j], 0ull - uu * uu);
     }
@@ -396,7 +402,7 @@ __device__ __forceinline__ void remove_set(const Ex& E, const Front& F, FrontCtl
   FPROF(tm.lap(G, 6));
   for (int k = E.rank; k < nrem; k += E.size) {  // independent of the chunks: issued first
     const int u = F.rem[k];
-    F.deg[u] = 0;
+    F.deg[u] = kDead;
     F.forced[u] = 1;
   }
   for (int c = E.rank; c < nch; c += E.size) {
@@ -540,8 +546,9 @@ __device__ __forceinline__ void sweep_d1(const Ex& E, const Front& F, FrontCtl* 
   // round trip (degree, tracked flag, id sum, adjacency bounds).
   for (int k = E.rank; k < ncur; k += E.size) {
     const int v = L[k];
-    const int d = dget(F.deg, v);
-    const uint8_t tr = __ldg(F.trk + v);
+    const uint32_t wv = __ldcg(F.deg + v);  // degree and tracked flag, one request
+    const int d = dval(wv);
+    const bool tr = (wv & kTrkBit) != 0;
     const int o0 = __ldg(off + v), o1 = __ldg(off + v + 1);
     if (d != 1) continue;
     int u, u2;
@@ -711,9 +718,7 @@ __device__ __forceinline__ void sweep_hd(const Front& F, FrontCtl* G, BlockQ* q,
   if (gt == 0) next_slots(G, s);
   int ch = 0, dm = 0;
   for (int v = gt; v < n; v += T) {
-    const int raw = (int)__ldcg(F.deg + v);
-    if (raw < 0) F.deg[v] = 0;  // dead below zero (rm_chunk): the block-level sweep reads raw
-    const int d = raw > 0 ? raw : 0;
+    const int d = dget(F.deg, v);
     ch += (d > 0 && d > bud);
     dm = d > dm ? d : dm;
   }
@@ -732,6 +737,9 @@ __device__ __forceinline__ void sweep_hd(const Front& F, FrontCtl* G, BlockQ* q,
   if (bud > kSpecBudget / 2) S.spec_m = max(S.spec_m, DM + S.forced);
   int applied = 0;
   if (CH > 0) {
+    // the block-level pass reads plain degrees: decode, then re-encode below
+    for (int v = gt; v < n; v += T) F.deg[v] = (uint32_t)dget(F.deg, v);
+    grid_barrier(&G->bar, (const int*)G);
     if (blockIdx.x == 0) {
       NodeWs<uint32_t> w = carve_ws<uint32_t>(wsmem, n, bs, off, nbr);
       PassRet h = high_degree_pass(w, 0, n - 1, bud, hd_out, 0);
@@ -743,6 +751,8 @@ __device__ __forceinline__ void sweep_hd(const Front& F, FrontCtl* G, BlockQ* q,
         G->cnt2[S.p2] = 0;
       }
     }
+    grid_barrier(&G->bar, (const int*)G);
+    for (int v = gt; v < n; v += T) F.deg[v] = denc((int)__ldcg(F.deg + v), F.trk[v] != 0);
     grid_barrier(&G->bar, (const int*)G);
     applied = cld(G, &G->hd_applied);
     if (applied > 0) {
@@ -821,12 +831,13 @@ __global__ void __launch_bounds__(kRootGridThreads, 1)
   const bool real_budget = budget <= kSpecBudget / 2;
   // init: degrees, tags, the first frontier (every degree-1 / degree-2 vertex)
   for (int v = gt; v < n; v += T) {
-    const int d = init ? off[v + 1] - off[v] : (int)F.deg[v];
-    if (init) F.deg[v] = (uint32_t)d;
+    const int len = off[v + 1] - off[v];
+    const int d = init ? len : (int)F.deg[v];
+    F.deg[v] = denc(d, len > kTrack);
     F.key[v] = 0ull;
     F.rs[v] = 0;
     F.forced[v] = 0;
-    F.trk[v] = off[v + 1] - off[v] > kTrack;
+    F.trk[v] = len > kTrack;
     if (d == 1) qpush(&q, 0, F.l1[0], &G->cnt1[0], v);
     else if (d == 2) qpush(&q, 1, F.l2[0], &G->cnt2[0], v);
   }
@@ -905,9 +916,10 @@ __global__ void __launch_bounds__(kRootGridThreads, 1)
   int cnt = 0, mn = kInf, mx = -1;
   for (int v = b; v < e; ++v) {
     cnt += F.forced[v];
-    const int raw = (int)__ldcg(F.deg + v);
-    if (raw < 0) F.deg[v] = 0;  // the host and the next launch read the array raw
-    if (raw > 0) {
+    const uint32_t w = __ldcg(F.deg + v);
+    const int dv = dval(w);
+    if (w != (uint32_t)dv) F.deg[v] = (uint32_t)dv;  // plain degrees for the host / next launch
+    if (dv > 0) {
       mn = min(mn, v);
       mx = v;
     }

@@ -1,4 +1,4 @@
-"""Frontier root kernel (VCG_ROOT_GRID=2) against the oracle's root reduction
+"""Frontier root kernel (VCG_ROOT_GRID=2; BOUNDED=1 for real budgets) against the oracle's root reduction
 on many random shapes: forced set, rule counts, vertex map, reduced CSR.
 Prints the mismatches and a total (race hunting for the speculative
 decrements and the one-phase degree-one decisions)."""
@@ -39,8 +39,11 @@ while time.time() - t0 < budget:
         e |= {(i, i + 2) for i in range(0, n - 2, rng.randint(2, 7))}
     edges = sorted((min(a, b), max(a, b)) for a, b in e if a != b)
     nn, off, nbr = csr(n, edges)
-    want = oracle.root_reduce(nn, off, nbr)
-    pre = vc.root_reduce(vc.StaticGraph(nn, off, nbr), ordered=False)
+    # BOUNDED=1: a real budget (the high-degree rule fires: the kernel's
+    # block-level pass between its decode / re-encode of the degree words)
+    bound = rng.randint(1, max(1, n // 8)) if os.environ.get("BOUNDED") else None
+    want = oracle.root_reduce(nn, off, nbr, bound=bound)
+    pre = vc.root_reduce(vc.StaticGraph(nn, off, nbr), ordered=False, bound=bound)
     total += 1
     ok = (pre.kernel["kind"] == "frontier" and pre.forced == sorted(want["forced"])
           and pre.rule_counts == want["rule_counts"]
