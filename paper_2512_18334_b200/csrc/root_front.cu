@@ -70,7 +70,10 @@ constexpr int kSolo = 0;     // default: frontier size below which block 0 sweep
 #define VCG_FRONT_CHUNK 4  // 4 vs 8 vs 16 vs 2: ba100k 0.85 / 0.90 / 0.97 / 0.99 ms
 #endif
 constexpr int kChunk = VCG_FRONT_CHUNK;  // adjacency entries per removal work item
-constexpr int kTrack = 12;   // adjacencies longer than this keep live-neighbour id sums
+#ifndef VCG_FRONT_TRACK
+#define VCG_FRONT_TRACK 8  // 8 vs 12 vs 20: planted1m 0.274 / 0.283 / 0.279 ms
+#endif
+constexpr int kTrack = VCG_FRONT_TRACK;  // adjacencies longer than this keep live-neighbour id sums
 
 enum Phase { F_D1 = 0, F_TRI = 1, F_HD = 2, F_DONE = 3 };
 constexpr int kLog = 96;
