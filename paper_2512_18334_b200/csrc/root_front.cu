@@ -209,6 +209,9 @@ __device__ __forceinline__ unsigned long long claim_key(int tg, int v) {
 // into per-entry global appends: 93 / 80 us -> 52 / 56 us, root kernel 0.39 ->
 // 0.32 ms.  Larger queues measured slower (12288 / 6144: 0.43 ms, the L1
 // carve-out shrinks), fewer staged chunks too (8192 / 2048: 0.43 ms).
+#ifndef VCG_FRONT_THREADS  // block size of the frontier kernel (one block per SM)
+#define VCG_FRONT_THREADS kRootGridThreads
+#endif
 #ifndef VCG_FRONT_DYNQ
 #define VCG_FRONT_DYNQ 1
 #endif
@@ -793,7 +796,13 @@ __device__ __forceinline__ void sweep_hd(const Front& F, FrontCtl* G, BlockQ* q,
 
 }  // namespace
 
-__global__ void __launch_bounds__(kRootGridThreads, 1)
+// One block per SM; 512 threads, or 1024 on graphs of >= kFrontBigN vertices
+// (their heavy sweeps are L2-request bound and want more requests in
+// flight: planted1m 0.276 -> 0.262 ms; the long cascades of smaller graphs
+// want cheaper barriers: ba100k 0.83 ms at 512, 0.86 at 1024, 0.90 at 768).
+constexpr int kFrontBigN = 1 << 19;
+template <int TH>
+__global__ void __launch_bounds__(TH, 1)
     k_root_front(int n, const int32_t* off, const int32_t* nbr, char* wsmem, char* fmem,
                  int budget, int32_t* out, long long* ret, int init, void* ctl_mem,
                  int solo_max) {
@@ -1030,7 +1039,8 @@ size_t root_front_bytes(int n, long long m2) {
   return 24 * nn + 40 * nn + 2 * nn + 16 * ((size_t)n + (size_t)m2 / kChunk + 1) + 256;
 }
 
-int root_front_blocks() {
+template <int TH>
+static int front_blocks() {
   static thread_local int dev_cached = -1, blocks = 0;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
@@ -1038,10 +1048,10 @@ int root_front_blocks() {
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
 #if VCG_FRONT_DYNQ
-    cudaFuncSetAttribute((const void*)k_root_front, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(BlockQ));
+    cudaFuncSetAttribute((const void*)k_root_front<TH>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BlockQ));
 #endif
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_root_front, kRootGridThreads,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_root_front<TH>, TH,
                                                   VCG_FRONT_DYNQ ? sizeof(BlockQ) : 0);
     per_sm = per_sm > 2 ? 2 : per_sm;
     blocks = sms * per_sm;
@@ -1051,10 +1061,16 @@ int root_front_blocks() {
   return blocks;
 }
 
+int root_front_blocks() { return front_blocks<VCG_FRONT_THREADS>(); }
+
 cudaError_t root_front_launch(int n, const int32_t* off, const int32_t* nbr, char* ws,
                               char* front, int budget, int32_t* out, long long* ret, int init,
                               void* ctl) {
-  const int blocks = root_front_blocks();
+  // VCG_FRONT_BIGBLOCK / VCG_FRONT_SMALLBLOCK force a variant (tests, A/B)
+  const bool force_big = getenv("VCG_FRONT_BIGBLOCK") != nullptr;  // read per call (tests)
+  const bool force_small = getenv("VCG_FRONT_SMALLBLOCK") != nullptr;
+  const bool big = (n >= kFrontBigN || force_big) && !force_small;
+  const int blocks = big ? front_blocks<1024>() : front_blocks<VCG_FRONT_THREADS>();
   if (blocks < 1) return cudaErrorInvalidConfiguration;
   cudaError_t e = cudaMemsetAsync(ctl, 0, sizeof(FrontCtl), cudaStreamPerThread);
   if (e != cudaSuccess) return e;
@@ -1062,8 +1078,8 @@ cudaError_t root_front_launch(int n, const int32_t* off, const int32_t* nbr, cha
   static const int solo_env = getenv("VCG_FRONT_SOLO") ? atoi(getenv("VCG_FRONT_SOLO")) : -1;
   int solo_max = solo_env >= 0 ? solo_env : kSolo;
   void* args[] = {&n, &off, &nbr, &ws, &front, &budget, &out, &ret, &init, &ctl, &solo_max};
-  return cudaLaunchCooperativeKernel((const void*)k_root_front, dim3(blocks),
-                                     dim3(kRootGridThreads), args,
+  const void* kern = big ? (const void*)k_root_front<1024> : (const void*)k_root_front<VCG_FRONT_THREADS>;
+  return cudaLaunchCooperativeKernel(kern, dim3(blocks), dim3(big ? 1024 : VCG_FRONT_THREADS), args,
                                      VCG_FRONT_DYNQ ? sizeof(BlockQ) : 0, cudaStreamPerThread);
 }
 

@@ -246,3 +246,26 @@ def test_front_root_reduce_families(front_root):
         assert pre.vertex_map.tolist() == want["vertex_map"], name
         assert pre.graph.offsets.tolist() == want["offsets"].tolist(), name
         assert pre.graph.neighbors.tolist() == want["neighbors"].tolist(), name
+
+
+def test_front_root_reduce_1024_thread_variant(front_root, monkeypatch):
+    """The 1024-thread frontier kernel (graphs of >= 2^19 vertices; forced
+    here with VCG_FRONT_BIGBLOCK) on every reference fixture and the
+    adversarial families."""
+    import oracle
+    import paper_2512_18334_b200 as vc
+
+    monkeypatch.setenv("VCG_FRONT_BIGBLOCK", "1")
+    for case in golden("root_reduce.json"):
+        g = _graph(case)
+        pre = vc.root_reduce(g, bound=case["bound"], ordered=False)
+        assert pre.forced == sorted(case["forced"]), case.get("name")
+        assert pre.rule_counts == case["rule_counts"]
+        assert pre.vertex_map.tolist() == case["vertex_map"]
+    for name, n, edges in _families():
+        nn, off, nbr = csr(n, edges)
+        want = oracle.root_reduce(nn, off, nbr)
+        pre = vc.root_reduce(vc.StaticGraph(nn, off, nbr), ordered=False)
+        assert pre.forced == sorted(want["forced"]), name
+        assert pre.rule_counts == want["rule_counts"], name
+        assert pre.vertex_map.tolist() == want["vertex_map"], name
