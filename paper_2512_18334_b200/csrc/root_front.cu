@@ -240,6 +240,7 @@ __device__ __forceinline__ void qpush(BlockQ* q, int which, int* list, int* gcnt
 __device__ __forceinline__ void qflush(BlockQ* q, int* list0, int* cnt0, int* list1, int* cnt1) {
   __syncthreads();
   const int c0 = min(q->cnt[0], kQ), c1 = min(q->cnt[1], kQ);
+  if (c0 == 0 && c1 == 0) return;  // nothing staged (block-uniform): no more barriers
   if (threadIdx.x == 0) {
     q->base[0] = c0 ? atomicAdd(cnt0, c0) : 0;
     q->base[1] = c1 ? atomicAdd(cnt1, c1) : 0;
@@ -296,6 +297,13 @@ __device__ __forceinline__ void add_removed(const Front& F, FrontCtl* G, BlockQ*
 __device__ __forceinline__ void rflush(BlockQ* q, int* rem, int* nrem, int4* chunks, int* nch) {
   __syncthreads();
   const int c0 = min(q->cnt[0], kQ), c = q->cused;
+  if (c0 == 0 && c == 0) {  // nothing staged (block-uniform): no more barriers
+    if (q->ccnt) {  // chunk reservations that overflowed: reset after every thread read
+      __syncthreads();
+      if (threadIdx.x == 0) q->ccnt = 0;
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     q->base[0] = c0 ? atomicAdd(nrem, c0) : 0;
     q->cbase = c ? atomicAdd(nch, c) : 0;
