@@ -91,7 +91,7 @@ struct FrontCtl {
   int err, hd_applied, wlo, whi;  // wlo = max(INT_MAX - lowest live), whi = max(highest live + 1)
   unsigned long long edges, walked, items;
   unsigned bar, nbar;                         // grid_barrier word, barriers passed
-  unsigned long long tph[16];                 // phase times (ns, thread 0): A, B, C, barriers, sub-phases
+  unsigned long long tph[24];                 // phase times (ns, thread 0): A, B, C, barriers, sub-phases
   St st;                                      // block 0 -> grid after a solo segment
   int nlog;                                   // per-sweep log (trace builds read it)
   long long slog[kLog][5];                    // phase, end ns, frontier, removed, chunks
@@ -864,7 +864,9 @@ __global__ void __launch_bounds__(TH, 1)
     if (d == 1) qpush(&q, 0, F.l1[0], &G->cnt1[0], v);
     else if (d == 2) qpush(&q, 1, F.l2[0], &G->cnt2[0], v);
   }
+  FPROF(Timer ti(gt == 0); ti.t = gt == 0 ? t_start : 0; ti.lap(G, 16));
   qflush(&q, F.l1[0], &G->cnt1[0], F.l2[0], &G->cnt2[0]);
+  FPROF(ti.lap(G, 17));
   if (real_budget) {  // scratch of the block-level high-degree sweep
     NodeWs<uint32_t> w = carve_ws<uint32_t>(wsmem, n, &bs, off, nbr);
     for (int v = gt; v < n; v += T) {
@@ -873,8 +875,11 @@ __global__ void __launch_bounds__(TH, 1)
     }
   }
   grid_barrier(&G->bar, (const int*)G);  // degrees initialised
+  FPROF(ti.lap(G, 18));
   init_sums(F, off, nbr, n, init != 0);
+  FPROF(ti.lap(G, 19));
   grid_barrier(&G->bar, (const int*)G);
+  FPROF(ti.lap(G, 20));
   if (gt == 0) {
     G->slog[0][0] = 0;
     G->slog[0][1] = (long long)globaltimer();
@@ -1029,6 +1034,9 @@ void root_front_print_log(const void* ctl) {
   FrontCtl h;
   if (cudaMemcpy(&h, ctl, sizeof(FrontCtl), cudaMemcpyDeviceToHost) != cudaSuccess) return;
   static const char* nm[4] = {"init", "d1", "tri", "hd"};
+  if (h.tph[16])  // -DVCG_FRONT_PROF builds
+    fprintf(stderr, "[vcg root]   init us: pass %.1f qflush %.1f barrier %.1f sums %.1f barrier %.1f\n",
+            h.tph[16] * 1e-3, h.tph[17] * 1e-3, h.tph[18] * 1e-3, h.tph[19] * 1e-3, h.tph[20] * 1e-3);
   if (h.tph[7]) fprintf(stderr, "[vcg root]   sub-phases us: C vld %.1f chunks %.1f sync %.1f flush %.1f | B work %.1f sync %.1f qflush %.1f cflush %.1f | pre-A %.1f\n",
           h.tph[6] * 1e-3, h.tph[7] * 1e-3, h.tph[8] * 1e-3, h.tph[9] * 1e-3, h.tph[10] * 1e-3,
           h.tph[11] * 1e-3, h.tph[12] * 1e-3, h.tph[1] * 1e-3, h.tph[13] * 1e-3);
